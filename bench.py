@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 hydro cell-updates/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload sedov] [--impl ours|reference]
+
+A "step" = one full SSP-RK3 time step (3 fused reconstruct+KT-flux+update
+stages = the reference's 3 hydro rounds, workload.hpp:116) over every
+sub-grid, halo exchange and the dt max-reduction included.  cell-updates/s =
+total_cells * steps / seconds (workload.cpp:608-609).
+
+N=1 workload: BASELINE configs[1], Sedov–Taylor on 16^3 = 4096 sub-grids
+(128^3 cells, nf = 6, FP64).  N>1: weak scaling, 4096 sub-grids per GPU
+(domain 16 x 16 x 16N sub-grids, one contiguous Morton chunk = one z-slab per
+rank) with cross-GPU halos over NCCL.  `--workload polytrope` runs configs[2]
+(32^3 sub-grids per GPU, 5 species, nf = 11).
+
+`--impl reference` times the CPU path of the reference's algorithm (the
+oracle port in oracle/, all host threads; the reference itself ships no hydro
+arithmetic) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (sub-grids per GPU edge, n_species, problem)
+    "sedov": (16, 0, "sedov"),
+    "polytrope": (32, 5, "polytrope"),
+    "random": (16, 0, "random_device"),
+    "random11": (32, 5, "random_device"),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0):
+    """The oracle (CPU restatement of the path) on a bounded sample: an 8^3
+    sub-grid piece of the same workload, all host threads."""
+    import oracle
+    oracle.build()
+    edge, species, problem = WORKLOADS[workload]
+    nf = 6 + species
+    dx = 1.0 / (edge * 8)
+    n = 8
+    p = oracle.params(nf=nf, dx=dx)
+    nbr, pos, _ = oracle.uniform_mesh(n, n, n)
+    from paper_2210_06437_b200 import hydro as H
+    mesh = H.Mesh(nbr, pos, np.zeros(len(pos), np.int32), 1, (n, n, n))
+    prob = "random" if problem == "random_device" else problem
+    U = H.ic_fill(H.HydroConfig(dx=dx, n_species=species), prob, mesh, np.arange(mesh.n))
+    threads = os.cpu_count() or 1
+    for _ in range(warmup):
+        U, _ = oracle.run(p, nbr, U, 1, nthreads=threads)
+    done, t0 = 0, time.perf_counter()
+    while done < steps or (time.perf_counter() - t0) < target_s:
+        U, _ = oracle.run(p, nbr, U, 1, nthreads=threads)
+        done += 1
+        if done >= 200:
+            break
+    sec = time.perf_counter() - t0
+    cells = mesh.n * 512
+    return {"value": cells * done / sec, "unit": "cell-updates/s", "cores": threads, "kind": "port",
+            "sample": f"{n}^3 = {mesh.n} sub-grids of the {workload} workload ({cells} cells), {done} SSP-RK3 steps, "
+                      f"{threads} threads, oracle/hydro_oracle.c", "seconds": sec, "steps": done}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="sedov", choices=sorted(WORKLOADS))
+    ap.add_argument("--recon", default="ppm", choices=["ppm", "minmod"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    a = ap.parse_args(argv)
+    a.warmup = max(a.warmup, 3)
+
+    rank, local_rank, world = dist_env()
+    edge, species, problem = WORKLOADS[a.workload]
+    nf = 6 + species
+    metric = "hydro cell-updates/sec (FP64)"
+    unit = "cell-updates/s"
+    sub_per_gpu = edge ** 3
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        cb = cpu_reference(a.workload, a.steps, a.warmup)
+        line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": a.gpus, "steps": cb["steps"],
+                "warmup": a.warmup, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"{a.workload} (bounded CPU sample)", "recon": a.recon, "nf": nf},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    from paper_2210_06437_b200 import hydro as H
+    H.lib()  # fail loudly without the CUDA library
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    dims = (edge, edge, edge * world)
+    dx = 1.0 / (edge * 8)
+    mesh = H.uniform_mesh(*dims, world=world)
+    cfg = H.HydroConfig(device_id=local_rank, n_species=species, dx=dx, recon=a.recon)
+    dev = H.CudaDevice(cfg)
+    session = H.WorkloadSession(mesh, dev, H.StepConfig(num_steps=a.steps), rank=rank)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dev.comm_init(obj[0], world, rank)
+    session.load_problem(problem)
+    n_owned = dev.local_counts()[0]
+    cells_local = n_owned * 512
+    state_bytes = 3 * (n_owned + dev.local_counts()[1]) * nf * 512 * 8
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up (untimed)
+    dev.compute_dt()
+    dev.step(a.warmup)
+    dev.synchronize()
+    dev.flush_activity()
+    barrier()
+    dev.synchronize()
+    launches0 = dev.launch_count()
+    with ClockSampler(local_rank) as clk:
+        ms = dev.time_steps(a.steps)
+    launches = dev.launch_count() - launches0
+    barrier()
+    recs = [r for r in dev.flush_activity() if r.kind == "kernel" and r.name.startswith("hydro_stage")]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_cells = mesh.n * 512
+    value = total_cells * a.steps / (ms * 1e-3)
+
+    # roofline of the dominant (stage) kernel: algorithmic bytes / kernel time
+    peaks, peak_kind = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    b_alg_step = 64 * nf * cells_local  # 8 nf (3S - 1) per cell-update, S = 3
+    kernel_ns = sum(r.end_ns - r.start_ns for r in recs)
+    n_stage_launches = len(recs)
+    achieved = (b_alg_step * a.steps) / (kernel_ns * 1e-9) / 1e9 if kernel_ns > 0 else None
+    stage_share = kernel_ns * 1e-6 / ms if ms > 0 else None
+
+    # end to end: host buffers through the C ABI, H2D + step + D2H every step
+    e2e = None
+    if not a.no_e2e:
+        nbytes = n_owned * nf * 512 * 8
+        hin = dev.host_pinned_alloc(nbytes)
+        hout = dev.host_pinned_alloc(nbytes)
+        import ctypes
+        U = dev.download()
+        ctypes.memmove(hin, U.ctypes.data, nbytes)
+        dev.step_host(hin, hout, 1)  # warm
+        barrier()
+        k_e2e = max(3, min(a.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            dev.step_host(hin, hout, 1)
+            hin, hout = hout, hin
+        sec = time.perf_counter() - t0
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor([sec], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        e2e = {"value": total_cells * k_e2e / sec, "unit": unit, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": k_e2e,
+               "path": "ts_hydro_step_host: pinned host U^n -> H2D -> dt + 1 step -> D2H"}
+        dev.host_pinned_free(hin)
+        dev.host_pinned_free(hout)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cb = cpu_reference(a.workload, 2, 1, target_s=10.0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{a.workload}: {sub_per_gpu} sub-grids (8^3 + 3-deep halo) per GPU, "
+                                   f"domain {dims[0]}x{dims[1]}x{dims[2]} sub-grids",
+                       "problem": problem, "nf": nf, "recon": a.recon, "total_cells": total_cells,
+                       "parallelism": f"domain decomposition over {world} GPU(s), NCCL halos",
+                       "l2": f"working set {state_bytes / 2**20:.0f} MiB (3 state buffers) > 126 MiB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "peak_source": peak_kind,
+                         "alg_bytes_per_cell_update": 64 * nf,
+                         "kernel": "stage_kernel (fused reconstruct + KT flux + RK update)",
+                         "stage_launches": n_stage_launches, "stage_share_of_step": stage_share},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/*
+ * ts_hydro.h — C ABI of the B200-native hydro hot path (libts_hydro.so).
+ *
+ * Drop-in boundary for the path the reference `taskscope` toolkit only
+ * simulates: `WorkloadSession::fluxes_body` (reference
+ * proj/core/src/workload.cpp:544-552) awaiting `SimDevice::launch_kernel`
+ * (proj/core/include/taskscope/device.hpp:57-58, device.cpp:24-32) for the
+ * `reconstruct_kernel` / `flux_kernel` pair, the ghost exchange around it
+ * (`collect_body`, workload.cpp:519-542) and the per-kernel timing hook
+ * (`ActivityRecord` -> `Profiler::deliver_activity`, snapshot.hpp:88-99,
+ * profiler.cpp:298-318).
+ *
+ * Conventions:
+ *   - every entry point returns TS_OK (0) or a TS_E* code; no exception ever
+ *     crosses the ABI.  TS_EINVAL maps to the reference's std::invalid_argument,
+ *     TS_ESHUTDOWN to its std::runtime_error("device is shut down"); CUDA and
+ *     NCCL failures carry their own text in ts_hydro_last_error();
+ *   - host arrays are borrowed for the duration of the call only;
+ *   - the context owns every device buffer, stream, event and communicator;
+ *   - state arrays are [sub-grid][field][z][y][x] FP64 (x fastest, the
+ *     reference's linear index x + N(y + N z), workload.cpp:353), N = 8;
+ *     fields: rho, sx, sy, sz, E, tau, then n_species passive densities;
+ *   - face order -x,+x,-y,+y,-z,+z, opposite = face ^ 1 (workload.hpp:28-30).
+ *
+ * There is no CPU fallback: every compute entry point runs on the GPU or
+ * fails with TS_ECUDA.
+ */
+#ifndef TS_HYDRO_H
+#define TS_HYDRO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_HYDRO_ABI_VERSION 1
+
+#define TS_OK 0
+#define TS_EINVAL 1     /* reference: std::invalid_argument            */
+#define TS_ESHUTDOWN 2  /* reference: std::runtime_error (device.cpp:62) */
+#define TS_ECUDA 3
+#define TS_ENCCL 4
+#define TS_ENOMEM 5
+#define TS_ESTATE 6     /* call out of order (e.g. stepping before set_mesh) */
+
+#define TS_RECON_PPM 0     /* PPM, MC-limited slopes + CW84 monotonicity (Octo-Tiger form) */
+#define TS_RECON_MINMOD 1  /* piecewise-linear minmod */
+
+/* ActivityKind, reference snapshot.hpp:79-86 */
+#define TS_ACTIVITY_KERNEL 0
+#define TS_ACTIVITY_COPY_H2D 1
+#define TS_ACTIVITY_COPY_D2H 2
+#define TS_ACTIVITY_COPY_D2D 3
+#define TS_ACTIVITY_ALLOC 4
+#define TS_ACTIVITY_FREE 5
+
+/* Initial-condition problems for ts_hydro_ic_fill. */
+#define TS_PROBLEM_SOD 0
+#define TS_PROBLEM_SEDOV 1
+#define TS_PROBLEM_RANDOM 2
+#define TS_PROBLEM_POLYTROPE 3
+#define TS_PROBLEM_BINARY 4
+
+typedef struct ts_hydro_ctx ts_hydro_ctx;
+
+typedef struct ts_hydro_config {
+    int32_t device_id;                 /* DeviceConfig::device_id (device.hpp:23)            */
+    uint32_t stream_count;             /* DeviceConfig::stream_count (device.hpp:24), 128    */
+    uint32_t activity_buffer_capacity; /* DeviceConfig::activity_buffer_capacity (device.hpp:26) */
+    int32_t cells_per_edge;            /* SubGrid::cells_per_edge (workload.hpp:60); must be 8 */
+    int32_t n_species;                 /* passive species; nf = 6 + n_species, 0..5          */
+    int32_t recon;                     /* TS_RECON_*                                          */
+    double gamma;                      /* ideal-gas adiabatic index                           */
+    double cfl;                        /* Courant number                                      */
+    double dx;                         /* cell width (uniform, single level)                  */
+    double p_floor;                    /* pressure floor used by the EOS                      */
+} ts_hydro_config;
+
+/* ActivityRecord (snapshot.hpp:88-99) with RunClock-compatible timestamps:
+ * steady_clock nanoseconds (subtract RunClock::epoch() to get RunClock ns). */
+typedef struct ts_activity_record {
+    uint8_t kind;
+    uint8_t has_bytes;
+    uint16_t reserved;
+    int32_t device_id;
+    int32_t stream_id;
+    int32_t pad;
+    const char* name; /* static taxonomy string, valid for the library's lifetime */
+    uint64_t start_ns;
+    uint64_t end_ns;
+    uint64_t bytes;
+    uint64_t correlation_guid;
+} ts_activity_record;
+
+/* DeviceMemoryState, device.hpp:29-34 */
+typedef struct ts_memory_state {
+    uint64_t current_device_bytes;
+    uint64_t peak_device_bytes;
+    uint64_t current_host_pinned_bytes;
+    uint64_t peak_host_pinned_bytes;
+} ts_memory_state;
+
+/* Completion callback: runs on a CUDA host thread once the launch finished on
+ * the device (never before, device.hpp:54-56).  It must not call CUDA. */
+typedef void (*ts_done_fn)(void* user);
+
+/* Auto-delivery sink for activity records (the SimDevice default sink that
+ * receives records when the buffer reaches capacity, device.cpp:105-111). */
+typedef void (*ts_activity_sink_fn)(const ts_activity_record* records, uint64_t n, void* user);
+
+/* ---- library / context --------------------------------------------------- */
+int ts_hydro_abi_version(void);
+void ts_hydro_default_config(ts_hydro_config* cfg);
+const char* ts_hydro_strerror(int code);
+int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out);
+const char* ts_hydro_last_error(const ts_hydro_ctx* ctx);
+/* SimDevice::shutdown (device.cpp:223-233): waits for in-flight work, later
+ * launches fail with TS_ESHUTDOWN. */
+int ts_hydro_shutdown(ts_hydro_ctx* ctx);
+int ts_hydro_destroy(ts_hydro_ctx* ctx);
+int ts_hydro_num_fields(const ts_hydro_ctx* ctx);
+
+/* ---- mesh (Mesh / SubGrid, workload.hpp:53-97) ---------------------------- */
+/* Product-side uniform mesh builder: nx*ny*nz same-level sub-grids numbered
+ * along the Morton curve, owners dealt in contiguous chunks like build_mesh
+ * (workload.cpp:298-323).  periodic_mask bit d wraps axis d. */
+int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_mask, int32_t world,
+                          int64_t* neighbor_ids, int32_t* pos, int32_t* owner);
+/* Binds the global mesh; validates it like Mesh::validate (workload.cpp:140-168).
+ * This context owns the sub-grids with owner == rank (ascending global id);
+ * foreign neighbours become halo proxies filled by the exchange. */
+int ts_hydro_set_mesh(ts_hydro_ctx* ctx, int64_t n_grids, const int64_t* neighbor_ids,
+                      const int32_t* owner, int32_t world_size, int32_t rank);
+int ts_hydro_local_counts(const ts_hydro_ctx* ctx, int64_t* n_owned, int64_t* n_proxy,
+                          int64_t* n_interior);
+int ts_hydro_owned_ids(const ts_hydro_ctx* ctx, int64_t* global_ids);
+/* Halo plan toward `peer`: number of 3-deep slabs sent, and per slab the
+ * (global sub-grid id, face of that sub-grid) pairs in wire order. */
+int ts_hydro_halo_plan(const ts_hydro_ctx* ctx, int32_t peer, int64_t* n_send, int64_t* send_pairs,
+                       int64_t* n_recv, int64_t* recv_pairs);
+
+/* ---- state ---------------------------------------------------------------- */
+/* Host-side initial conditions for owned sub-grids (the same [g][nf][512]
+ * layout), problems TS_PROBLEM_*; dims = mesh extent in sub-grids. */
+int ts_hydro_ic_fill(const ts_hydro_config* cfg, int32_t problem, int64_t n, const int64_t* global_ids,
+                     const int32_t* pos, const int32_t* dims, uint64_t seed, double* out);
+/* U^n <- host (owned sub-grids [first, first+count) in owned order). */
+int ts_hydro_upload(ts_hydro_ctx* ctx, int64_t first, int64_t count, const double* host);
+int ts_hydro_download(ts_hydro_ctx* ctx, int64_t first, int64_t count, double* host);
+/* Device-side synthetic state (cell_value generator, workload.cpp:329-332). */
+int ts_hydro_init_random(ts_hydro_ctx* ctx, uint64_t seed);
+
+/* ---- stepping -------------------------------------------------------------- */
+/* Max signal speed of U^n (all ranks) -> dt for the next step. */
+int ts_hydro_compute_dt(ts_hydro_ctx* ctx, double* dt_out);
+/* nsteps SSP-RK3 steps (3 stages = the reference's 3 hydro rounds per step,
+ * workload.hpp:116), each stage: halo exchange + fused
+ * reconstruct/flux/update; dt from the cell-centred CFL condition. Async. */
+int ts_hydro_step(ts_hydro_ctx* ctx, uint64_t nsteps);
+/* Host-buffer step (e2e path): U^n from `host_in`, nsteps steps, U^{n+nsteps}
+ * to `host_out` (pinned or pageable), synchronous. */
+int ts_hydro_step_host(ts_hydro_ctx* ctx, const double* host_in, double* host_out, uint64_t nsteps);
+int ts_hydro_synchronize(ts_hydro_ctx* ctx);
+/* nsteps steps bracketed by CUDA events on the compute stream (the stream
+ * every launch of a step is ordered on); blocks and returns device ms. */
+int ts_hydro_time_steps(ts_hydro_ctx* ctx, uint64_t nsteps, double* ms);
+int ts_hydro_last_dt(ts_hydro_ctx* ctx, double* dt);
+int ts_hydro_steps_done(const ts_hydro_ctx* ctx, uint64_t* steps);
+/* Kernel launches issued by this context so far (all kinds). */
+int ts_hydro_launch_count(const ts_hydro_ctx* ctx, uint64_t* launches);
+
+/* The compute_fluxes drop-in (workload.cpp:544-552): one fused RK stage
+ * (1..3) over `count` owned sub-grids on stream `stream_id`; `done` fires once
+ * the device finished.  dt comes from the last ts_hydro_compute_dt. */
+int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned_index, int64_t count,
+                          uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
+/* Rotate buffers after a manual stage-3 sequence. */
+int ts_hydro_finish_step(ts_hydro_ctx* ctx);
+
+/* ---- ghost exchange --------------------------------------------------------- */
+/* The reference's 1-deep face exchange of field 0 (workload.cpp:487-542):
+ * ghost[g][face][j] = neighbour cell face_cell_index(8, face^1, j), 0 where no
+ * neighbour; [n_owned][6][64]. */
+int ts_hydro_exchange_faces(ts_hydro_ctx* ctx, double* ghost_host);
+/* 26-neighbour padded tiles (8+2*depth)^3 of every owned sub-grid, all fields. */
+int ts_hydro_fill_halo(ts_hydro_ctx* ctx, int32_t depth, double* tiles_host);
+/* Cross-GPU halo transport (NCCL, loaded at run time). */
+int ts_hydro_nccl_unique_id(uint8_t id[128]);
+int ts_hydro_comm_init(ts_hydro_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
+/* One packed-halo exchange of U^n (pack -> grouped send/recv -> unpack). */
+int ts_hydro_halo_exchange(ts_hydro_ctx* ctx);
+
+/* ---- timing hook -------------------------------------------------------------- */
+int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void* user);
+/* SimDevice::flush_activity: waits for in-flight work, returns completed
+ * records not yet delivered (at most once).  out == NULL -> count only. */
+int ts_hydro_flush_activity(ts_hydro_ctx* ctx, ts_activity_record* out, uint64_t cap, uint64_t* n_out);
+int ts_hydro_memory_state(const ts_hydro_ctx* ctx, ts_memory_state* out);
+/* SimDevice::host_pinned_alloc / host_pinned_free (device.hpp:63-64), backed
+ * by cudaHostAlloc; counted in ts_memory_state. */
+int ts_hydro_host_alloc(ts_hydro_ctx* ctx, uint64_t bytes, void** ptr);
+int ts_hydro_host_free(ts_hydro_ctx* ctx, void* ptr);
+/* steady_clock ns now (the clock the records are on). */
+uint64_t ts_hydro_clock_ns(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

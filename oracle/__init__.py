@@ -1,0 +1,218 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes front end of ``oracle/liboracle.so`` (the plain-C restatement in
+``hydro_oracle.c``) and, when it was built, of ``oracle/_ref`` (the reference's
+own core compiled from /root/reference).  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs may import this
+package, and only as the checker / CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libtaskscope_ref.so")
+
+N = 8
+NC = 512
+
+_lib = None
+_ref = None
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("nf", ctypes.c_int32),
+        ("recon", ctypes.c_int32),
+        ("gamma", ctypes.c_double),
+        ("cfl", ctypes.c_double),
+        ("dx", ctypes.c_double),
+        ("p_floor", ctypes.c_double),
+    ]
+
+
+def build(force: bool = False) -> None:
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
+
+
+def build_ref() -> bool:
+    """Compile the reference core into oracle/_ref (only where /root/reference exists)."""
+    if not os.path.isdir("/root/reference/proj/core/src"):
+        return os.path.exists(REF_PATH)
+    subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+    return True
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.orc_mix64.restype = ctypes.c_uint64
+        L.orc_mix64.argtypes = [ctypes.c_uint64]
+        L.orc_mix64_2.restype = ctypes.c_uint64
+        L.orc_mix64_2.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        L.orc_cell_value.restype = ctypes.c_double
+        L.orc_cell_value.argtypes = [ctypes.c_uint64] * 3
+        L.orc_face_cell_index.restype = ctypes.c_uint64
+        L.orc_face_cell_index.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
+        L.orc_morton3.restype = ctypes.c_uint64
+        L.orc_morton3.argtypes = [ctypes.c_uint32] * 3
+        L.orc_uniform_mesh.restype = ctypes.c_int
+        L.orc_uniform_mesh.argtypes = [ctypes.c_int] * 7 + [_i64p, _i32p, _i32p]
+        L.orc_exchange_faces.argtypes = [ctypes.c_int, ctypes.c_int64, _i64p, _f64p, _f64p]
+        L.orc_fill_halo.argtypes = [ctypes.c_int, ctypes.c_int64, _i64p, _f64p, ctypes.c_int, _f64p]
+        L.orc_max_signal_speed.restype = ctypes.c_double
+        L.orc_max_signal_speed.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64, _f64p]
+        L.orc_stage.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i64p, _f64p, _f64p, _f64p,
+                                ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_int64]
+        L.orc_run.restype = ctypes.c_int
+        L.orc_run.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i64p, _f64p, ctypes.c_int,
+                              _f64p, ctypes.c_int]
+        L.orc_field_sums.argtypes = [ctypes.c_int, ctypes.c_int64, _f64p, _f64p]
+        L.orc_ic_sod.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i32p, ctypes.c_int, _f64p]
+        L.orc_ic_sedov.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i32p, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, _f64p]
+        L.orc_ic_random.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64,
+                                    ctypes.c_uint64, _f64p]
+        _lib = L
+    return _lib
+
+
+def ref():
+    """The compiled reference (oracle/_ref) or None when it was never built."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_PATH):
+            return None
+        R = ctypes.CDLL(REF_PATH)
+        R.ref_mix64.restype = ctypes.c_uint64
+        R.ref_mix64.argtypes = [ctypes.c_uint64]
+        R.ref_mix64_2.restype = ctypes.c_uint64
+        R.ref_mix64_2.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        R.ref_cell_value.restype = ctypes.c_double
+        R.ref_cell_value.argtypes = [ctypes.c_uint64] * 3
+        R.ref_face_cell_index.restype = ctypes.c_uint64
+        R.ref_face_cell_index.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
+        R.ref_build_mesh.restype = ctypes.c_int64
+        R.ref_build_mesh.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i32p, _i32p, _i32p,
+                                     _i64p, ctypes.c_int64]
+        R.ref_exchange_ghosts.restype = ctypes.c_int
+        R.ref_exchange_ghosts.argtypes = [ctypes.c_int64, _i64p, _i32p, _i32p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_uint64, _f64p, _u64p]
+        R.ref_fill_cells.argtypes = [ctypes.c_int64, ctypes.c_uint64, _f64p]
+        _ref = R
+    return _ref
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def params(nf=6, recon=0, gamma=1.4, cfl=0.4, dx=1.0 / 32, p_floor=1e-12) -> Params:
+    return Params(nf, recon, gamma, cfl, dx, p_floor)
+
+
+def uniform_mesh(nx, ny, nz, periodic=(False, False, False), world=1):
+    n = nx * ny * nz
+    nbr = np.zeros((n, 6), np.int64)
+    pos = np.zeros((n, 3), np.int32)
+    owner = np.zeros(n, np.int32)
+    rc = lib().orc_uniform_mesh(nx, ny, nz, int(periodic[0]), int(periodic[1]), int(periodic[2]), world,
+                                _p(nbr, _i64p), _p(pos, _i32p), _p(owner, _i32p))
+    if rc != 0:
+        raise ValueError("bad mesh dimensions")
+    return nbr, pos, owner
+
+
+def ic_sod(p: Params, pos, axis=0):
+    U = np.zeros((len(pos), p.nf, NC), np.float64)
+    lib().orc_ic_sod(ctypes.byref(p), len(pos), _p(np.ascontiguousarray(pos), _i32p), axis, _p(U, _f64p))
+    return U
+
+
+def ic_sedov(p: Params, pos, dims):
+    U = np.zeros((len(pos), p.nf, NC), np.float64)
+    lib().orc_ic_sedov(ctypes.byref(p), len(pos), _p(np.ascontiguousarray(pos), _i32p), dims[0], dims[1],
+                       dims[2], _p(U, _f64p))
+    return U
+
+
+def ic_random(p: Params, g_begin, g_end, seed=2210):
+    U = np.zeros((g_end - g_begin, p.nf, NC), np.float64)
+    lib().orc_ic_random(ctypes.byref(p), g_begin, g_end, seed, _p(U, _f64p))
+    return U
+
+
+def max_signal_speed(p: Params, U):
+    U = np.ascontiguousarray(U)
+    return lib().orc_max_signal_speed(ctypes.byref(p), 0, U.shape[0], _p(U, _f64p))
+
+
+def stage(p: Params, nbr, Uprev, Un, stage_no, dtdx, g_begin=0, g_end=None):
+    nbr = np.ascontiguousarray(nbr, np.int64)
+    Uprev = np.ascontiguousarray(Uprev)
+    Un = np.ascontiguousarray(Un)
+    out = np.zeros_like(Uprev)
+    if g_end is None:
+        g_end = Uprev.shape[0]
+    lib().orc_stage(ctypes.byref(p), Uprev.shape[0], _p(nbr, _i64p), _p(Uprev, _f64p), _p(Un, _f64p),
+                    _p(out, _f64p), stage_no, dtdx, g_begin, g_end)
+    return out
+
+
+def run(p: Params, nbr, U, nsteps, nthreads=1):
+    """nsteps SSP-RK3 steps; returns (U_new, dt_history)."""
+    nbr = np.ascontiguousarray(nbr, np.int64)
+    U = np.array(U, np.float64, copy=True, order="C")
+    dts = np.zeros(max(nsteps, 1), np.float64)
+    rc = lib().orc_run(ctypes.byref(p), U.shape[0], _p(nbr, _i64p), _p(U, _f64p), nsteps, _p(dts, _f64p),
+                       nthreads)
+    if rc != 0:
+        raise MemoryError("oracle run failed")
+    return U, dts[:nsteps]
+
+
+def field_sums(U):
+    U = np.ascontiguousarray(U)
+    s = np.zeros(U.shape[1], np.float64)
+    lib().orc_field_sums(U.shape[1], U.shape[0], _p(U, _f64p), _p(s, _f64p))
+    return s
+
+
+def exchange_faces(nbr, U):
+    U = np.ascontiguousarray(U)
+    ghost = np.zeros((U.shape[0], 6, N * N), np.float64)
+    lib().orc_exchange_faces(U.shape[1], U.shape[0], _p(np.ascontiguousarray(nbr, np.int64), _i64p),
+                             _p(U, _f64p), _p(ghost, _f64p))
+    return ghost
+
+
+def fill_halo(nbr, U, h=3):
+    U = np.ascontiguousarray(U)
+    pe = N + 2 * h
+    tiles = np.zeros((U.shape[0], U.shape[1], pe, pe, pe), np.float64)
+    lib().orc_fill_halo(U.shape[1], U.shape[0], _p(np.ascontiguousarray(nbr, np.int64), _i64p),
+                        _p(U, _f64p), h, _p(tiles, _f64p))
+    return tiles
+
+
+def to_global(U, pos, dims, field=0):
+    """Assemble field `field` of a [g][nf][512] state into a [z][y][x] array."""
+    nx, ny, nz = dims
+    out = np.zeros((nz * N, ny * N, nx * N), np.float64)
+    for g in range(U.shape[0]):
+        x, y, z = pos[g]
+        out[z * N:(z + 1) * N, y * N:(y + 1) * N, x * N:(x + 1) * N] = U[g, field].reshape(N, N, N)
+    return out

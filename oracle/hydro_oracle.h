@@ -1,0 +1,97 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement (plain C, FP64, scalar) of the hydro hot path that the
+ * B200 kernels in paper_2210_06437_b200/csrc implement.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library, and only as the checker or the CPU baseline — never
+ * as the product path.
+ *
+ * What it restates (see DESIGN.md §2 for the full numerics contract):
+ *   - the reference data model: SubGrid cells x-fastest
+ *     (reference proj/core/src/workload.cpp:353), face order -x,+x,-y,+y,-z,+z
+ *     with opposite = face^1 (workload.hpp:28-30), face_cell_index
+ *     (workload.cpp:340-354), cell_value / mix64 synthetic data
+ *     (workload.cpp:329-332, sampling.hpp:12-21), contiguous Morton-chunk
+ *     ownership (workload.cpp:298-323), 3 hydro rounds per step
+ *     (workload.hpp:116, workload.cpp:559-564);
+ *   - the hydro arithmetic the reference only simulates
+ *     (reconstruct_kernel / flux_kernel, workload.cpp:544-552): PPM with
+ *     minmod-theta (MC) limited slopes and the Colella–Woodward monotonicity
+ *     step in the form Octo-Tiger uses, a minmod-PLM variant,
+ *     the Kurganov–Tadmor central flux, SSP-RK3 (Shu–Osher) and
+ *     a cell-centred CFL time step.
+ *
+ * Parity status: the reference ships no hydro arithmetic (SPEC.md:8, 519,
+ * 528), so the physics is pinned by known-answer tests (exact Sod Riemann
+ * solution, exact conservation, symmetry) and the data-model pieces by golden
+ * vectors generated from the compiled reference (tests/golden/).
+ */
+#ifndef TS_HYDRO_ORACLE_H
+#define TS_HYDRO_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_N 8
+#define ORC_NC 512
+
+typedef struct {
+    int32_t nf;        /* 6 + passive species: rho, sx, sy, sz, E, tau, species... */
+    int32_t recon;     /* 0 = PPM (MC-limited), 1 = minmod PLM */
+    double gamma;
+    double cfl;
+    double dx;
+    double p_floor;
+} orc_params;
+
+/* --- reference data-model restatements (golden-vector pinned) --- */
+uint64_t orc_mix64(uint64_t x);
+uint64_t orc_mix64_2(uint64_t a, uint64_t b);
+double orc_cell_value(uint64_t grid_id, uint64_t step, uint64_t index);
+uint64_t orc_face_cell_index(int edge, int face, uint64_t j);
+uint64_t orc_morton3(uint32_t x, uint32_t y, uint32_t z);
+
+/* Uniform single-level mesh of nx*ny*nz sub-grids numbered along the Morton
+ * curve; neighbours [g][6] (-1 = domain boundary -> outflow), positions
+ * [g][3], owner [g] dealt in contiguous chunks over `world` ranks. */
+int orc_uniform_mesh(int nx, int ny, int nz, int periodic_x, int periodic_y, int periodic_z,
+                     int world, int64_t* nbr, int32_t* pos, int32_t* owner);
+
+/* Reference 1-deep face exchange of a scalar field (field 0 of U):
+ * ghost[g][face][j] = U[nbr][face_cell_index(8, face^1, j)] or 0 if absent. */
+void orc_exchange_faces(int nf, int64_t ngrids, const int64_t* nbr, const double* U, double* ghost);
+
+/* Padded (N+2H)^3 tile per sub-grid and field, 26-neighbour halo of depth h. */
+void orc_fill_halo(int nf, int64_t ngrids, const int64_t* nbr, const double* U, int h, double* tiles);
+
+/* --- hydro --- */
+double orc_max_signal_speed(const orc_params* p, int64_t g_begin, int64_t g_end, const double* U);
+
+/* One SSP-RK3 stage (1, 2 or 3) for sub-grids [g_begin, g_end). */
+void orc_stage(const orc_params* p, int64_t ngrids, const int64_t* nbr, const double* Uprev,
+               const double* Un, double* Uout, int stage, double dtdx, int64_t g_begin,
+               int64_t g_end);
+
+/* nsteps full steps in place on U; dt of every step into dt_hist (may be 0).
+ * nthreads > 1 splits every stage over pthreads by sub-grid range. */
+int orc_run(const orc_params* p, int64_t ngrids, const int64_t* nbr, double* U, int nsteps,
+            double* dt_hist, int nthreads);
+
+/* Sums of every field over all cells (fixed order) for conservation checks. */
+void orc_field_sums(int nf, int64_t ngrids, const double* U, double* sums);
+
+/* --- initial conditions (cell-centred, domain [0, nx*8*dx) x ...) --- */
+void orc_ic_sod(const orc_params* p, int64_t ngrids, const int32_t* pos, int axis, double* U);
+void orc_ic_sedov(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz,
+                  double* U);
+void orc_ic_random(const orc_params* p, int64_t g_begin, int64_t g_end, uint64_t seed, double* U);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,6 @@
+// Fused stage kernel instantiations for nf = 8 fields (see hydro_stage.cuh).
+#include "hydro_stage.cuh"
+
+namespace tsh {
+template cudaError_t launch_stage_n<8>(const StageArgs&, int, int, int, cudaStream_t);
+}  // namespace tsh

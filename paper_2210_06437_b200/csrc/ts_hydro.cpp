@@ -1,0 +1,1355 @@
+// ts_hydro.cpp — host side of libts_hydro.so: the C ABI of include/ts_hydro.h.
+//
+// One context = one GPU = one locality of the reference's World
+// (distrib.hpp:112-203).  The context owns:
+//   - three state buffers A (U^n), B (U^(1)), C (U^(2)) laid out
+//     [local sub-grid][field][512]; SSP-RK3 runs A->B, (B,A)->C, (C,A)->A so
+//     U^n never moves;
+//   - the local mesh: owned sub-grids (ascending global id) then halo proxies
+//     of foreign face neighbours; an interior list (no foreign neighbour) and
+//     a boundary list;
+//   - per-peer packed-halo plans and an NCCL communicator (dlopen'ed);
+//   - a ring of per-launch [start,end] globaltimer stamps written by the
+//     kernels themselves — the per-kernel timing hook that stands in for the
+//     reference's ActivityRecord feed (device.cpp:75-103, profiler.cpp:298-318).
+#include "../../include/ts_hydro.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hydro_kernels.h"
+
+namespace {
+
+constexpr int kN = 8;
+constexpr int kNC = 512;
+constexpr int kSlab = 3 * kN * kN;
+
+// Static taxonomy strings (record names outlive every context).
+constexpr const char* kNameStage[4] = {"", "hydro_stage1_kernel", "hydro_stage2_kernel",
+                                       "hydro_stage3_kernel"};
+constexpr const char* kNameSignal = "signal_speed_kernel";
+constexpr const char* kNameH2D = "copy_host_to_device";
+constexpr const char* kNameD2H = "copy_device_to_host";
+constexpr const char* kNameAlloc = "device_alloc";
+constexpr const char* kNameFree = "device_free";
+
+uint64_t steady_ns() {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+// ---- NCCL, resolved at run time so single-GPU users need no NCCL ----------
+struct Nccl {
+    bool loaded = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) {
+            n.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return;
+        }
+#define TS_SYM(field, name)                                              \
+    n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name));       \
+    if (n.field == nullptr) {                                            \
+        n.why = std::string("libnccl lacks ") + name;                    \
+        return;                                                          \
+    }
+        TS_SYM(GetUniqueId, "ncclGetUniqueId");
+        TS_SYM(CommInitRank, "ncclCommInitRank");
+        TS_SYM(CommDestroy, "ncclCommDestroy");
+        TS_SYM(CommAbort, "ncclCommAbort");
+        TS_SYM(Send, "ncclSend");
+        TS_SYM(Recv, "ncclRecv");
+        TS_SYM(AllReduce, "ncclAllReduce");
+        TS_SYM(GroupStart, "ncclGroupStart");
+        TS_SYM(GroupEnd, "ncclGroupEnd");
+        TS_SYM(GetErrorString, "ncclGetErrorString");
+#undef TS_SYM
+        n.loaded = true;
+    });
+    return n;
+}
+
+struct PendingLaunch {
+    uint8_t kind;
+    const char* name;
+    int32_t stream_id;
+    uint64_t guid;
+    uint32_t slot;  // stamp slot
+};
+
+struct Peer {
+    int rank = -1;
+    std::vector<int64_t> send_pairs;  // (global id, face) flattened
+    std::vector<int64_t> recv_pairs;
+    int64_t send_off = 0, recv_off = 0;  // entry offsets into the concatenated tables
+    int64_t n_send = 0, n_recv = 0;
+};
+
+}  // namespace
+
+struct ts_hydro_ctx {
+    ts_hydro_config cfg{};
+    int nf = 6;
+    int dev = 0;
+    int sms = 148;
+    std::string err;
+    std::recursive_mutex mu;
+    bool shut = false;
+    bool host_only = false;  // device_id = -1: mesh / halo planning only, no compute
+
+    std::vector<cudaStream_t> streams;  // lazily created; [0] compute, [1] comm
+    cudaEvent_t ev_in = nullptr, ev_halo = nullptr, ev_red = nullptr;
+
+    // mesh
+    bool have_mesh = false;
+    int world = 1, rank = 0;
+    int64_t n_global = 0, n_owned = 0, n_proxy = 0;
+    std::vector<int64_t> owned_gid, proxy_gid;
+    std::vector<int32_t> nbr_local;  // [n_local][6]
+    std::vector<int32_t> interior, boundary;
+    std::vector<Peer> peers;
+
+    // device memory
+    double* U[3] = {nullptr, nullptr, nullptr};
+    int32_t* d_nbr = nullptr;
+    int32_t* d_interior = nullptr;
+    int32_t* d_boundary = nullptr;
+    long long* d_gid = nullptr;
+    int2* d_send_entries = nullptr;
+    int2* d_recv_entries = nullptr;
+    double* d_send = nullptr;
+    double* d_recv = nullptr;
+    int64_t n_send_total = 0, n_recv_total = 0;
+    double* d_scal = nullptr;     // [0..1] amax ping-pong, [2] scratch amax, [3] dummy
+    double* d_dt_hist = nullptr;  // [kDtHist]
+    static constexpr uint64_t kDtHist = 4096;
+    unsigned long long* d_stamps = nullptr;  // [cap][2]
+    unsigned long long* h_clock = nullptr;   // mapped pinned
+    std::map<void*, uint64_t> dev_allocs;
+    std::map<void*, uint64_t> host_allocs;
+    ts_memory_state mem{};
+
+    // comm
+    ncclComm_t comm = nullptr;
+    int comm_size = 1;
+
+    // stepping
+    uint64_t steps_done = 0;
+    uint64_t launches = 0;
+    bool dt_valid = false;
+
+    // activity
+    std::vector<PendingLaunch> pending;  // launches holding a stamp slot
+    std::vector<ts_activity_record> completed;
+    uint32_t next_slot = 0;
+    int64_t clock_offset = 0;  // steady_ns - globaltimer
+    ts_activity_sink_fn sink = nullptr;
+    void* sink_user = nullptr;
+
+    size_t state_elems() const { return (size_t)(n_owned + n_proxy) * nf * kNC; }
+};
+
+namespace {
+
+int fail(ts_hydro_ctx* c, int code, const std::string& msg) {
+    if (c != nullptr) c->err = msg;
+    return code;
+}
+
+int cuda_fail(ts_hydro_ctx* c, cudaError_t e, const char* what) {
+    return fail(c, TS_ECUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+#define TS_CUDA(ctx, call)                                   \
+    do {                                                     \
+        cudaError_t _e = (call);                             \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
+    } while (0)
+
+#define TS_NCCL(ctx, call)                                                                        \
+    do {                                                                                          \
+        ncclResult_t _r = (call);                                                                 \
+        if (_r != ncclSuccess)                                                                    \
+            return fail(ctx, TS_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(_r));     \
+    } while (0)
+
+int guard(ts_hydro_ctx* c) {
+    if (c == nullptr) return TS_EINVAL;
+    if (c->shut) return fail(c, TS_ESHUTDOWN, "device is shut down");
+    return TS_OK;
+}
+
+int ensure_stream(ts_hydro_ctx* c, uint32_t id, cudaStream_t* out) {
+    if (id >= c->streams.size()) return fail(c, TS_EINVAL, "invalid stream id");
+    if (c->streams[id] == nullptr)
+        TS_CUDA(c, cudaStreamCreateWithFlags(&c->streams[id], cudaStreamNonBlocking));
+    *out = c->streams[id];
+    return TS_OK;
+}
+
+void record_mem(ts_hydro_ctx* c, uint8_t kind, uint64_t bytes) {
+    ts_activity_record r{};
+    r.kind = kind;
+    r.has_bytes = 1;
+    r.device_id = c->cfg.device_id;
+    r.stream_id = -1;
+    r.name = kind == TS_ACTIVITY_ALLOC ? kNameAlloc : kNameFree;
+    r.start_ns = r.end_ns = steady_ns();
+    r.bytes = bytes;
+    c->completed.push_back(r);
+}
+
+template <typename T>
+int dalloc(ts_hydro_ctx* c, T** p, size_t elems) {
+    const size_t bytes = std::max<size_t>(elems, 1) * sizeof(T);
+    void* raw = nullptr;
+    cudaError_t e = cudaMalloc(&raw, bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(c, TS_ENOMEM, std::string("cudaMalloc of ") + std::to_string(bytes) +
+                                      " bytes failed: " + cudaGetErrorString(e));
+    }
+    *p = static_cast<T*>(raw);
+    c->dev_allocs[raw] = bytes;
+    c->mem.current_device_bytes += bytes;
+    c->mem.peak_device_bytes = std::max(c->mem.peak_device_bytes, c->mem.current_device_bytes);
+    record_mem(c, TS_ACTIVITY_ALLOC, bytes);
+    return TS_OK;
+}
+
+template <typename T>
+void dfree(ts_hydro_ctx* c, T** p) {
+    if (*p == nullptr) return;
+    auto it = c->dev_allocs.find(*p);
+    if (it != c->dev_allocs.end()) {
+        c->mem.current_device_bytes -= it->second;
+        record_mem(c, TS_ACTIVITY_FREE, it->second);
+        c->dev_allocs.erase(it);
+    }
+    cudaFree(*p);
+    *p = nullptr;
+}
+
+void free_mesh(ts_hydro_ctx* c) {
+    for (auto& b : c->U) dfree(c, &b);
+    dfree(c, &c->d_nbr);
+    dfree(c, &c->d_interior);
+    dfree(c, &c->d_boundary);
+    dfree(c, &c->d_gid);
+    dfree(c, &c->d_send_entries);
+    dfree(c, &c->d_recv_entries);
+    dfree(c, &c->d_send);
+    dfree(c, &c->d_recv);
+    c->have_mesh = false;
+}
+
+// Harvest the stamps of every pending launch (device must be idle).
+int harvest(ts_hydro_ctx* c) {
+    if (c->pending.empty()) return TS_OK;
+    const uint32_t cap = c->cfg.activity_buffer_capacity;
+    std::vector<unsigned long long> st((size_t)cap * 2);
+    TS_CUDA(c, cudaMemcpy(st.data(), c->d_stamps, st.size() * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost));
+    for (const PendingLaunch& p : c->pending) {
+        ts_activity_record r{};
+        r.kind = p.kind;
+        r.device_id = c->cfg.device_id;
+        r.stream_id = p.stream_id;
+        r.name = p.name;
+        r.correlation_guid = p.guid;
+        const unsigned long long enc_start = st[2 * (size_t)p.slot];
+        const unsigned long long end = st[2 * (size_t)p.slot + 1];
+        if (enc_start == 0 || end == 0) continue;  // launch had no CTA (empty)
+        const unsigned long long start = ~enc_start;
+        r.start_ns = (uint64_t)((int64_t)start + c->clock_offset);
+        r.end_ns = (uint64_t)((int64_t)std::max(end, start) + c->clock_offset);
+        c->completed.push_back(r);
+    }
+    c->pending.clear();
+    c->next_slot = 0;
+    TS_CUDA(c, cudaMemset(c->d_stamps, 0, (size_t)cap * 2 * sizeof(unsigned long long)));
+    return TS_OK;
+}
+
+int sync_all(ts_hydro_ctx* c) {
+    for (cudaStream_t s : c->streams)
+        if (s != nullptr) TS_CUDA(c, cudaStreamSynchronize(s));
+    return TS_OK;
+}
+
+void deliver_to_sink(ts_hydro_ctx* c) {
+    if (c->sink == nullptr || c->completed.empty()) return;
+    std::vector<ts_activity_record> batch;
+    batch.swap(c->completed);
+    c->sink(batch.data(), batch.size(), c->sink_user);
+}
+
+// Reserve a stamp slot for a launch; flushes (waits) when the ring is full,
+// handing records to the sink like SimDevice::take_if_full (device.cpp:105-111).
+int begin_launch(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream_id, uint64_t guid,
+                 unsigned long long** stamp) {
+    if (c->next_slot >= c->cfg.activity_buffer_capacity) {
+        int rc = sync_all(c);
+        if (rc) return rc;
+        rc = harvest(c);
+        if (rc) return rc;
+        deliver_to_sink(c);
+    }
+    const uint32_t slot = c->next_slot++;
+    c->pending.push_back({kind, name, stream_id, guid, slot});
+    *stamp = c->d_stamps + 2 * (size_t)slot;
+    c->launches++;
+    return TS_OK;
+}
+
+// Host-timed copy record (synchronous copies).
+void record_copy(ts_hydro_ctx* c, uint8_t kind, uint64_t bytes, uint64_t t0, uint64_t t1) {
+    ts_activity_record r{};
+    r.kind = kind;
+    r.has_bytes = 1;
+    r.device_id = c->cfg.device_id;
+    r.stream_id = 0;
+    r.name = kind == TS_ACTIVITY_COPY_H2D ? kNameH2D : kNameD2H;
+    r.start_ns = t0;
+    r.end_ns = t1;
+    r.bytes = bytes;
+    c->completed.push_back(r);
+}
+
+int calibrate_clock(ts_hydro_ctx* c) {
+    cudaStream_t s;
+    int rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    int64_t best_span = INT64_MAX;
+    for (int trial = 0; trial < 5; ++trial) {
+        volatile unsigned long long* hv = c->h_clock;
+        *hv = 0;
+        const uint64_t t0 = steady_ns();
+        TS_CUDA(c, tsh::launch_clock(c->h_clock, s));
+        while (*hv == 0) {
+        }
+        const uint64_t t1 = steady_ns();
+        const unsigned long long g = *hv;
+        TS_CUDA(c, cudaStreamSynchronize(s));
+        const int64_t span = (int64_t)(t1 - t0);
+        if (span < best_span) {
+            best_span = span;
+            c->clock_offset = (int64_t)(t0 + (t1 - t0) / 2) - (int64_t)g;
+        }
+    }
+    return TS_OK;
+}
+
+// ---- mesh helpers -----------------------------------------------------------
+uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+    uint64_t out = 0;
+    for (int b = 0; b < 21; ++b) {
+        out |= (uint64_t)((x >> b) & 1u) << (3 * b);
+        out |= (uint64_t)((y >> b) & 1u) << (3 * b + 1);
+        out |= (uint64_t)((z >> b) & 1u) << (3 * b + 2);
+    }
+    return out;
+}
+
+int build_plans(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner) {
+    c->peers.clear();
+    if (c->world <= 1) return TS_OK;
+    std::vector<Peer> peers((size_t)c->world);
+    for (int r = 0; r < c->world; ++r) peers[(size_t)r].rank = r;
+    // send: my owned sub-grids' slabs facing a foreign neighbour, by (gid, face)
+    for (int64_t h : c->owned_gid)
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * h + f];
+            if (nb < 0) continue;
+            const int r = owner[nb];
+            if (r == c->rank) continue;
+            peers[(size_t)r].send_pairs.push_back(h);
+            peers[(size_t)r].send_pairs.push_back(f);
+        }
+    // recv: foreign proxies' slabs facing one of my sub-grids, by (gid, face)
+    for (int64_t p : c->proxy_gid)
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * p + f];
+            if (nb < 0 || owner[nb] != c->rank) continue;
+            peers[(size_t)owner[p]].recv_pairs.push_back(p);
+            peers[(size_t)owner[p]].recv_pairs.push_back(f);
+        }
+    int64_t so = 0, ro = 0;
+    for (Peer& p : peers) {
+        p.n_send = (int64_t)p.send_pairs.size() / 2;
+        p.n_recv = (int64_t)p.recv_pairs.size() / 2;
+        p.send_off = so;
+        p.recv_off = ro;
+        so += p.n_send;
+        ro += p.n_recv;
+    }
+    c->n_send_total = so;
+    c->n_recv_total = ro;
+    c->peers = std::move(peers);
+    return TS_OK;
+}
+
+int64_t local_of(const ts_hydro_ctx* c, int64_t gid) {
+    auto it = std::lower_bound(c->owned_gid.begin(), c->owned_gid.end(), gid);
+    if (it != c->owned_gid.end() && *it == gid) return it - c->owned_gid.begin();
+    auto jt = std::lower_bound(c->proxy_gid.begin(), c->proxy_gid.end(), gid);
+    if (jt != c->proxy_gid.end() && *jt == gid) return c->n_owned + (jt - c->proxy_gid.begin());
+    return -1;
+}
+
+tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
+    tsh::StageArgs a{};
+    double* A = c->U[0];
+    double* B = c->U[1];
+    double* C = c->U[2];
+    a.Uprev = stage == 1 ? A : (stage == 2 ? B : C);
+    a.Un = A;
+    a.Uout = stage == 1 ? B : (stage == 2 ? C : A);
+    a.nbr = c->d_nbr;
+    a.list = nullptr;
+    a.first = 0;
+    const int par = (int)(c->steps_done & 1);
+    a.amax_in = c->d_scal + par;
+    a.amax_out = c->d_scal + (par ^ 1);
+    a.amax_reset = nullptr;
+    a.dt_out = nullptr;
+    a.gamma = c->cfg.gamma;
+    a.gm1 = c->cfg.gamma - 1.0;
+    a.cfl = c->cfg.cfl;
+    a.dx = c->cfg.dx;
+    a.p_floor = c->cfg.p_floor;
+    return a;
+}
+
+int launch_stage_list(ts_hydro_ctx* c, tsh::StageArgs a, int stage, const int32_t* d_list, int64_t count,
+                      int first, uint32_t stream_id, uint64_t guid) {
+    if (count <= 0) return TS_OK;
+    cudaStream_t s;
+    int rc = ensure_stream(c, stream_id, &s);
+    if (rc) return rc;
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)stream_id, guid, &stamp);
+    if (rc) return rc;
+    a.list = d_list;
+    a.first = first;
+    a.stamp = stamp;
+    TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)count, s));
+    return TS_OK;
+}
+
+// Pack -> grouped NCCL send/recv -> unpack of buffer `buf` on the comm stream.
+int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
+    cudaStream_t cs;
+    int rc = ensure_stream(c, 1, &cs);
+    if (rc) return rc;
+    if (c->n_send_total > 0) {
+        c->launches++;
+        TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs));
+    }
+    if (c->comm != nullptr) {
+        Nccl& n = nccl();
+        const size_t per = (size_t)c->nf * kSlab;
+        TS_NCCL(c, n.GroupStart());
+        for (const Peer& p : c->peers) {
+            if (p.rank == c->rank) continue;
+            if (p.n_send > 0)
+                TS_NCCL(c, n.Send(c->d_send + (size_t)p.send_off * per, (size_t)p.n_send * per, ncclFloat64,
+                                  p.rank, c->comm, cs));
+            if (p.n_recv > 0)
+                TS_NCCL(c, n.Recv(c->d_recv + (size_t)p.recv_off * per, (size_t)p.n_recv * per, ncclFloat64,
+                                  p.rank, c->comm, cs));
+        }
+        TS_NCCL(c, n.GroupEnd());
+    }
+    if (c->n_recv_total > 0) {
+        c->launches++;
+        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, c->d_recv, c->sms, cs));
+    }
+    return TS_OK;
+}
+
+int do_compute_dt(ts_hydro_ctx* c) {
+    cudaStream_t s;
+    int rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    double* slot = c->d_scal + (c->steps_done & 1);
+    TS_CUDA(c, cudaMemsetAsync(slot, 0, sizeof(double), s));
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameSignal, 0, 0, &stamp);
+    if (rc) return rc;
+    TS_CUDA(c, tsh::launch_signal(c->U[0], c->nf, c->n_owned, c->cfg.gamma, c->cfg.p_floor, slot, stamp,
+                                  c->sms, s));
+    if (c->comm != nullptr && c->comm_size > 1) {
+        Nccl& n = nccl();
+        TS_NCCL(c, n.AllReduce(slot, slot, 1, ncclFloat64, ncclMax, c->comm, s));
+    }
+    c->dt_valid = true;
+    return TS_OK;
+}
+
+int do_step(ts_hydro_ctx* c) {
+    cudaStream_t s, cs;
+    int rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    const bool multi = c->world > 1;
+    if (multi) {
+        rc = ensure_stream(c, 1, &cs);
+        if (rc) return rc;
+    }
+    for (int stage = 1; stage <= 3; ++stage) {
+        tsh::StageArgs a = stage_args(c, stage);
+        if (stage == 1) {
+            a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
+            a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+        }
+        if (!multi) {
+            rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0);
+            if (rc) return rc;
+            continue;
+        }
+        double* in = const_cast<double*>(a.Uprev);
+        TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+        TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+        rc = exchange_on_comm(c, in);
+        if (rc) return rc;
+        TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
+        // interior sub-grids overlap the exchange; the boundary ones wait for it
+        rc = launch_stage_list(c, a, stage, c->d_interior, (int64_t)c->interior.size(), 0, 0, 0);
+        if (rc) return rc;
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+        tsh::StageArgs b = a;
+        b.amax_reset = nullptr;  // the interior launch (or this one if alone) resets
+        if (c->interior.empty()) b.amax_reset = a.amax_reset;
+        if (!c->interior.empty()) b.dt_out = nullptr;
+        rc = launch_stage_list(c, b, stage, c->d_boundary, (int64_t)c->boundary.size(), 0, 0, 0);
+        if (rc) return rc;
+    }
+    if (multi && c->comm != nullptr) {
+        double* slot = c->d_scal + ((c->steps_done & 1) ^ 1);
+        TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+        TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+        Nccl& n = nccl();
+        TS_NCCL(c, n.AllReduce(slot, slot, 1, ncclFloat64, ncclMax, c->comm, cs));
+        TS_CUDA(c, cudaEventRecord(c->ev_red, cs));
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_red, 0));
+    }
+    c->steps_done++;
+    return TS_OK;
+}
+
+int check_state(ts_hydro_ctx* c) {
+    int rc = guard(c);
+    if (rc) return rc;
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    if (!c->have_mesh) return fail(c, TS_ESTATE, "no mesh bound (call ts_hydro_set_mesh first)");
+    return TS_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+int ts_hydro_abi_version(void) { return TS_HYDRO_ABI_VERSION; }
+
+void ts_hydro_default_config(ts_hydro_config* cfg) {
+    if (cfg == nullptr) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->device_id = 0;
+    cfg->stream_count = 128;
+    cfg->activity_buffer_capacity = 1024;
+    cfg->cells_per_edge = 8;
+    cfg->n_species = 0;
+    cfg->recon = TS_RECON_PPM;
+    cfg->gamma = 1.4;
+    cfg->cfl = 0.4;
+    cfg->dx = 1.0 / 32.0;
+    cfg->p_floor = 1e-12;
+}
+
+const char* ts_hydro_strerror(int code) {
+    switch (code) {
+        case TS_OK: return "ok";
+        case TS_EINVAL: return "invalid argument";
+        case TS_ESHUTDOWN: return "device is shut down";
+        case TS_ECUDA: return "CUDA error";
+        case TS_ENCCL: return "NCCL error";
+        case TS_ENOMEM: return "out of device memory";
+        case TS_ESTATE: return "call out of order";
+    }
+    return "unknown error";
+}
+
+uint64_t ts_hydro_clock_ns(void) { return steady_ns(); }
+
+static int validate_config(const ts_hydro_config* cfg, std::string* why) {
+    if (cfg->cells_per_edge != kN) {
+        *why = "cells_per_edge must be 8 (the sub-grid size this path is built for)";
+        return TS_EINVAL;
+    }
+    if (cfg->n_species < 0 || cfg->n_species > 5) {
+        *why = "n_species must be in [0, 5]";
+        return TS_EINVAL;
+    }
+    if (cfg->recon != TS_RECON_PPM && cfg->recon != TS_RECON_MINMOD) {
+        *why = "unknown reconstruction";
+        return TS_EINVAL;
+    }
+    if (!(cfg->gamma > 1.0) || !(cfg->cfl > 0.0) || !(cfg->dx > 0.0) || !(cfg->p_floor >= 0.0)) {
+        *why = "gamma > 1, cfl > 0, dx > 0 and p_floor >= 0 are required";
+        return TS_EINVAL;
+    }
+    if (cfg->stream_count < 2) {
+        *why = "stream_count must be at least 2 (compute + halo)";
+        return TS_EINVAL;
+    }
+    if (cfg->activity_buffer_capacity == 0) {
+        *why = "activity_buffer_capacity must be positive";
+        return TS_EINVAL;
+    }
+    return TS_OK;
+}
+
+int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
+    if (cfg == nullptr || out == nullptr) return TS_EINVAL;
+    *out = nullptr;
+    std::string why;
+    if (validate_config(cfg, &why) != TS_OK) {
+        std::fprintf(stderr, "ts_hydro_create: %s\n", why.c_str());
+        return TS_EINVAL;
+    }
+    auto* c = new (std::nothrow) ts_hydro_ctx();
+    if (c == nullptr) return TS_ENOMEM;
+    c->cfg = *cfg;
+    c->nf = 6 + cfg->n_species;
+    c->dev = cfg->device_id;
+    if (cfg->device_id < 0) {
+        c->host_only = true;
+        *out = c;
+        return TS_OK;
+    }
+    cudaError_t e = cudaSetDevice(c->dev);
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "ts_hydro_create: cudaSetDevice(%d): %s\n", c->dev, cudaGetErrorString(e));
+        delete c;
+        return TS_ECUDA;
+    }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev);
+    c->streams.assign(cfg->stream_count, nullptr);
+    int rc = TS_OK;
+    if ((e = cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming)) != cudaSuccess) {
+        rc = cuda_fail(c, e, "cudaEventCreate");
+    }
+    if (!rc) rc = dalloc(c, &c->d_scal, 8);
+    if (!rc) rc = dalloc(c, &c->d_dt_hist, ts_hydro_ctx::kDtHist);
+    if (!rc) rc = dalloc(c, &c->d_stamps, (size_t)cfg->activity_buffer_capacity * 2);
+    if (!rc && (e = cudaMemset(c->d_stamps, 0, (size_t)cfg->activity_buffer_capacity * 2 * 8)) != cudaSuccess)
+        rc = cuda_fail(c, e, "cudaMemset");
+    if (!rc && (e = cudaMemset(c->d_scal, 0, 8 * sizeof(double))) != cudaSuccess) rc = cuda_fail(c, e, "cudaMemset");
+    if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, sizeof(unsigned long long), cudaHostAllocMapped)) !=
+                   cudaSuccess)
+        rc = cuda_fail(c, e, "cudaHostAlloc");
+    if (!rc) rc = calibrate_clock(c);
+    if (rc) {
+        std::fprintf(stderr, "ts_hydro_create: %s\n", c->err.c_str());
+        ts_hydro_destroy(c);
+        return rc;
+    }
+    // creation-time records are bookkeeping of the context itself
+    c->completed.clear();
+    *out = c;
+    return TS_OK;
+}
+
+const char* ts_hydro_last_error(const ts_hydro_ctx* ctx) { return ctx == nullptr ? "null context" : ctx->err.c_str(); }
+
+int ts_hydro_num_fields(const ts_hydro_ctx* ctx) { return ctx == nullptr ? -1 : ctx->nf; }
+
+int ts_hydro_shutdown(ts_hydro_ctx* ctx) {
+    if (ctx == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (ctx->shut) return TS_OK;
+    if (ctx->host_only) {
+        ctx->shut = true;
+        return TS_OK;
+    }
+    cudaSetDevice(ctx->dev);
+    int rc = sync_all(ctx);
+    if (!rc) rc = harvest(ctx);
+    deliver_to_sink(ctx);
+    ctx->shut = true;
+    return rc;
+}
+
+int ts_hydro_destroy(ts_hydro_ctx* ctx) {
+    if (ctx == nullptr) return TS_EINVAL;
+    if (ctx->host_only) {
+        delete ctx;
+        return TS_OK;
+    }
+    {
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        cudaSetDevice(ctx->dev);
+        if (!ctx->shut) {
+            sync_all(ctx);
+            harvest(ctx);
+            deliver_to_sink(ctx);
+            ctx->shut = true;
+        }
+        if (ctx->comm != nullptr && nccl().loaded) nccl().CommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+        free_mesh(ctx);
+        dfree(ctx, &ctx->d_scal);
+        dfree(ctx, &ctx->d_dt_hist);
+        dfree(ctx, &ctx->d_stamps);
+        for (auto& kv : ctx->host_allocs) cudaFreeHost(kv.first);
+        ctx->host_allocs.clear();
+        if (ctx->h_clock) cudaFreeHost(ctx->h_clock);
+        if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+        if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+        if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
+        for (cudaStream_t s : ctx->streams)
+            if (s) cudaStreamDestroy(s);
+    }
+    delete ctx;
+    return TS_OK;
+}
+
+int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_mask, int32_t world,
+                          int64_t* nbr, int32_t* pos, int32_t* owner) {
+    if (nx < 1 || ny < 1 || nz < 1 || world < 1 || nbr == nullptr || pos == nullptr || owner == nullptr)
+        return TS_EINVAL;
+    const int64_t n = (int64_t)nx * ny * nz;
+    struct K {
+        uint64_t key;
+        int32_t x, y, z;
+    };
+    std::vector<K> keys;
+    keys.reserve((size_t)n);
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) keys.push_back({morton3((uint32_t)x, (uint32_t)y, (uint32_t)z), x, y, z});
+    std::sort(keys.begin(), keys.end(), [](const K& a, const K& b) { return a.key < b.key; });
+    std::vector<int64_t> id_of((size_t)n);
+    for (int64_t g = 0; g < n; ++g) {
+        pos[3 * g] = keys[(size_t)g].x;
+        pos[3 * g + 1] = keys[(size_t)g].y;
+        pos[3 * g + 2] = keys[(size_t)g].z;
+        id_of[(size_t)(((int64_t)keys[(size_t)g].z * ny + keys[(size_t)g].y) * nx + keys[(size_t)g].x)] = g;
+    }
+    const int dims[3] = {nx, ny, nz};
+    for (int64_t g = 0; g < n; ++g)
+        for (int face = 0; face < 6; ++face) {
+            int cc[3] = {pos[3 * g], pos[3 * g + 1], pos[3 * g + 2]};
+            const int axis = face / 2;
+            cc[axis] += (face & 1) ? 1 : -1;
+            int64_t nb = -1;
+            if (cc[axis] < 0 || cc[axis] >= dims[axis]) {
+                if (periodic_mask & (1 << axis)) {
+                    cc[axis] = (cc[axis] + dims[axis]) % dims[axis];
+                    nb = id_of[(size_t)(((int64_t)cc[2] * ny + cc[1]) * nx + cc[0])];
+                }
+            } else {
+                nb = id_of[(size_t)(((int64_t)cc[2] * ny + cc[1]) * nx + cc[0])];
+            }
+            nbr[6 * g + face] = nb;
+        }
+    // contiguous Morton chunks, first `extra` ranks one larger (workload.cpp:314-323)
+    const int64_t base = n / world, extra = n % world;
+    int64_t cursor = 0;
+    for (int r = 0; r < world; ++r) {
+        const int64_t count = base + (r < extra ? 1 : 0);
+        for (int64_t j = 0; j < count; ++j) owner[cursor++] = r;
+    }
+    return TS_OK;
+}
+
+int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int32_t* owner, int32_t world,
+                      int32_t rank) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (n < 1 || nbr == nullptr || owner == nullptr) return fail(c, TS_EINVAL, "empty mesh");
+    if (world < 1) return fail(c, TS_EINVAL, "mesh world_size must be positive");
+    if (rank < 0 || rank >= world) return fail(c, TS_EINVAL, "rank outside the world");
+    if (n > (int64_t)INT32_MAX / 2) return fail(c, TS_EINVAL, "too many sub-grids");
+    // Mesh::validate (workload.cpp:140-168)
+    for (int64_t i = 0; i < n; ++i) {
+        const std::string where = "sub-grid " + std::to_string(i) + ": ";
+        if (owner[i] < 0 || owner[i] >= world) return fail(c, TS_EINVAL, where + "owner outside the world");
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * i + f];
+            if (nb == -1) continue;
+            if (nb < 0 || nb >= n) return fail(c, TS_EINVAL, where + "neighbor id out of range");
+            if (nb == i) return fail(c, TS_EINVAL, where + "sub-grid linked to itself");
+            if (nbr[6 * nb + (f ^ 1)] != i) return fail(c, TS_EINVAL, where + "neighbor link is not symmetric");
+        }
+    }
+    if (!c->host_only) {
+        cudaSetDevice(c->dev);
+        rc = sync_all(c);
+        if (rc) return rc;
+        free_mesh(c);
+    }
+    c->world = world;
+    c->rank = rank;
+    c->n_global = n;
+    c->owned_gid.clear();
+    c->proxy_gid.clear();
+    for (int64_t i = 0; i < n; ++i)
+        if (owner[i] == rank) c->owned_gid.push_back(i);
+    std::vector<char> is_proxy((size_t)n, 0);
+    for (int64_t g : c->owned_gid)
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * g + f];
+            if (nb >= 0 && owner[nb] != rank) is_proxy[(size_t)nb] = 1;
+        }
+    for (int64_t i = 0; i < n; ++i)
+        if (is_proxy[(size_t)i]) c->proxy_gid.push_back(i);
+    c->n_owned = (int64_t)c->owned_gid.size();
+    c->n_proxy = (int64_t)c->proxy_gid.size();
+    const int64_t nl = c->n_owned + c->n_proxy;
+    c->nbr_local.assign((size_t)nl * 6, -1);
+    c->interior.clear();
+    c->boundary.clear();
+    for (int64_t l = 0; l < c->n_owned; ++l) {
+        const int64_t g = c->owned_gid[(size_t)l];
+        bool foreign = false;
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * g + f];
+            if (nb < 0) continue;
+            c->nbr_local[(size_t)l * 6 + f] = (int32_t)local_of(c, nb);
+            if (owner[nb] != rank) foreign = true;
+        }
+        (foreign ? c->boundary : c->interior).push_back((int32_t)l);
+    }
+    rc = build_plans(c, nbr, owner);
+    if (rc) return rc;
+    if (c->host_only) {
+        c->have_mesh = true;
+        return TS_OK;
+    }
+    const size_t elems = c->state_elems();
+    for (auto& b : c->U) {
+        rc = dalloc(c, &b, elems);
+        if (rc) return rc;
+        TS_CUDA(c, cudaMemset(b, 0, elems * sizeof(double)));
+    }
+    rc = dalloc(c, &c->d_nbr, (size_t)nl * 6);
+    if (!rc) rc = dalloc(c, &c->d_interior, c->interior.size());
+    if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
+    if (!rc) rc = dalloc(c, &c->d_gid, (size_t)c->n_owned);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpy(c->d_nbr, c->nbr_local.data(), c->nbr_local.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    if (!c->interior.empty())
+        TS_CUDA(c, cudaMemcpy(c->d_interior, c->interior.data(), c->interior.size() * sizeof(int32_t),
+                              cudaMemcpyHostToDevice));
+    if (!c->boundary.empty())
+        TS_CUDA(c, cudaMemcpy(c->d_boundary, c->boundary.data(), c->boundary.size() * sizeof(int32_t),
+                              cudaMemcpyHostToDevice));
+    {
+        std::vector<long long> gid(c->owned_gid.begin(), c->owned_gid.end());
+        if (!gid.empty())
+            TS_CUDA(c, cudaMemcpy(c->d_gid, gid.data(), gid.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    }
+    if (world > 1) {
+        std::vector<int2> se((size_t)c->n_send_total), re((size_t)c->n_recv_total);
+        for (const Peer& p : c->peers) {
+            for (int64_t k = 0; k < p.n_send; ++k)
+                se[(size_t)(p.send_off + k)] = make_int2((int)local_of(c, p.send_pairs[(size_t)(2 * k)]),
+                                                         (int)p.send_pairs[(size_t)(2 * k + 1)]);
+            for (int64_t k = 0; k < p.n_recv; ++k)
+                re[(size_t)(p.recv_off + k)] = make_int2((int)local_of(c, p.recv_pairs[(size_t)(2 * k)]),
+                                                         (int)p.recv_pairs[(size_t)(2 * k + 1)]);
+        }
+        rc = dalloc(c, &c->d_send_entries, se.size());
+        if (!rc) rc = dalloc(c, &c->d_recv_entries, re.size());
+        if (!rc) rc = dalloc(c, &c->d_send, (size_t)c->n_send_total * c->nf * kSlab);
+        if (!rc) rc = dalloc(c, &c->d_recv, (size_t)c->n_recv_total * c->nf * kSlab);
+        if (rc) return rc;
+        if (!se.empty())
+            TS_CUDA(c, cudaMemcpy(c->d_send_entries, se.data(), se.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        if (!re.empty())
+            TS_CUDA(c, cudaMemcpy(c->d_recv_entries, re.data(), re.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+    c->steps_done = 0;
+    c->dt_valid = false;
+    c->have_mesh = true;
+    return TS_OK;
+}
+
+int ts_hydro_local_counts(const ts_hydro_ctx* c, int64_t* n_owned, int64_t* n_proxy, int64_t* n_interior) {
+    if (c == nullptr) return TS_EINVAL;
+    if (!c->have_mesh) return TS_ESTATE;
+    if (n_owned) *n_owned = c->n_owned;
+    if (n_proxy) *n_proxy = c->n_proxy;
+    if (n_interior) *n_interior = (int64_t)c->interior.size();
+    return TS_OK;
+}
+
+int ts_hydro_owned_ids(const ts_hydro_ctx* c, int64_t* ids) {
+    if (c == nullptr || ids == nullptr) return TS_EINVAL;
+    if (!c->have_mesh) return TS_ESTATE;
+    std::copy(c->owned_gid.begin(), c->owned_gid.end(), ids);
+    return TS_OK;
+}
+
+int ts_hydro_halo_plan(const ts_hydro_ctx* c, int32_t peer, int64_t* n_send, int64_t* send_pairs,
+                       int64_t* n_recv, int64_t* recv_pairs) {
+    if (c == nullptr) return TS_EINVAL;
+    if (!c->have_mesh) return TS_ESTATE;
+    if (peer < 0 || peer >= c->world) return TS_EINVAL;
+    if (c->world <= 1 || peer == c->rank) {
+        if (n_send) *n_send = 0;
+        if (n_recv) *n_recv = 0;
+        return TS_OK;
+    }
+    const Peer& p = c->peers[(size_t)peer];
+    if (n_send) *n_send = p.n_send;
+    if (n_recv) *n_recv = p.n_recv;
+    if (send_pairs) std::copy(p.send_pairs.begin(), p.send_pairs.end(), send_pairs);
+    if (recv_pairs) std::copy(p.recv_pairs.begin(), p.recv_pairs.end(), recv_pairs);
+    return TS_OK;
+}
+
+int ts_hydro_upload(ts_hydro_ctx* c, int64_t first, int64_t count, const double* host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (first < 0 || count < 0 || first + count > c->n_owned || (count > 0 && host == nullptr))
+        return fail(c, TS_EINVAL, "upload range outside the owned sub-grids");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    const size_t per = (size_t)c->nf * kNC;
+    const uint64_t t0 = steady_ns();
+    TS_CUDA(c, cudaMemcpy(c->U[0] + (size_t)first * per, host, (size_t)count * per * sizeof(double),
+                          cudaMemcpyHostToDevice));
+    record_copy(c, TS_ACTIVITY_COPY_H2D, (uint64_t)count * per * sizeof(double), t0, steady_ns());
+    c->dt_valid = false;
+    return TS_OK;
+}
+
+int ts_hydro_download(ts_hydro_ctx* c, int64_t first, int64_t count, double* host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (first < 0 || count < 0 || first + count > c->n_owned || (count > 0 && host == nullptr))
+        return fail(c, TS_EINVAL, "download range outside the owned sub-grids");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    const size_t per = (size_t)c->nf * kNC;
+    const uint64_t t0 = steady_ns();
+    TS_CUDA(c, cudaMemcpy(host, c->U[0] + (size_t)first * per, (size_t)count * per * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    record_copy(c, TS_ACTIVITY_COPY_D2H, (uint64_t)count * per * sizeof(double), t0, steady_ns());
+    return TS_OK;
+}
+
+int ts_hydro_init_random(ts_hydro_ctx* c, uint64_t seed) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    c->launches++;
+    TS_CUDA(c, tsh::launch_init_random(c->U[0], c->nf, c->d_gid, c->n_owned, seed, c->cfg.gamma, c->sms, s));
+    TS_CUDA(c, cudaStreamSynchronize(s));
+    c->dt_valid = false;
+    return TS_OK;
+}
+
+int ts_hydro_compute_dt(ts_hydro_ctx* c, double* dt_out) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    rc = do_compute_dt(c);
+    if (rc) return rc;
+    if (dt_out != nullptr) {
+        double amax = 0.0;
+        cudaStream_t s = c->streams[0];
+        TS_CUDA(c, cudaMemcpyAsync(&amax, c->d_scal + (c->steps_done & 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+        TS_CUDA(c, cudaStreamSynchronize(s));
+        *dt_out = (c->cfg.cfl * c->cfg.dx) / amax;
+    }
+    return TS_OK;
+}
+
+int ts_hydro_step(ts_hydro_ctx* c, uint64_t nsteps) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    if (c->world > 1 && c->comm == nullptr)
+        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init before stepping");
+    if (!c->dt_valid) {
+        rc = do_compute_dt(c);
+        if (rc) return rc;
+    }
+    for (uint64_t k = 0; k < nsteps; ++k) {
+        rc = do_step(c);
+        if (rc) return rc;
+    }
+    return TS_OK;
+}
+
+int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out, uint64_t nsteps) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    const size_t bytes = (size_t)c->n_owned * c->nf * kNC * sizeof(double);
+    TS_CUDA(c, cudaMemcpyAsync(c->U[0], host_in, bytes, cudaMemcpyHostToDevice, s));
+    rc = do_compute_dt(c);
+    if (rc) return rc;
+    for (uint64_t k = 0; k < nsteps; ++k) {
+        rc = do_step(c);
+        if (rc) return rc;
+    }
+    TS_CUDA(c, cudaMemcpyAsync(host_out, c->U[0], bytes, cudaMemcpyDeviceToHost, s));
+    TS_CUDA(c, cudaStreamSynchronize(s));
+    return TS_OK;
+}
+
+int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (ms == nullptr) return fail(c, TS_EINVAL, "null output");
+    if (c->world > 1 && c->comm == nullptr)
+        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init before stepping");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    if (!c->dt_valid) {
+        rc = do_compute_dt(c);
+        if (rc) return rc;
+    }
+    cudaEvent_t e0, e1;
+    TS_CUDA(c, cudaEventCreate(&e0));
+    TS_CUDA(c, cudaEventCreate(&e1));
+    TS_CUDA(c, cudaEventRecord(e0, s));
+    for (uint64_t k = 0; k < nsteps && rc == TS_OK; ++k) rc = do_step(c);
+    cudaError_t e = cudaEventRecord(e1, s);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float f = 0.0f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&f, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(c, e, "event timing");
+    *ms = (double)f;
+    return TS_OK;
+}
+
+int ts_hydro_synchronize(ts_hydro_ctx* c) {
+    if (c == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->host_only) return TS_OK;
+    cudaSetDevice(c->dev);
+    return sync_all(c);
+}
+
+int ts_hydro_last_dt(ts_hydro_ctx* c, double* dt) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (dt == nullptr) return TS_EINVAL;
+    if (c->steps_done == 0) return fail(c, TS_ESTATE, "no step taken yet");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpy(dt, c->d_dt_hist + ((c->steps_done - 1) % ts_hydro_ctx::kDtHist), sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    return TS_OK;
+}
+
+int ts_hydro_steps_done(const ts_hydro_ctx* c, uint64_t* steps) {
+    if (c == nullptr || steps == nullptr) return TS_EINVAL;
+    *steps = c->steps_done;
+    return TS_OK;
+}
+
+int ts_hydro_launch_count(const ts_hydro_ctx* c, uint64_t* launches) {
+    if (c == nullptr || launches == nullptr) return TS_EINVAL;
+    *launches = c->launches;
+    return TS_OK;
+}
+
+namespace {
+struct DoneThunk {
+    ts_done_fn fn;
+    void* user;
+    int32_t* list;
+};
+void CUDART_CB done_host(void* p) {
+    auto* t = static_cast<DoneThunk*>(p);
+    if (t->fn) t->fn(t->user);
+    delete t;
+}
+}  // namespace
+
+int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_index, int64_t count,
+                          uint32_t stream_id, uint64_t guid, ts_done_fn done, void* user) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (stage < 1 || stage > 3) return fail(c, TS_EINVAL, "stage must be 1, 2 or 3");
+    if (count <= 0 || owned_index == nullptr) return fail(c, TS_EINVAL, "empty sub-grid list");
+    if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
+    if (c->world > 1) return fail(c, TS_ESTATE, "per-sub-grid launches are single-rank (use ts_hydro_step)");
+    if (!c->dt_valid) return fail(c, TS_ESTATE, "no dt (call ts_hydro_compute_dt first)");
+    std::vector<int32_t> list((size_t)count);
+    for (int64_t k = 0; k < count; ++k) {
+        if (owned_index[k] < 0 || owned_index[k] >= c->n_owned)
+            return fail(c, TS_EINVAL, "sub-grid index outside the owned range");
+        list[(size_t)k] = (int32_t)owned_index[k];
+    }
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, stream_id, &s);
+    if (rc) return rc;
+    int32_t* d_list = nullptr;
+    TS_CUDA(c, cudaMallocAsync((void**)&d_list, list.size() * sizeof(int32_t), s));
+    TS_CUDA(c, cudaMemcpyAsync(d_list, list.data(), list.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    tsh::StageArgs a = stage_args(c, stage);
+    a.amax_out = c->d_scal + 3;  // dummy: the caller recomputes dt per step
+    rc = launch_stage_list(c, a, stage, d_list, count, 0, stream_id, guid);
+    if (rc) return rc;
+    TS_CUDA(c, cudaFreeAsync(d_list, s));
+    if (done != nullptr) {
+        auto* t = new DoneThunk{done, user, nullptr};
+        TS_CUDA(c, cudaLaunchHostFunc(s, done_host, t));
+    }
+    // pageable H2D copies are staged before cudaMemcpyAsync returns: `list` may go
+    return TS_OK;
+}
+
+int ts_hydro_finish_step(ts_hydro_ctx* c) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    c->steps_done++;
+    c->dt_valid = false;
+    return TS_OK;
+}
+
+int ts_hydro_exchange_faces(ts_hydro_ctx* c, double* ghost_host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (ghost_host == nullptr) return fail(c, TS_EINVAL, "null ghost buffer");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    if (c->world > 1) {
+        rc = ts_hydro_halo_exchange(c);
+        if (rc) return rc;
+    }
+    double* d = nullptr;
+    const size_t n = (size_t)c->n_owned * 6 * kN * kN;
+    rc = dalloc(c, &d, n);
+    if (rc) return rc;
+    c->launches++;
+    cudaError_t e = tsh::launch_face_exchange(c->U[0], c->nf, c->d_nbr, c->n_owned, d, c->sms, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ghost_host, d, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    dfree(c, &d);
+    if (e != cudaSuccess) return cuda_fail(c, e, "face exchange");
+    return TS_OK;
+}
+
+int ts_hydro_fill_halo(ts_hydro_ctx* c, int32_t depth, double* tiles_host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (depth < 0 || depth > kN || tiles_host == nullptr) return fail(c, TS_EINVAL, "halo depth must be in [0, 8]");
+    if (c->world > 1 && depth > 3) return fail(c, TS_EINVAL, "cross-rank halos are 3 deep");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    if (c->world > 1) {
+        rc = ts_hydro_halo_exchange(c);
+        if (rc) return rc;
+    }
+    const size_t pe = (size_t)(kN + 2 * depth);
+    const size_t n = (size_t)c->n_owned * c->nf * pe * pe * pe;
+    double* d = nullptr;
+    rc = dalloc(c, &d, n);
+    if (rc) return rc;
+    c->launches++;
+    cudaError_t e = tsh::launch_fill_halo(c->U[0], c->nf, c->d_nbr, c->n_owned, depth, d, c->sms, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tiles_host, d, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    dfree(c, &d);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fill halo");
+    return TS_OK;
+}
+
+int ts_hydro_nccl_unique_id(uint8_t id[128]) {
+    if (id == nullptr) return TS_EINVAL;
+    Nccl& n = nccl();
+    if (!n.loaded) {
+        std::fprintf(stderr, "ts_hydro_nccl_unique_id: %s\n", n.why.c_str());
+        return TS_ENCCL;
+    }
+    ncclUniqueId u;
+    if (n.GetUniqueId(&u) != ncclSuccess) return TS_ENCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return TS_OK;
+}
+
+int ts_hydro_comm_init(ts_hydro_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (id == nullptr || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TS_EINVAL, "bad comm arguments");
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    Nccl& n = nccl();
+    if (!n.loaded) return fail(c, TS_ENCCL, n.why);
+    cudaSetDevice(c->dev);
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    if (c->comm != nullptr) {
+        n.CommDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    TS_NCCL(c, n.CommInitRank(&c->comm, nranks, u, rank));
+    c->comm_size = nranks;
+    return TS_OK;
+}
+
+int ts_hydro_halo_exchange(ts_hydro_ctx* c) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->world <= 1) return TS_OK;
+    if (c->comm == nullptr) return fail(c, TS_ESTATE, "ts_hydro_comm_init not called");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    rc = sync_all(c);
+    if (rc) return rc;
+    rc = exchange_on_comm(c, c->U[0]);
+    if (rc) return rc;
+    return sync_all(c);
+}
+
+int ts_hydro_set_activity_sink(ts_hydro_ctx* c, ts_activity_sink_fn sink, void* user) {
+    if (c == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->sink = sink;
+    c->sink_user = user;
+    return TS_OK;
+}
+
+int ts_hydro_flush_activity(ts_hydro_ctx* c, ts_activity_record* out, uint64_t cap, uint64_t* n_out) {
+    if (c == nullptr || n_out == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    int rc = TS_OK;
+    if (!c->shut && !c->host_only) {
+        cudaSetDevice(c->dev);
+        rc = sync_all(c);
+        if (!rc) rc = harvest(c);
+        if (rc) return rc;
+    }
+    if (out == nullptr) {
+        *n_out = c->completed.size();
+        return TS_OK;
+    }
+    const uint64_t n = std::min<uint64_t>(cap, c->completed.size());
+    std::copy(c->completed.begin(), c->completed.begin() + (ptrdiff_t)n, out);
+    c->completed.erase(c->completed.begin(), c->completed.begin() + (ptrdiff_t)n);
+    *n_out = n;
+    return TS_OK;
+}
+
+int ts_hydro_memory_state(const ts_hydro_ctx* c, ts_memory_state* out) {
+    if (c == nullptr || out == nullptr) return TS_EINVAL;
+    *out = c->mem;
+    return TS_OK;
+}
+
+int ts_hydro_host_alloc(ts_hydro_ctx* c, uint64_t bytes, void** ptr) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (bytes == 0 || ptr == nullptr) return fail(c, TS_EINVAL, "zero-byte allocation");
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    cudaSetDevice(c->dev);
+    void* p = nullptr;
+    TS_CUDA(c, cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+    c->host_allocs[p] = bytes;
+    c->mem.current_host_pinned_bytes += bytes;
+    c->mem.peak_host_pinned_bytes = std::max(c->mem.peak_host_pinned_bytes, c->mem.current_host_pinned_bytes);
+    *ptr = p;
+    return TS_OK;
+}
+
+int ts_hydro_host_free(ts_hydro_ctx* c, void* ptr) {
+    if (c == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    auto it = c->host_allocs.find(ptr);
+    if (it == c->host_allocs.end()) return fail(c, TS_EINVAL, "free of unknown or already-freed pinned handle");
+    c->mem.current_host_pinned_bytes -= it->second;
+    c->host_allocs.erase(it);
+    cudaFreeHost(ptr);
+    return TS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// ts_hydro_ic.cpp — host-side initial conditions for the benchmark configs
+// (BASELINE.json configs).  Cell-centred, global coordinates
+// from the sub-grid positions, so every rank fills exactly its own slice.
+//
+// SOD, SEDOV and RANDOM restate the same formulas as the oracle (they are
+// compared bitwise in tests/); POLYTROPE and BINARY are product-only inputs
+// (parity tests feed the same array to both sides).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../include/ts_hydro.h"
+
+namespace {
+
+constexpr int kN = 8;
+constexpr int kNC = 512;
+
+uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+uint64_t mix64(uint64_t a, uint64_t b) { return mix64(a ^ mix64(b)); }
+double cell_value(uint64_t g, uint64_t s, uint64_t i) {
+    return static_cast<double>(mix64(mix64(g, s), i) >> 11) * 0x1.0p-53;
+}
+
+struct Prim {
+    double rho, vx, vy, vz, p, extra_e;
+    double species[5];
+};
+
+void store(const ts_hydro_config& cfg, double* u, const Prim& w, int nf) {
+    const double eint = w.p / (cfg.gamma - 1.0);
+    const double v2 = std::fma(w.vx, w.vx, std::fma(w.vy, w.vy, w.vz * w.vz));
+    u[0] = w.rho;
+    u[kNC] = w.rho * w.vx;
+    u[2 * kNC] = w.rho * w.vy;
+    u[3 * kNC] = w.rho * w.vz;
+    u[4 * kNC] = std::fma(0.5 * w.rho, v2, eint) + w.extra_e;
+    u[5 * kNC] = std::pow(eint + w.extra_e, 1.0 / cfg.gamma);
+    for (int k = 6; k < nf; ++k) u[k * kNC] = (k - 6) < 5 ? w.species[k - 6] : 0.0;
+}
+
+// Lane–Emden theta(xi) for index n, tabulated by RK4 to the first zero.
+struct LaneEmden {
+    std::vector<double> theta;
+    double h = 1e-4;
+    double xi1 = 0.0;
+    explicit LaneEmden(double n) {
+        double xi = 1e-6, th = 1.0 - xi * xi / 6.0, dth = -xi / 3.0;
+        theta.push_back(1.0);
+        auto f = [n](double x, double t, double dt, double* d2) {
+            const double tp = t > 0.0 ? std::pow(t, n) : 0.0;
+            *d2 = -tp - 2.0 / x * dt;
+        };
+        while (th > 0.0 && xi < 20.0) {
+            double a1, a2, a3, a4;
+            f(xi, th, dth, &a1);
+            const double t1 = th + 0.5 * h * dth, d1 = dth + 0.5 * h * a1;
+            f(xi + 0.5 * h, t1, d1, &a2);
+            const double t2 = th + 0.5 * h * d1, d2 = dth + 0.5 * h * a2;
+            f(xi + 0.5 * h, t2, d2, &a3);
+            const double t3 = th + h * d2, d3 = dth + h * a3;
+            f(xi + h, t3, d3, &a4);
+            th += h / 6.0 * (dth + 2 * d1 + 2 * d2 + d3);
+            dth += h / 6.0 * (a1 + 2 * a2 + 2 * a3 + a4);
+            xi += h;
+            theta.push_back(th > 0.0 ? th : 0.0);
+        }
+        xi1 = xi;
+    }
+    double operator()(double xi) const {
+        if (xi >= xi1) return 0.0;
+        const double k = xi / h;
+        const size_t i = static_cast<size_t>(k);
+        if (i + 1 >= theta.size()) return 0.0;
+        const double fr = k - static_cast<double>(i);
+        return theta[i] * (1.0 - fr) + theta[i + 1] * fr;
+    }
+};
+
+}  // namespace
+
+extern "C" int ts_hydro_ic_fill(const ts_hydro_config* cfg, int32_t problem, int64_t n, const int64_t* gids,
+                                const int32_t* pos, const int32_t* dims, uint64_t seed, double* out) {
+    if (cfg == nullptr || out == nullptr || n < 0 || pos == nullptr || dims == nullptr) return TS_EINVAL;
+    if (problem == TS_PROBLEM_RANDOM && gids == nullptr) return TS_EINVAL;
+    if (problem < TS_PROBLEM_SOD || problem > TS_PROBLEM_BINARY) return TS_EINVAL;
+    const int nf = 6 + cfg->n_species;
+    const double dx = cfg->dx;
+    const int64_t nc[3] = {(int64_t)dims[0] * kN, (int64_t)dims[1] * kN, (int64_t)dims[2] * kN};
+    const double L[3] = {nc[0] * dx, nc[1] * dx, nc[2] * dx};
+
+    // polytrope: one star per cubic block of side T sub-grids (weak scaling tiles)
+    const int T = std::min(dims[0], std::min(dims[1], dims[2]));
+    const double Lb = T * kN * dx;
+    const double R = 0.4 * 0.5 * Lb;
+    // binary: primary n=1.5 polytrope + secondary of half its radius, q ~ 0.1, in contact
+    static const LaneEmden le15(1.5);
+    const double R1 = 0.22 * L[0], R2 = 0.5 * R1;
+    const double sep = R1 + R2;
+    const double rc1 = 1.0, rc2 = 0.8;  // M2/M1 = (rc2/rc1)(R2/R1)^3 = 0.1
+    const double m1 = rc1 * R1 * R1 * R1, m2 = rc2 * R2 * R2 * R2;
+    const double cxm = 0.5 * L[0], cy = 0.5 * L[1], cz = 0.5 * L[2];
+    const double x1 = cxm - sep * m2 / (m1 + m2), x2 = cxm + sep * m1 / (m1 + m2);
+    const double kPi = 3.14159265358979323846;
+
+    auto work = [&](int64_t g0, int64_t g1) {
+        for (int64_t g = g0; g < g1; ++g)
+            for (int z = 0; z < kN; ++z)
+                for (int y = 0; y < kN; ++y)
+                    for (int x = 0; x < kN; ++x) {
+                        const int c = (z * kN + y) * kN + x;
+                        double* u = out + (size_t)g * nf * kNC + c;
+                        const int64_t ci[3] = {(int64_t)pos[3 * g] * kN + x, (int64_t)pos[3 * g + 1] * kN + y,
+                                               (int64_t)pos[3 * g + 2] * kN + z};
+                        Prim w{};
+                        switch (problem) {
+                            case TS_PROBLEM_SOD: {
+                                const bool left = 2 * ci[0] + 1 < nc[0];
+                                w.rho = left ? 1.0 : 0.125;
+                                w.p = left ? 1.0 : 0.1;
+                                break;
+                            }
+                            case TS_PROBLEM_SEDOV: {
+                                bool centre = true;
+                                for (int d = 0; d < 3; ++d)
+                                    if (!(ci[d] == nc[d] / 2 - 1 || ci[d] == nc[d] / 2)) centre = false;
+                                w.rho = 1.0;
+                                w.p = 1e-5;
+                                w.extra_e = centre ? 1.0 / (8.0 * dx * dx * dx) : 0.0;
+                                break;
+                            }
+                            case TS_PROBLEM_RANDOM: {
+                                const uint64_t id = (uint64_t)gids[g];
+                                double r[16];
+                                for (int k = 0; k < nf; ++k) r[k] = cell_value(id, seed, (uint64_t)k * kNC + (uint64_t)c);
+                                const double rho = 0.5 + r[0];
+                                const double vx = r[1] - 0.5, vy = r[2] - 0.5, vz = r[3] - 0.5;
+                                const double pr = 0.5 + r[4];
+                                const double v2 = std::fma(vx, vx, std::fma(vy, vy, vz * vz));
+                                u[0] = rho;
+                                u[kNC] = rho * vx;
+                                u[2 * kNC] = rho * vy;
+                                u[3 * kNC] = rho * vz;
+                                u[4 * kNC] = std::fma(0.5 * rho, v2, pr / (cfg->gamma - 1.0));
+                                u[5 * kNC] = 0.5 + r[5];
+                                for (int k = 6; k < nf; ++k) u[k * kNC] = rho * r[k];
+                                continue;
+                            }
+                            case TS_PROBLEM_POLYTROPE: {
+                                double rr[3];
+                                for (int d = 0; d < 3; ++d) {
+                                    const double xc = (ci[d] + 0.5) * dx;
+                                    const double b = std::floor(xc / Lb);
+                                    rr[d] = xc - (b + 0.5) * Lb;
+                                }
+                                const double r = std::sqrt(rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2]);
+                                const double xi = kPi * r / R;
+                                const double th = r < R ? (xi > 1e-12 ? std::sin(xi) / xi : 1.0) : 0.0;
+                                w.rho = std::max(th, 1e-10);
+                                w.p = w.rho * w.rho;  // K = 1, n = 1
+                                if (r < R) {
+                                    w.vx = -0.1 * rr[1];
+                                    w.vy = 0.1 * rr[0];
+                                    const int shell = std::min(4, (int)(5.0 * r / R));
+                                    w.species[shell] = w.rho;
+                                }
+                                break;
+                            }
+                            case TS_PROBLEM_BINARY: {
+                                const double px = (ci[0] + 0.5) * dx, py = (ci[1] + 0.5) * dx, pz = (ci[2] + 0.5) * dx;
+                                const double r1 = std::sqrt((px - x1) * (px - x1) + (py - cy) * (py - cy) + (pz - cz) * (pz - cz));
+                                const double r2 = std::sqrt((px - x2) * (px - x2) + (py - cy) * (py - cy) + (pz - cz) * (pz - cz));
+                                const double t1 = le15(le15.xi1 * r1 / R1), t2 = le15(le15.xi1 * r2 / R2);
+                                const double d1 = rc1 * std::pow(t1, 1.5), d2 = rc2 * std::pow(t2, 1.5);
+                                w.rho = std::max(d1 + d2, 1e-10);
+                                w.p = std::pow(w.rho, 5.0 / 3.0);
+                                if (d1 + d2 > 0.0) {
+                                    w.vx = -0.1 * (py - cy);
+                                    w.vy = 0.1 * (px - cxm);
+                                }
+                                w.species[0] = d1;
+                                w.species[1] = d2;
+                                break;
+                            }
+                        }
+                        store(*cfg, u, w, nf);
+                    }
+    };
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 64));
+    std::vector<std::thread> th;
+    for (int64_t t = 1; t < nt; ++t) th.emplace_back(work, n * t / nt, n * (t + 1) / nt);
+    work(0, n / nt);
+    for (auto& x : th) x.join();
+    return TS_OK;
+}
