@@ -148,6 +148,8 @@ int ts_hydro_ic_fill(const ts_hydro_config* cfg, int32_t problem, int64_t n, con
 /* U^n <- host (owned sub-grids [first, first+count) in owned order). */
 int ts_hydro_upload(ts_hydro_ctx* ctx, int64_t first, int64_t count, const double* host);
 int ts_hydro_download(ts_hydro_ctx* ctx, int64_t first, int64_t count, double* host);
+/* Diagnostic: any of the three RK buffers (0 = U^n, 1 = U^(1), 2 = U^(2)). */
+int ts_hydro_download_buffer(ts_hydro_ctx* ctx, int32_t which, int64_t first, int64_t count, double* host);
 /* Device-side synthetic state (cell_value generator, workload.cpp:329-332). */
 int ts_hydro_init_random(ts_hydro_ctx* ctx, uint64_t seed);
 

@@ -257,11 +257,15 @@ static void side_flux(const orc_params* p, int axis, const double* u, double* f,
     const double rho = u[0], sx = u[1], sy = u[2], sz = u[3], E = u[4];
     const double inv = 1.0 / rho;
     const double vx = sx * inv, vy = sy * inv, vz = sz * inv;
-    const double ke2 = fma(sx, vx, fma(sy, vy, sz * vz));
+    /* |s|^2/rho summed normal component first, then the two transverse ones
+     * in x, y, z order: the same expression for every sweep direction */
+    const double s3[3] = {sx, sy, sz}, v3[3] = {vx, vy, vz};
+    const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
+    const double ke2 = fma(s3[axis], v3[axis], fma(s3[t1], v3[t1], s3[t2] * v3[t2]));
     double pr = (p->gamma - 1.0) * fma(-0.5, ke2, E);
     pr = fmax(pr, p->p_floor);
     const double c = sqrt((p->gamma * pr) * inv);
-    const double v = axis == 0 ? vx : (axis == 1 ? vy : vz);
+    const double v = v3[axis];
     *a = fabs(v) + c;
     *vn = v;
     f[0] = u[1 + axis];

@@ -22,8 +22,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
-BUILD = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libts_hydro.so")
+# Tuning builds: TS_VARIANT=name TS_DEFINES="-DTS_MINB=8" -> build_name/ + libts_hydro_name.so
+VARIANT = os.environ.get("TS_VARIANT", "")
+BUILD = os.path.join(PKG, "build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(PKG, "libts_hydro" + (f"_{VARIANT}" if VARIANT else "") + ".so")
+EXTRA = os.environ.get("TS_DEFINES", "").split()
 
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = shutil.which("nvcc") or os.path.join(CUDA_HOME, "bin", "nvcc")
@@ -51,7 +54,7 @@ def _compile(src: str, force: bool):
     if not force and not _stale(obj, src, _headers()):
         return obj, None
     if src.endswith(".cu"):
-        cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, *EXTRA, "-c", src, "-o", obj]
     else:
         cmd = ["g++", *CXX_FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,6 +1,27 @@
 // hydro_stage.cuh — the fused reconstruct + Kurganov–Tadmor flux + SSP-RK3
-// stage kernel (one sub-grid per 64-thread CTA).  Instantiated once per field
-// count in stage_nf*.cu so the variants build in parallel.
+// stage kernel.  Instantiated once per field count in stage_nf*.cu so the
+// variants build in parallel.
+//
+// Shape: one 8^3 sub-grid per 64-thread CTA.  Each thread owns one pencil
+// (a line of 8 interior cells + 3 ghosts per side) and sweeps x, then y, then
+// z.  Along its pencil it marches face by face: per face it advances the PPM
+// (or minmod) reconstruction of every field by one cell (slopes, interface
+// values, monotonicity limiter all kept in registers — nothing is recomputed
+// and nothing goes through shared memory), evaluates the KT flux from the two
+// face states, and retires the flux difference of the cell behind it into a
+// shared-memory accumulator dU.  The z sweep fuses the RK stage update: it
+// writes U^(k) straight to HBM and, in stage 3, reduces the cell-centred CFL
+// signal speed of U^{n+1} (warp shuffle + one atomic per warp).  Per stage a
+// sub-grid therefore reads U^(k-1) (own interior + the 3-deep face slabs of its
+// six face neighbours, read in place — the direct_local path of reference
+// workload.cpp:532-536), reads U^n, and writes U^(k): one HBM round trip.
+//
+// The sweep direction is a runtime loop (not unrolled) and the face march is
+// a rolled loop with one-face-ahead prefetch: the code stays small enough for
+// the instruction cache (the fully unrolled first version was ~16k SASS
+// instructions and stalled on instruction fetch).  Momentum components are
+// visited in (normal, transverse-1, transverse-2) order so one code path
+// serves every direction.
 #pragma once
 
 #include <cstdint>
@@ -10,264 +31,257 @@
 
 namespace tsh {
 
-// ---------------------------------------------------------------------------
-// Fused stage kernel
-// ---------------------------------------------------------------------------
+constexpr int kThreads = 64;  // pencils per sweep = threads per CTA
+constexpr int kFA = 6;        // fields marched together: rho, s_n, s_t1, s_t2, E, tau
+constexpr int kFaces = N + 1;
 
-template <int AXIS>
-__device__ __forceinline__ int cell_off(int a, int b, int s) {
-    if (AXIS == 0) return (b * N + a) * N + s;
-    if (AXIS == 1) return (b * N + s) * N + a;
-    return (s * N + b) * N + a;
-}
+// Resident CTAs per SM the register allocation is sized for (tuning knob).
+#ifndef TS_MINB
+#define TS_MINB 6
+#endif
 
-// Shared-memory slot of cell (x, y, z): rows XOR-swizzled by y to spread
-// the x-sweep's column writes over the banks.
-__device__ __forceinline__ int sm_off(int x, int y, int z) { return (z * N + y) * N + (x ^ y); }
-
-template <int AXIS>
-__device__ __forceinline__ int sm_cell(int a, int b, int s) {
-    if (AXIS == 0) return sm_off(s, a, b);
-    if (AXIS == 1) return sm_off(a, s, b);
-    return sm_off(a, b, s);
-}
-
-// 14-cell pencil of one field: own interior + 3 cells of each face neighbour
-// read directly from its interior (the direct_local path of workload.cpp:532-536),
-// or clamped at a domain boundary (outflow).
-template <int AXIS>
-__device__ __forceinline__ void load_pencil(double (&q)[P], const double* __restrict__ own,
-                                            const double* __restrict__ lo,
-                                            const double* __restrict__ hi, int a, int b) {
-    if (AXIS == 0) {
-        const double2* row = reinterpret_cast<const double2*>(own + cell_off<0>(a, b, 0));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double2 v = __ldg(row + k);
-            q[3 + 2 * k] = v.x;
-            q[4 + 2 * k] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int s = 0; s < N; ++s) q[s + 3] = __ldg(own + cell_off<AXIS>(a, b, s));
-    }
-    if (lo != nullptr) {
-#pragma unroll
-        for (int s = 0; s < 3; ++s) q[s] = __ldg(lo + cell_off<AXIS>(a, b, N - 3 + s));
-    } else {
-        q[0] = q[3];
-        q[1] = q[3];
-        q[2] = q[3];
-    }
-    if (hi != nullptr) {
-#pragma unroll
-        for (int s = 0; s < 3; ++s) q[N + 3 + s] = __ldg(hi + cell_off<AXIS>(a, b, s));
-    } else {
-        q[N + 3] = q[N + 2];
-        q[N + 4] = q[N + 2];
-        q[N + 5] = q[N + 2];
-    }
-}
-
-// Running reconstruction state of one field along the pencil.
-struct Recon {
-    double D;     // limited slope of the current cell (PPM)
-    double fc;    // interface value at the current cell's left face (PPM)
-    double hi;    // limited right state of the previous cell
-    double dlast; // q[i+1] - q[i]
+template <int NF>
+struct StageSmem {
+    static constexpr int dU = NF * NC;                           // flux-difference accumulator
+    static constexpr int cache = NF > kFA ? kFaces * 3 * kThreads : 0;  // (vL, vR, a) per face
+    static constexpr int doubles = dU + cache;
 };
 
-// Cells -2, -1 (array 1, 2): leaves state ready for cell 0 (array 3).
+// Shared-memory slot of linear cell offset o = (z*8 + y)*8 + x: rows XOR-swizzled
+// by y so the x sweep's strided column accesses spread over the banks.
+__device__ __forceinline__ int sm_slot(int o) { return o ^ ((o >> 3) & 7); }
+
+struct Pencil {
+    const double* __restrict__ own;  // field 0 of this sub-grid in U^(k-1)
+    const double* __restrict__ lo;   // field 0 of the -axis neighbour (nullptr: outflow)
+    const double* __restrict__ hi;   // field 0 of the +axis neighbour (nullptr: outflow)
+    int base;                        // offset of pencil cell 0 within a field
+    int ss;                          // stride along the pencil
+};
+
+// Address of field 0 at pencil position s (-3 .. 10): the own interior, the
+// face neighbour's interior, or the clamped boundary cell (outflow).  Uniform
+// across the CTA, computed once per face for all fields.
+__device__ __forceinline__ const double* paddr(const Pencil& p, int s) {
+    if (s < 0) return p.lo != nullptr ? p.lo + p.base + (s + N) * p.ss : p.own + p.base;
+    if (s >= N) return p.hi != nullptr ? p.hi + p.base + (s - N) * p.ss : p.own + p.base + (N - 1) * p.ss;
+    return p.own + p.base + s * p.ss;
+}
+
+// Running reconstruction state of one field along the pencil.  On entry to
+// face j (between cells j-1 and j): w0 = q[j], w1 = q[j+1], D = slope(j),
+// fc = interface value at face j, hi = limited right edge of cell j-1,
+// dl = q[j+1] - q[j], qn = the next pencil value (prefetched), wp = q[j-1]
+// (the U^(k-1) value of the cell retired at face j).
+struct Recon {
+    double w0, w1, D, fc, hi, dl, qn, wp;
+};
+
 template <int RECON>
-__device__ __forceinline__ void recon_begin(const double (&q)[P], Recon& r) {
+__device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
     if (RECON == 0) {
-        const double d0 = q[1] - q[0];
-        const double d1 = q[2] - q[1];
-        const double d2 = q[3] - q[2];
+        const double q0 = __ldg(paddr(p, -3) + fo), q1 = __ldg(paddr(p, -2) + fo);
+        const double q2 = __ldg(paddr(p, -1) + fo), q3 = __ldg(paddr(p, 0) + fo);
+        const double q4 = __ldg(paddr(p, 1) + fo);
+        r.qn = __ldg(paddr(p, 2) + fo);
+        const double d0 = q1 - q0, d1 = q2 - q1, d2 = q3 - q2, d3 = q4 - q3;
         const double D1 = mc_slope(d1, d0);
         const double D2 = mc_slope(d2, d1);
-        const double f2 = ppm_face(q[1], q[2], D1, D2);
-        const double d3 = q[4] - q[3];
         const double D3 = mc_slope(d3, d2);
-        const double f3 = ppm_face(q[2], q[3], D2, D3);
+        const double f2 = ppm_face(q1, q2, D1, D2);
+        const double f3 = ppm_face(q2, q3, D2, D3);
         double l = f2, h = f3;
-        ppm_limit(l, q[2], h);
+        ppm_limit(l, q2, h);
         r.hi = h;
         r.D = D3;
         r.fc = f3;
-        r.dlast = d3;
+        r.dl = d3;
+        r.w0 = q3;
+        r.w1 = q4;
+        r.wp = q2;
     } else {
-        const double d1 = q[2] - q[1];
-        const double d2 = q[3] - q[2];
-        const double s = minmod_slope(d2, d1);
-        r.hi = fma(0.5, s, q[2]);
-        r.dlast = d2;
+        const double q1 = __ldg(paddr(p, -2) + fo), q2 = __ldg(paddr(p, -1) + fo);
+        const double q3 = __ldg(paddr(p, 0) + fo);
+        r.qn = __ldg(paddr(p, 1) + fo);
+        const double s = minmod_slope(q3 - q2, q2 - q1);
+        r.hi = fma(0.5, s, q2);
+        r.dl = q3 - q2;
+        r.w0 = q3;
+        r.wp = q2;
     }
 }
 
-// Advance to cell j (array i = j + 3); returns the states of face j
-// (between cells j-1 and j): uL = right edge of j-1, uR = left edge of j.
-template <int RECON, int J>
-__device__ __forceinline__ void recon_step(const double (&q)[P], Recon& r, double& uL, double& uR) {
-    constexpr int i = J + 3;
+// Advance to face j: returns uL (right edge of cell j-1) and uR (left edge
+// of cell j); `next` is the address (field 0) of the pencil value the next
+// face needs, nullptr after the last.
+template <int RECON>
+__device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r, double& uL, double& uR) {
+    const double q = r.qn;
+    r.qn = next != nullptr ? __ldg(next + fo) : 0.0;
     if (RECON == 0) {
-        const double dn = q[i + 2] - q[i + 1];
-        const double Dn = mc_slope(dn, r.dlast);
-        const double fn = ppm_face(q[i], q[i + 1], r.D, Dn);
+        const double dn = q - r.w1;
+        const double Dn = mc_slope(dn, r.dl);
+        const double fn = ppm_face(r.w0, r.w1, r.D, Dn);
         double l = r.fc, h = fn;
-        ppm_limit(l, q[i], h);
+        ppm_limit(l, r.w0, h);
         uL = r.hi;
         uR = l;
         r.hi = h;
         r.D = Dn;
         r.fc = fn;
-        r.dlast = dn;
+        r.dl = dn;
+        r.wp = r.w0;
+        r.w0 = r.w1;
+        r.w1 = q;
     } else {
-        const double dn = q[i + 1] - q[i];
-        const double s = minmod_slope(dn, r.dlast);
+        const double dn = q - r.w0;
+        const double s = minmod_slope(dn, r.dl);
         uL = r.hi;
-        uR = fma(-0.5, s, q[i]);
-        r.hi = fma(0.5, s, q[i]);
-        r.dlast = dn;
+        uR = fma(-0.5, s, r.w0);
+        r.hi = fma(0.5, s, r.w0);
+        r.dl = dn;
+        r.wp = r.w0;
+        r.w0 = q;
     }
 }
 
-struct SweepCtx {
-    const double* __restrict__ Uprev;
+struct StageCtx {
     const double* __restrict__ Un;
     double* __restrict__ Uout;
-    double* __restrict__ dU;  // shared
-    size_t own;               // element offset of the sub-grid's field 0
-    long long lo, hi;         // element offsets of the face neighbours' field 0, -1 if none
-    int a, b;
+    double* __restrict__ dU;     // shared accumulator
+    double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
+    size_t own;                  // element offset of the sub-grid's field 0
     double dtdx;
     EosParams e;
 };
 
-// Accumulate the flux difference of cell c for field f.
-//   MODE 0: dU  = d            (x sweep)
-//   MODE 1: dU += d            (y sweep)
-//   MODE 2: U_out = RK(U_n, U_prev + dtdx (dU + d))   (z sweep, fused update)
-template <int AXIS, int NF, int MODE, int STAGE>
-__device__ __forceinline__ double accumulate(const SweepCtx& c, int f, int cell, double d,
-                                             double uprev) {
-    const int sm = f * NC + sm_cell<AXIS>(c.a, c.b, cell);
-    if (MODE == 0) {
-        c.dU[sm] = d;
+// Retire the flux difference d of cell offset `o`, field f (uprev = U^(k-1)
+// of that cell, un = its U^n).
+//   mode 0 (x): dU  = d;  mode 1 (y): dU += d;
+//   mode 2 (z): U_out = RK(U_n, U_prev + dtdx (dU + d)).
+template <int STAGE>
+__device__ __forceinline__ double retire(const StageCtx& c, int mode, int f, int o, double d, double uprev,
+                                         double un) {
+    double* slot = c.dU + f * NC + sm_slot(o);
+    if (mode == 0) {
+        *slot = d;
         return 0.0;
-    } else if (MODE == 1) {
-        c.dU[sm] = c.dU[sm] + d;
+    }
+    if (mode == 1) {
+        *slot = *slot + d;
         return 0.0;
+    }
+    const double tot = *slot + d;
+    const double ustar = fma(c.dtdx, tot, uprev);
+    double out;
+    if (STAGE == 1) {
+        out = ustar;
+    } else if (STAGE == 2) {
+        out = fma(0.75, un, 0.25 * ustar);
     } else {
-        const double tot = c.dU[sm] + d;
-        const double ustar = fma(c.dtdx, tot, uprev);
-        const size_t at = c.own + (size_t)f * NC + cell_off<AXIS>(c.a, c.b, cell);
-        double out;
-        if (STAGE == 1) {
-            out = ustar;
-        } else if (STAGE == 2) {
-            out = fma(0.75, __ldg(c.Un + at), 0.25 * ustar);
-        } else {
-            out = fma(1.0 / 3.0, __ldg(c.Un + at), (2.0 / 3.0) * ustar);
-        }
-        c.Uout[at] = out;
-        return out;
+        out = fma(1.0 / 3.0, un, (2.0 / 3.0) * ustar);
     }
+    c.Uout[c.own + (size_t)f * NC + o] = out;
+    return out;
 }
 
-template <int AXIS, int NF, int RECON, int MODE, int STAGE, int J>
-__device__ __forceinline__ void hydro_face(const SweepCtx& c, const double (&q)[5][P], Recon (&r)[5],
-                                           double (&Fprev)[5], double (&vLc)[N + 1],
-                                           double (&vRc)[N + 1], double (&ac)[N + 1], double& amax) {
-    double uL[5], uR[5];
+template <int NF, int RECON, int STAGE>
+__device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mode, const int (&fm)[kFA],
+                                      double& amax) {
+    const int t = threadIdx.x;
+    int fo[kFA];
 #pragma unroll
-    for (int f = 0; f < 5; ++f) recon_step<RECON, J>(q[f], r[f], uL[f], uR[f]);
-    double vL, pL, aL, vR, pR, aR;
-    face_eos<AXIS>(uL, c.e, vL, pL, aL);
-    face_eos<AXIS>(uR, c.e, vR, pR, aR);
-    const double a = fmax(aL, aR);
-    double fL[5], fR[5], F[5];
-    hydro_flux<AXIS>(uL, vL, pL, fL);
-    hydro_flux<AXIS>(uR, vR, pR, fR);
+    for (int k = 0; k < kFA; ++k) fo[k] = fm[k] * NC;
+    Recon r[kFA];
 #pragma unroll
-    for (int f = 0; f < 5; ++f) F[f] = kt(a, uL[f], uR[f], fL[f], fR[f]);
-    if (NF > 5) {
-        vLc[J] = vL;
-        vRc[J] = vR;
-        ac[J] = a;
-    }
-    if (J > 0) {
-        double out[5];
+    for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
+    // U^n of the cell retired at the next face (z sweep, stages 2 and 3)
+    const bool need_un = STAGE > 1 && mode == 2;
+    const double* un_row = c.Un + c.own + p.base;
+    double un[kFA];
 #pragma unroll
-        for (int f = 0; f < 5; ++f)
-            out[f] = accumulate<AXIS, NF, MODE, STAGE>(c, f, J - 1, Fprev[f] - F[f], q[f][J + 2]);
-        if (MODE == 2 && STAGE == 3)
-            amax = fmax(amax, cell_signal_speed(out[0], out[1], out[2], out[3], out[4], c.e));
-    }
-#pragma unroll
-    for (int f = 0; f < 5; ++f) Fprev[f] = F[f];
-}
-
-template <int AXIS, int NF, int RECON, int MODE, int STAGE, int J>
-__device__ __forceinline__ void passive_face(const SweepCtx& c, int f, const double (&q)[P], Recon& r,
-                                             double& Fprev, const double (&vLc)[N + 1],
-                                             const double (&vRc)[N + 1], const double (&ac)[N + 1]) {
-    double uL, uR;
-    recon_step<RECON, J>(q, r, uL, uR);
-    const double F = kt(ac[J], uL, uR, uL * vLc[J], uR * vRc[J]);
-    if (J > 0) accumulate<AXIS, NF, MODE, STAGE>(c, f, J - 1, Fprev - F, q[J + 2]);
-    Fprev = F;
-}
-
-template <int AXIS, int NF, int RECON, int MODE, int STAGE>
-__device__ __forceinline__ void sweep(const SweepCtx& c, double& amax) {
-    const double* lo = c.lo >= 0 ? c.Uprev + c.lo : nullptr;
-    const double* hi = c.hi >= 0 ? c.Uprev + c.hi : nullptr;
-    double vLc[N + 1], vRc[N + 1], ac[N + 1];
-    {
-        double q[5][P];
-#pragma unroll
-        for (int f = 0; f < 5; ++f)
-            load_pencil<AXIS>(q[f], c.Uprev + c.own + (size_t)f * NC, lo ? lo + (size_t)f * NC : nullptr,
-                              hi ? hi + (size_t)f * NC : nullptr, c.a, c.b);
-        Recon r[5];
-#pragma unroll
-        for (int f = 0; f < 5; ++f) recon_begin<RECON>(q[f], r[f]);
-        double Fprev[5];
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 0>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 1>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 2>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 3>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 4>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 5>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 6>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 7>(c, q, r, Fprev, vLc, vRc, ac, amax);
-        hydro_face<AXIS, NF, RECON, MODE, STAGE, 8>(c, q, r, Fprev, vLc, vRc, ac, amax);
-    }
+    for (int k = 0; k < kFA; ++k) un[k] = need_un ? __ldg(un_row + fo[k]) : 0.0;
+    double Fp[kFA];
 #pragma unroll 1
-    for (int f = 5; f < NF; ++f) {
-        double q[P];
-        load_pencil<AXIS>(q, c.Uprev + c.own + (size_t)f * NC, lo ? lo + (size_t)f * NC : nullptr,
-                          hi ? hi + (size_t)f * NC : nullptr, c.a, c.b);
-        Recon r;
-        recon_begin<RECON>(q, r);
-        double Fp;
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 0>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 1>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 2>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 3>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 4>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 5>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 6>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 7>(c, f, q, r, Fp, vLc, vRc, ac);
-        passive_face<AXIS, NF, RECON, MODE, STAGE, 8>(c, f, q, r, Fp, vLc, vRc, ac);
+    for (int j = 0; j < kFaces; ++j) {
+        const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+        double uL[kFA], uR[kFA], up[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) {
+            up[k] = r[k].wp;  // U^(k-1) of cell j-1, the one retired at this face
+            recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+        }
+        // Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
+        const double invL = 1.0 / uL[0], invR = 1.0 / uR[0];
+        const double vL = uL[1] * invL, vR = uR[1] * invR;
+        const double keL = fma(uL[1], vL, fma(uL[2], uL[2] * invL, uL[3] * (uL[3] * invL)));
+        const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
+        const double pL = fmax(c.e.gm1 * fma(-0.5, keL, uL[4]), c.e.p_floor);
+        const double pR = fmax(c.e.gm1 * fma(-0.5, keR, uR[4]), c.e.p_floor);
+        const double aL = fabs(vL) + sqrt((c.e.gamma * pL) * invL);
+        const double aR = fabs(vR) + sqrt((c.e.gamma * pR) * invR);
+        const double a = fmax(aL, aR);
+        double F[kFA];
+        F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
+        F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
+        F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+        F[3] = kt(a, uL[3], uR[3], uL[3] * vL, uR[3] * vR);
+        F[4] = kt(a, uL[4], uR[4], (uL[4] + pL) * vL, (uR[4] + pR) * vR);
+        F[5] = kt(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
+        if (NF > kFA) {
+            c.cache[(j * 3 + 0) * kThreads + t] = vL;
+            c.cache[(j * 3 + 1) * kThreads + t] = vR;
+            c.cache[(j * 3 + 2) * kThreads + t] = a;
+        }
+        if (j > 0) {
+            const int o = p.base + (j - 1) * p.ss;
+            double out[kFA];
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) out[k] = retire<STAGE>(c, mode, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+            if (STAGE == 3 && mode == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
+                amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
+            if (need_un && j < N) {
+#pragma unroll
+                for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + j * p.ss + fo[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
+    }
+    if (NF > kFA) {
+        // passive species: same march, transported with the hydro face data
+#pragma unroll 1
+        for (int f = kFA; f < NF; ++f) {
+            const int fof = f * NC;
+            Recon q;
+            recon_begin<RECON>(p, fof, q);
+            double unf = need_un ? __ldg(un_row + fof) : 0.0;
+            double Fq = 0.0;
+#pragma unroll 1
+            for (int j = 0; j < kFaces; ++j) {
+                const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+                double uL, uR;
+                const double upf = q.wp;
+                recon_step<RECON>(next, fof, q, uL, uR);
+                const double vL = c.cache[(j * 3 + 0) * kThreads + t];
+                const double vR = c.cache[(j * 3 + 1) * kThreads + t];
+                const double a = c.cache[(j * 3 + 2) * kThreads + t];
+                const double F = kt(a, uL, uR, uL * vL, uR * vR);
+                if (j > 0) {
+                    retire<STAGE>(c, mode, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                    if (need_un && j < N) unf = __ldg(un_row + j * p.ss + fof);
+                }
+                Fq = F;
+            }
+        }
     }
 }
 
 template <int NF, int RECON, int STAGE>
-__global__ void __launch_bounds__(64) stage_kernel(StageArgs A) {
-    extern __shared__ double dU[];
-    if (A.stamp != nullptr && threadIdx.x == 0) atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
+__global__ void __launch_bounds__(kThreads, TS_MINB) stage_kernel(StageArgs A) {
+    extern __shared__ double smem[];
+    if (A.stamp != nullptr && threadIdx.x == 0)
+        atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
     const int g = A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x;
     const int t = threadIdx.x;
     const double amax_in = *A.amax_in;
@@ -280,29 +294,34 @@ __global__ void __launch_bounds__(64) stage_kernel(StageArgs A) {
     int nb[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) nb[k] = __ldg(A.nbr + 6 * g + k);
-    SweepCtx c;
-    c.Uprev = A.Uprev;
+
+    StageCtx c;
     c.Un = A.Un;
     c.Uout = A.Uout;
-    c.dU = dU;
+    c.dU = smem;
+    c.cache = smem + StageSmem<NF>::dU;
     c.own = (size_t)g * NF * NC;
-    c.a = t & (N - 1);
-    c.b = t >> 3;
     c.dtdx = dtdx;
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
+    const double* own = A.Uprev + c.own;
+    const int a = t & (N - 1), b = t >> 3;
     double amax = 0.0;
 
-    c.lo = nb[0] >= 0 ? (long long)nb[0] * NF * NC : -1;
-    c.hi = nb[1] >= 0 ? (long long)nb[1] * NF * NC : -1;
-    sweep<0, NF, RECON, 0, STAGE>(c, amax);
-    __syncthreads();
-    c.lo = nb[2] >= 0 ? (long long)nb[2] * NF * NC : -1;
-    c.hi = nb[3] >= 0 ? (long long)nb[3] * NF * NC : -1;
-    sweep<1, NF, RECON, 1, STAGE>(c, amax);
-    __syncthreads();
-    c.lo = nb[4] >= 0 ? (long long)nb[4] * NF * NC : -1;
-    c.hi = nb[5] >= 0 ? (long long)nb[5] * NF * NC : -1;
-    sweep<2, NF, RECON, 2, STAGE>(c, amax);
+#pragma unroll 1
+    for (int axis = 0; axis < 3; ++axis) {
+        const int nlo = axis == 0 ? nb[0] : (axis == 1 ? nb[2] : nb[4]);
+        const int nhi = axis == 0 ? nb[1] : (axis == 1 ? nb[3] : nb[5]);
+        Pencil p;
+        p.own = own;
+        p.lo = nlo >= 0 ? A.Uprev + (size_t)nlo * NF * NC : nullptr;
+        p.hi = nhi >= 0 ? A.Uprev + (size_t)nhi * NF * NC : nullptr;
+        p.base = axis == 0 ? (b * N + a) * N : (axis == 1 ? b * N * N + a : b * N + a);
+        p.ss = axis == 0 ? 1 : (axis == 1 ? N : N * N);
+        // fields in (rho, s_normal, s_t1, s_t2, E, tau) order, t1 < t2
+        const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
+        sweep<NF, RECON, STAGE>(c, p, axis, fm, amax);
+        if (axis < 2) __syncthreads();
+    }
 
     if (STAGE == 3) {
 #pragma unroll
@@ -317,7 +336,7 @@ __global__ void __launch_bounds__(64) stage_kernel(StageArgs A) {
 
 template <int NF, int RECON, int STAGE>
 inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s) {
-    const size_t smem = (size_t)NF * NC * sizeof(double);
+    const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE>,
@@ -325,7 +344,7 @@ inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    stage_kernel<NF, RECON, STAGE><<<n_ctas, 64, smem, s>>>(a);
+    stage_kernel<NF, RECON, STAGE><<<n_ctas, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -302,6 +302,8 @@ int harvest(ts_hydro_ctx* c) {
     c->pending.clear();
     c->next_slot = 0;
     TS_CUDA(c, cudaMemset(c->d_stamps, 0, (size_t)cap * 2 * sizeof(unsigned long long)));
+    // legacy-stream work does not order against our non-blocking streams
+    TS_CUDA(c, cudaDeviceSynchronize());
     return TS_OK;
 }
 
@@ -684,6 +686,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (!rc && (e = cudaMemset(c->d_stamps, 0, (size_t)cfg->activity_buffer_capacity * 2 * 8)) != cudaSuccess)
         rc = cuda_fail(c, e, "cudaMemset");
     if (!rc && (e = cudaMemset(c->d_scal, 0, 8 * sizeof(double))) != cudaSuccess) rc = cuda_fail(c, e, "cudaMemset");
+    if (!rc && (e = cudaDeviceSynchronize()) != cudaSuccess) rc = cuda_fail(c, e, "cudaDeviceSynchronize");
     if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, sizeof(unsigned long long), cudaHostAllocMapped)) !=
                    cudaSuccess)
         rc = cuda_fail(c, e, "cudaHostAlloc");
@@ -911,6 +914,8 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
         if (!re.empty())
             TS_CUDA(c, cudaMemcpy(c->d_recv_entries, re.data(), re.size() * sizeof(int2), cudaMemcpyHostToDevice));
     }
+    // set-up copies ran on the legacy stream: fence them before any kernel
+    TS_CUDA(c, cudaDeviceSynchronize());
     c->steps_done = 0;
     c->dt_valid = false;
     c->have_mesh = true;
@@ -962,8 +967,13 @@ int ts_hydro_upload(ts_hydro_ctx* c, int64_t first, int64_t count, const double*
     if (rc) return rc;
     const size_t per = (size_t)c->nf * kNC;
     const uint64_t t0 = steady_ns();
-    TS_CUDA(c, cudaMemcpy(c->U[0] + (size_t)first * per, host, (size_t)count * per * sizeof(double),
-                          cudaMemcpyHostToDevice));
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    // pageable cudaMemcpy may return before its DMA lands: copy on our stream and wait
+    TS_CUDA(c, cudaMemcpyAsync(c->U[0] + (size_t)first * per, host, (size_t)count * per * sizeof(double),
+                               cudaMemcpyHostToDevice, s));
+    TS_CUDA(c, cudaStreamSynchronize(s));
     record_copy(c, TS_ACTIVITY_COPY_H2D, (uint64_t)count * per * sizeof(double), t0, steady_ns());
     c->dt_valid = false;
     return TS_OK;
@@ -980,9 +990,33 @@ int ts_hydro_download(ts_hydro_ctx* c, int64_t first, int64_t count, double* hos
     if (rc) return rc;
     const size_t per = (size_t)c->nf * kNC;
     const uint64_t t0 = steady_ns();
-    TS_CUDA(c, cudaMemcpy(host, c->U[0] + (size_t)first * per, (size_t)count * per * sizeof(double),
-                          cudaMemcpyDeviceToHost));
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpyAsync(host, c->U[0] + (size_t)first * per, (size_t)count * per * sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+    TS_CUDA(c, cudaStreamSynchronize(s));
     record_copy(c, TS_ACTIVITY_COPY_D2H, (uint64_t)count * per * sizeof(double), t0, steady_ns());
+    return TS_OK;
+}
+
+int ts_hydro_download_buffer(ts_hydro_ctx* c, int32_t which, int64_t first, int64_t count, double* host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (which < 0 || which > 2) return fail(c, TS_EINVAL, "buffer must be 0, 1 or 2");
+    if (first < 0 || count < 0 || first + count > c->n_owned + c->n_proxy || (count > 0 && host == nullptr))
+        return fail(c, TS_EINVAL, "download range outside the local sub-grids");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    const size_t per = (size_t)c->nf * kNC;
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpyAsync(host, c->U[which] + (size_t)first * per, (size_t)count * per * sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+    TS_CUDA(c, cudaStreamSynchronize(s));
     return TS_OK;
 }
 

@@ -28,7 +28,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libts_hydro.so")
+LIB_PATH = os.environ.get("TS_HYDRO_LIB") or os.path.join(HERE, "libts_hydro.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "ts_hydro.h")
 
 N = 8
@@ -118,6 +118,7 @@ _SIGNATURES = {
     "ts_hydro_upload": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _f64p]),
     "ts_hydro_download": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _f64p]),
     "ts_hydro_init_random": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "ts_hydro_download_buffer": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _f64p]),
     "ts_hydro_compute_dt": (ctypes.c_int, [_vp, _f64p]),
     "ts_hydro_step": (ctypes.c_int, [_vp, ctypes.c_uint64]),
     "ts_hydro_step_host": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64]),
@@ -467,6 +468,14 @@ class CudaDevice:
             count = self.local_counts()[0] - first
         out = np.zeros((count, self.nf, NC), np.float64)
         self._check(lib().ts_hydro_download(self._h, first, count, _p(out, _f64p)), "download")
+        return out
+
+    def download_buffer(self, which: int, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        """Diagnostic: RK buffer 0 (U^n), 1 (U^(1)) or 2 (U^(2)), owned + proxy range."""
+        if count is None:
+            count = self.local_counts()[0] - first
+        out = np.zeros((count, self.nf, NC), np.float64)
+        self._check(lib().ts_hydro_download_buffer(self._h, which, first, count, _p(out, _f64p)), "download_buffer")
         return out
 
     def init_random(self, seed: int = 2210) -> None:
