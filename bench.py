@@ -110,7 +110,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0):
+def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0, recon: str = "ppm"):
     """The oracle (CPU restatement of the path) on a bounded sample: an 8^3
     sub-grid piece of the same workload, all host threads."""
     import oracle
@@ -119,7 +119,7 @@ def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0)
     nf = 6 + species
     dx = 1.0 / (edge * 8)
     n = 8
-    p = oracle.params(nf=nf, dx=dx)
+    p = oracle.params(nf=nf, dx=dx, recon={"ppm": 0, "minmod": 1}[recon])
     nbr, pos, _ = oracle.uniform_mesh(n, n, n)
     from paper_2210_06437_b200 import hydro as H
     mesh = H.Mesh(nbr, pos, np.zeros(len(pos), np.int32), 1, (n, n, n))
@@ -144,7 +144,7 @@ def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0)
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="sedov", choices=sorted(WORKLOADS))
     ap.add_argument("--recon", default="ppm", choices=["ppm", "minmod"])
@@ -164,7 +164,7 @@ def main(argv=None):
     if a.impl == "reference":
         if rank != 0:
             return 0
-        cb = cpu_reference(a.workload, a.steps, a.warmup)
+        cb = cpu_reference(a.workload, a.steps, a.warmup, recon=a.recon)
         line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": a.gpus, "steps": cb["steps"],
                 "warmup": a.warmup, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -201,10 +201,14 @@ def main(argv=None):
             import torch.distributed as dist
             dist.barrier()
 
-    # warm-up (untimed)
+    # warm-up (untimed): at least W steps and ~0.5 s of GPU work so clocks settle
     dev.compute_dt()
+    t_w = time.perf_counter()
     dev.step(a.warmup)
     dev.synchronize()
+    while time.perf_counter() - t_w < 0.5:
+        dev.step(a.warmup)
+        dev.synchronize()
     dev.flush_activity()
     barrier()
     dev.synchronize()
@@ -263,7 +267,7 @@ def main(argv=None):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cb = cpu_reference(a.workload, 2, 1, target_s=10.0)
+        cb = cpu_reference(a.workload, 2, 1, target_s=10.0, recon=a.recon)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:

@@ -39,6 +39,12 @@ constexpr int kFaces = N + 1;
 #ifndef TS_MINB
 #define TS_MINB 6
 #endif
+// Face-march unroll (measured on B200: 1 beats 3 — the larger body costs
+// more in scheduling / registers than the window moves it saves).
+#ifndef TS_FACE_UNROLL
+#define TS_FACE_UNROLL 1
+#endif
+constexpr int kFaceUnroll = TS_FACE_UNROLL;
 
 template <int NF>
 struct StageSmem {
@@ -202,7 +208,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
 #pragma unroll
     for (int k = 0; k < kFA; ++k) un[k] = need_un ? __ldg(un_row + fo[k]) : 0.0;
     double Fp[kFA];
-#pragma unroll 1
+#pragma unroll kFaceUnroll
     for (int j = 0; j < kFaces; ++j) {
         const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
         double uL[kFA], uR[kFA], up[kFA];
@@ -216,11 +222,11 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
         const double vL = uL[1] * invL, vR = uR[1] * invR;
         const double keL = fma(uL[1], vL, fma(uL[2], uL[2] * invL, uL[3] * (uL[3] * invL)));
         const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
-        const double pL = fmax(c.e.gm1 * fma(-0.5, keL, uL[4]), c.e.p_floor);
-        const double pR = fmax(c.e.gm1 * fma(-0.5, keR, uR[4]), c.e.p_floor);
+        const double pL = dmax(c.e.gm1 * fma(-0.5, keL, uL[4]), c.e.p_floor);
+        const double pR = dmax(c.e.gm1 * fma(-0.5, keR, uR[4]), c.e.p_floor);
         const double aL = fabs(vL) + sqrt((c.e.gamma * pL) * invL);
         const double aR = fabs(vR) + sqrt((c.e.gamma * pR) * invR);
-        const double a = fmax(aL, aR);
+        const double a = dmax(aL, aR);
         double F[kFA];
         F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
         F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
