@@ -97,7 +97,8 @@ __device__ __forceinline__ int slab_cell(int face, int k) {
 
 __global__ void __launch_bounds__(256) pack_kernel(const double* __restrict__ U, int nf,
                                                    const int2* __restrict__ entries, long long n_entries,
-                                                   double* __restrict__ buf) {
+                                                   double* __restrict__ buf, unsigned long long* stamp) {
+    if (stamp != nullptr && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
     const long long total = n_entries * nf * SLAB;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -108,11 +109,16 @@ __global__ void __launch_bounds__(256) pack_kernel(const double* __restrict__ U,
         const int2 en = entries[e];
         buf[i] = __ldg(U + ((size_t)en.x * nf + f) * NC + slab_cell(en.y, k));
     }
+    if (stamp != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(stamp + 1, globaltimer());
+    }
 }
 
 __global__ void __launch_bounds__(256) unpack_kernel(double* __restrict__ U, int nf,
                                                      const int2* __restrict__ entries, long long n_entries,
-                                                     const double* __restrict__ buf) {
+                                                     const double* __restrict__ buf, unsigned long long* stamp) {
+    if (stamp != nullptr && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
     const long long total = n_entries * nf * SLAB;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -122,6 +128,10 @@ __global__ void __launch_bounds__(256) unpack_kernel(double* __restrict__ U, int
         const long long e = ef / nf;
         const int2 en = entries[e];
         U[((size_t)en.x * nf + f) * NC + slab_cell(en.y, k)] = buf[i];
+    }
+    if (stamp != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(stamp + 1, globaltimer());
     }
 }
 
@@ -256,16 +266,16 @@ cudaError_t launch_init_random(double* U, int nf, const long long* gid, long lon
 }
 
 cudaError_t launch_pack(const double* U, int nf, const int2* entries, long long n, double* buf, int sms,
-                        cudaStream_t s) {
+                        cudaStream_t s, unsigned long long* stamp) {
     if (n <= 0) return cudaSuccess;
-    pack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf);
+    pack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp);
     return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(double* U, int nf, const int2* entries, long long n, const double* buf, int sms,
-                          cudaStream_t s) {
+                          cudaStream_t s, unsigned long long* stamp) {
     if (n <= 0) return cudaSuccess;
-    unpack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf);
+    unpack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp);
     return cudaGetLastError();
 }
 

@@ -28,9 +28,9 @@ cudaError_t launch_signal(const double* U, int nf, long long n_grids, double gam
 cudaError_t launch_init_random(double* U, int nf, const long long* gid, long long n_grids, uint64_t seed,
                                double gamma, int sms, cudaStream_t s);
 cudaError_t launch_pack(const double* U, int nf, const int2* entries, long long n, double* buf, int sms,
-                        cudaStream_t s);
+                        cudaStream_t s, unsigned long long* stamp);
 cudaError_t launch_unpack(double* U, int nf, const int2* entries, long long n, const double* buf, int sms,
-                          cudaStream_t s);
+                          cudaStream_t s, unsigned long long* stamp);
 cudaError_t launch_face_exchange(const double* U, int nf, const int* nbr, long long n_owned, double* ghost,
                                  int sms, cudaStream_t s);
 cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long n_owned, int h,

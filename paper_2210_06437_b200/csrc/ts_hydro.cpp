@@ -43,6 +43,8 @@ constexpr int kSlab = 3 * kN * kN;
 constexpr const char* kNameStage[4] = {"", "hydro_stage1_kernel", "hydro_stage2_kernel",
                                        "hydro_stage3_kernel"};
 constexpr const char* kNameSignal = "signal_speed_kernel";
+constexpr const char* kNamePack = "halo_pack_kernel";
+constexpr const char* kNameUnpack = "halo_unpack_kernel";
 constexpr const char* kNameH2D = "copy_host_to_device";
 constexpr const char* kNameD2H = "copy_device_to_host";
 constexpr const char* kNameAlloc = "device_alloc";
@@ -131,8 +133,8 @@ struct ts_hydro_ctx {
     bool shut = false;
     bool host_only = false;  // device_id = -1: mesh / halo planning only, no compute
 
-    std::vector<cudaStream_t> streams;  // lazily created; [0] compute, [1] comm
-    cudaEvent_t ev_in = nullptr, ev_halo = nullptr, ev_red = nullptr;
+    std::vector<cudaStream_t> streams;  // lazily created; [0] compute, [1] comm, [2] boundary
+    cudaEvent_t ev_in = nullptr, ev_halo = nullptr, ev_red = nullptr, ev_bnd = nullptr;
 
     // mesh
     bool have_mesh = false;
@@ -215,8 +217,16 @@ int guard(ts_hydro_ctx* c) {
 
 int ensure_stream(ts_hydro_ctx* c, uint32_t id, cudaStream_t* out) {
     if (id >= c->streams.size()) return fail(c, TS_EINVAL, "invalid stream id");
-    if (c->streams[id] == nullptr)
-        TS_CUDA(c, cudaStreamCreateWithFlags(&c->streams[id], cudaStreamNonBlocking));
+    if (c->streams[id] == nullptr) {
+        // The halo (1) and boundary (2) streams carry the critical path of a
+        // multi-GPU stage: at the highest priority the CTA scheduler hands them
+        // the first SM slots that interior CTAs free, so NCCL and the unpack are
+        // not starved behind a GPU-filling interior launch.
+        int lo = 0, hi = 0;
+        TS_CUDA(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int prio = (id == 1 || id == 2) ? hi : lo;
+        TS_CUDA(c, cudaStreamCreateWithPriority(&c->streams[id], cudaStreamNonBlocking, prio));
+    }
     *out = c->streams[id];
     return TS_OK;
 }
@@ -479,8 +489,10 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
     int rc = ensure_stream(c, 1, &cs);
     if (rc) return rc;
     if (c->n_send_total > 0) {
-        c->launches++;
-        TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs));
+        unsigned long long* stamp = nullptr;
+        rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNamePack, 1, 0, &stamp);
+        if (rc) return rc;
+        TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs, stamp));
     }
     if (c->comm != nullptr) {
         Nccl& n = nccl();
@@ -498,8 +510,10 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
         TS_NCCL(c, n.GroupEnd());
     }
     if (c->n_recv_total > 0) {
-        c->launches++;
-        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, c->d_recv, c->sms, cs));
+        unsigned long long* stamp = nullptr;
+        rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameUnpack, 1, 0, &stamp);
+        if (rc) return rc;
+        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, c->d_recv, c->sms, cs, stamp));
     }
     return TS_OK;
 }
@@ -524,12 +538,13 @@ int do_compute_dt(ts_hydro_ctx* c) {
 }
 
 int do_step(ts_hydro_ctx* c) {
-    cudaStream_t s, cs;
+    cudaStream_t s, cs, bs;
     int rc = ensure_stream(c, 0, &s);
     if (rc) return rc;
     const bool multi = c->world > 1;
     if (multi) {
         rc = ensure_stream(c, 1, &cs);
+        if (!rc) rc = ensure_stream(c, 2, &bs);
         if (rc) return rc;
     }
     for (int stage = 1; stage <= 3; ++stage) {
@@ -543,22 +558,28 @@ int do_step(ts_hydro_ctx* c) {
             if (rc) return rc;
             continue;
         }
+        // U^(k-1) complete (interior + boundary of the previous stage).  The
+        // interior launch goes first (it needs no halo); the exchange is issued
+        // behind it on the high-priority halo stream (pack -> NCCL -> unpack)
+        // and the boundary sub-grids follow on the high-priority boundary
+        // stream, so they back-fill SMs as interior CTAs retire.
         double* in = const_cast<double*>(a.Uprev);
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
         TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+        TS_CUDA(c, cudaStreamWaitEvent(bs, c->ev_in, 0));
+        rc = launch_stage_list(c, a, stage, c->d_interior, (int64_t)c->interior.size(), 0, 0, 0);
+        if (rc) return rc;
         rc = exchange_on_comm(c, in);
         if (rc) return rc;
         TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
-        // interior sub-grids overlap the exchange; the boundary ones wait for it
-        rc = launch_stage_list(c, a, stage, c->d_interior, (int64_t)c->interior.size(), 0, 0, 0);
-        if (rc) return rc;
-        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+        TS_CUDA(c, cudaStreamWaitEvent(bs, c->ev_halo, 0));
         tsh::StageArgs b = a;
-        b.amax_reset = nullptr;  // the interior launch (or this one if alone) resets
-        if (c->interior.empty()) b.amax_reset = a.amax_reset;
-        if (!c->interior.empty()) b.dt_out = nullptr;
-        rc = launch_stage_list(c, b, stage, c->d_boundary, (int64_t)c->boundary.size(), 0, 0, 0);
+        b.amax_reset = c->interior.empty() ? a.amax_reset : nullptr;
+        b.dt_out = c->interior.empty() ? a.dt_out : nullptr;
+        rc = launch_stage_list(c, b, stage, c->d_boundary, (int64_t)c->boundary.size(), 0, 2, 0);
         if (rc) return rc;
+        TS_CUDA(c, cudaEventRecord(c->ev_bnd, bs));
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_bnd, 0));
     }
     if (multi && c->comm != nullptr) {
         double* slot = c->d_scal + ((c->steps_done & 1) ^ 1);
@@ -677,7 +698,8 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     int rc = TS_OK;
     if ((e = cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming)) != cudaSuccess) {
+        (e = cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming)) != cudaSuccess) {
         rc = cuda_fail(c, e, "cudaEventCreate");
     }
     if (!rc) rc = dalloc(c, &c->d_scal, 8);
@@ -749,6 +771,7 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
         if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
         if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
+        if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
         for (cudaStream_t s : ctx->streams)
             if (s) cudaStreamDestroy(s);
     }

@@ -1,0 +1,42 @@
+"""Cross-GPU halo exchange (NCCL) parity: runs tools/multigpu_check.py under
+torchrun on 2 GPUs when the box has them (gpurun --gpus 2), else skips."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("args", [["--dims", "4", "4", "8"], ["--dims", "2", "4", "4", "--periodic", "xyz", "--species", "5"],
+                                  ["--dims", "4", "2", "6", "--recon", "minmod", "--steps", "2"]])
+def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args):
+    n = _gpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tools", "multigpu_check.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout

@@ -1,0 +1,62 @@
+"""Per-rank kernel timeline of a few steps from the library's own activity
+records (in-kernel globaltimer stamps).  Single GPU or under torchrun:
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29512 tools/timeline.py [--edge 16] [--steps 2]
+"""
+import argparse
+import os
+import sys
+
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2210_06437_b200 import hydro as H  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--edge", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--species", type=int, default=0)
+    a = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    mesh = H.uniform_mesh(a.edge, a.edge, a.edge * world, world=world)
+    dev = H.CudaDevice(H.HydroConfig(device_id=local, dx=1.0 / (8 * a.edge), n_species=a.species))
+    dev.set_mesh(mesh, rank)
+    if world > 1:
+        uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.comm_init(uid[0], world, rank)
+    dev.init_random(1)
+    dev.step(10)
+    dev.synchronize()
+    dev.flush_activity()
+    if world > 1:
+        dist.barrier()
+    ms = dev.time_steps(a.steps)
+    recs = sorted((r for r in dev.flush_activity() if r.kind == "kernel"), key=lambda r: r.start_ns)
+    t0 = recs[0].start_ns if recs else 0
+    lines = [f"rank {rank}: {a.steps} steps in {ms:.3f} ms (event-timed); owned/proxy/interior {dev.local_counts()}"]
+    busy = 0
+    for r in recs:
+        lines.append(f"  {r.name:22s} s{r.stream_id} {(r.start_ns - t0) / 1e3:9.1f} -> {(r.end_ns - t0) / 1e3:9.1f} us"
+                     f"  ({(r.end_ns - r.start_ns) / 1e3:7.1f})")
+    text = "\n".join(lines)
+    if world > 1:
+        out = [None] * world
+        dist.all_gather_object(out, text)
+        if rank == 0:
+            print("\n".join(out))
+        dist.destroy_process_group()
+    else:
+        print(text)
+
+
+if __name__ == "__main__":
+    main()
