@@ -1,0 +1,122 @@
+// ts_hydro_taskscope.hpp — the reference-side binding a taskscope maintainer
+// adds to use the B200 hydro path: a header-only C++ adapter over the C ABI
+// (ts_hydro.h) that speaks the reference's own types.
+//
+//   * CudaHydroDevice::launch_stage(stage, sub-grid, stream, guid) returns a
+//     taskscope::CompletionToken fulfilled from the CUDA host callback once
+//     the fused stage kernel finished — the replacement for the two
+//     SimDevice::launch_kernel awaits in WorkloadSession::fluxes_body
+//     (reference proj/core/src/workload.cpp:544-552, device.hpp:57-58);
+//   * flush_activity(Profiler&) converts ts_activity_record into
+//     taskscope::ActivityRecord on RunClock and calls
+//     Profiler::deliver_activity (device.cpp:127-130, profiler.cpp:298-318);
+//   * ts_hydro error codes become the reference's exception types
+//     (std::invalid_argument / std::runtime_error, device.cpp:26-62).
+//
+// Include it from code that already builds against the reference headers
+// (it needs taskscope/{device,profiler,clock}.hpp); see INTEGRATION.md.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "taskscope/clock.hpp"
+#include "taskscope/device.hpp"
+#include "taskscope/profiler.hpp"
+#include "taskscope/token.hpp"
+#include "ts_hydro.h"
+
+namespace taskscope {
+
+class CudaHydroDevice {
+public:
+    explicit CudaHydroDevice(const ts_hydro_config& cfg, Profiler* sink = nullptr) : sink_(sink) {
+        check(ts_hydro_create(&cfg, &ctx_), "ts_hydro_create");
+    }
+    ~CudaHydroDevice() {
+        if (ctx_ != nullptr) {
+            if (sink_ != nullptr) flush_activity(*sink_);
+            ts_hydro_destroy(ctx_);
+        }
+    }
+    CudaHydroDevice(const CudaHydroDevice&) = delete;
+    CudaHydroDevice& operator=(const CudaHydroDevice&) = delete;
+
+    ts_hydro_ctx* ctx() { return ctx_; }
+
+    // Binds the reference Mesh's neighbour / owner tables (workload.hpp:76-97).
+    void set_mesh(const std::vector<std::int64_t>& neighbor_ids, const std::vector<std::int32_t>& owner,
+                  std::int32_t world_size, std::int32_t rank) {
+        check(ts_hydro_set_mesh(ctx_, static_cast<std::int64_t>(owner.size()), neighbor_ids.data(), owner.data(),
+                                world_size, rank),
+              "set_mesh");
+    }
+
+    // The compute_fluxes drop-in: one fused RK stage of one owned sub-grid.
+    CompletionToken launch_stage(int stage, std::int64_t owned_index, std::uint32_t stream_id, Guid guid) {
+        auto* promise = new PromiseHandle();
+        CompletionToken token = promise->token();
+        const int rc = ts_hydro_launch_stage(ctx_, stage, &owned_index, 1, stream_id, guid, &fulfil, promise);
+        if (rc != TS_OK) {
+            delete promise;
+            check(rc, "launch_stage");
+        }
+        return token;
+    }
+
+    // SimDevice::flush_activity(Profiler&): at-most-once, RunClock timestamps.
+    std::uint64_t flush_activity(Profiler& sink) {
+        std::uint64_t n = 0;
+        check(ts_hydro_flush_activity(ctx_, nullptr, 0, &n), "flush_activity");
+        std::vector<ts_activity_record> recs(n);
+        check(ts_hydro_flush_activity(ctx_, recs.data(), n, &n), "flush_activity");
+        const auto epoch = static_cast<std::uint64_t>(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(RunClock::instance().epoch().time_since_epoch())
+                .count());
+        for (std::uint64_t i = 0; i < n; ++i) {
+            const ts_activity_record& r = recs[i];
+            ActivityRecord a;
+            a.kind = static_cast<ActivityKind>(r.kind);
+            a.name = r.name;
+            a.device_id = r.device_id;
+            a.stream_id = r.stream_id;
+            a.start_ns = r.start_ns > epoch ? r.start_ns - epoch : 0;
+            a.end_ns = r.end_ns > epoch ? r.end_ns - epoch : 0;
+            if (r.has_bytes) a.bytes = r.bytes;
+            a.correlation_guid = r.correlation_guid;
+            sink.deliver_activity(a);
+        }
+        return n;
+    }
+
+    DeviceMemoryState memory_state() const {
+        ts_memory_state m{};
+        ts_hydro_memory_state(ctx_, &m);
+        return DeviceMemoryState{m.current_device_bytes, m.peak_device_bytes, m.current_host_pinned_bytes,
+                                 m.peak_host_pinned_bytes};
+    }
+
+    void shutdown() { check(ts_hydro_shutdown(ctx_), "shutdown"); }
+
+private:
+    static void fulfil(void* user) {
+        auto* promise = static_cast<PromiseHandle*>(user);
+        promise->set_value();
+        delete promise;
+    }
+
+    void check(int rc, const char* what) const {
+        if (rc == TS_OK) return;
+        const std::string msg = std::string(what) + ": " +
+                                (ctx_ != nullptr ? ts_hydro_last_error(ctx_) : ts_hydro_strerror(rc));
+        if (rc == TS_EINVAL) throw std::invalid_argument(msg);
+        throw std::runtime_error(msg);
+    }
+
+    ts_hydro_ctx* ctx_ = nullptr;
+    Profiler* sink_ = nullptr;
+};
+
+}  // namespace taskscope
