@@ -31,16 +31,34 @@
 
 namespace tsh {
 
-constexpr int kThreads = 64;  // pencils per sweep = threads per CTA
+// Pencil-to-lane mapping: one lane per pencil (sweep) or a lane pair
+// (sweep_pair).  Measured on B200: the pair wins once passive species add
+// shared-memory pressure (nf 11: 0.93 -> 1.24 G cell-updates/s), the single
+// lane wins at nf 6 (3.01 vs 2.79).  TS_PAIR = 0 / 1 forces one for all nf.
+#ifndef TS_PAIR
+#define TS_PAIR 2
+#endif
+template <int NF>
+struct Lanes {
+    static constexpr bool pair = TS_PAIR == 2 ? (NF > 6) : (TS_PAIR == 1);
+    static constexpr int threads = 64 * (pair ? 2 : 1);
+    static constexpr int min_blocks = pair ? 4 : 6;
+};
+constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 constexpr int kFA = 6;        // fields marched together: rho, s_n, s_t1, s_t2, E, tau
 constexpr int kFaces = N + 1;
 
 // Resident CTAs per SM the register allocation is sized for (tuning knob).
-#ifndef TS_MINB
-#define TS_MINB 6
+#ifdef TS_MINB
+#define TS_MINB_FOR(NF) TS_MINB
+#else
+#define TS_MINB_FOR(NF) (Lanes<NF>::min_blocks)
 #endif
 // Face-march unroll (measured on B200: 1 beats 3 — the larger body costs
 // more in scheduling / registers than the window moves it saves).
+#ifndef TS_KEEP_DL
+#define TS_KEEP_DL 0
+#endif
 #ifndef TS_FACE_UNROLL
 #define TS_FACE_UNROLL 1
 #endif
@@ -49,7 +67,7 @@ constexpr int kFaceUnroll = TS_FACE_UNROLL;
 template <int NF>
 struct StageSmem {
     static constexpr int dU = NF * NC;                           // flux-difference accumulator
-    static constexpr int cache = NF > kFA ? kFaces * 3 * kThreads : 0;  // (vL, vR, a) per face
+    static constexpr int cache = NF > kFA ? kFaces * 3 * kPencils : 0;  // (vL, vR, a) per face
     static constexpr int doubles = dU + cache;
 };
 
@@ -77,11 +95,24 @@ __device__ __forceinline__ const double* paddr(const Pencil& p, int s) {
 // Running reconstruction state of one field along the pencil.  On entry to
 // face j (between cells j-1 and j): w0 = q[j], w1 = q[j+1], D = slope(j),
 // fc = interface value at face j, hi = limited right edge of cell j-1,
-// dl = q[j+1] - q[j], qn = the next pencil value (prefetched), wp = q[j-1]
+// qn = the next pencil value (prefetched), wp = q[j-1]
 // (the U^(k-1) value of the cell retired at face j).
 struct Recon {
-    double w0, w1, D, fc, hi, dl, qn, wp;
+    double w0, w1, D, fc, hi, qn, wp;
+#if TS_KEEP_DL
+    double dl;
+#endif
 };
+
+// q[j+1] - q[j]: recomputed (one DADD) rather than carried — a carried value
+// costs a register and two moves per face in the rolled march.
+__device__ __forceinline__ double recon_dl(const Recon& r) {
+#if TS_KEEP_DL
+    return r.dl;
+#else
+    return r.w1 - r.w0;
+#endif
+}
 
 template <int RECON>
 __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
@@ -101,7 +132,9 @@ __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
         r.hi = h;
         r.D = D3;
         r.fc = f3;
+#if TS_KEEP_DL
         r.dl = d3;
+#endif
         r.w0 = q3;
         r.w1 = q4;
         r.wp = q2;
@@ -111,7 +144,9 @@ __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
         r.qn = __ldg(paddr(p, 1) + fo);
         const double s = minmod_slope(q3 - q2, q2 - q1);
         r.hi = fma(0.5, s, q2);
+#if TS_KEEP_DL
         r.dl = q3 - q2;
+#endif
         r.w0 = q3;
         r.wp = q2;
     }
@@ -126,7 +161,7 @@ __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r,
     r.qn = next != nullptr ? __ldg(next + fo) : 0.0;
     if (RECON == 0) {
         const double dn = q - r.w1;
-        const double Dn = mc_slope(dn, r.dl);
+        const double Dn = mc_slope(dn, recon_dl(r));
         const double fn = ppm_face(r.w0, r.w1, r.D, Dn);
         double l = r.fc, h = fn;
         ppm_limit(l, r.w0, h);
@@ -135,17 +170,25 @@ __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r,
         r.hi = h;
         r.D = Dn;
         r.fc = fn;
+#if TS_KEEP_DL
         r.dl = dn;
+#endif
         r.wp = r.w0;
         r.w0 = r.w1;
         r.w1 = q;
     } else {
+        // PLM state: w0 = q[j], wp = q[j-1]; the left difference is w0 - wp
         const double dn = q - r.w0;
-        const double s = minmod_slope(dn, r.dl);
+#if TS_KEEP_DL
+        const double dm = r.dl;
+        r.dl = dn;
+#else
+        const double dm = r.w0 - r.wp;
+#endif
+        const double s = minmod_slope(dn, dm);
         uL = r.hi;
         uR = fma(-0.5, s, r.w0);
         r.hi = fma(0.5, s, r.w0);
-        r.dl = dn;
         r.wp = r.w0;
         r.w0 = q;
     }
@@ -191,6 +234,27 @@ __device__ __forceinline__ double retire(const StageCtx& c, int mode, int f, int
     return out;
 }
 
+// Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
+__device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[kFA], const double (&uR)[kFA],
+                                        double (&F)[kFA], double& vL, double& vR, double& a) {
+    const double invL = 1.0 / uL[0], invR = 1.0 / uR[0];
+    vL = uL[1] * invL;
+    vR = uR[1] * invR;
+    const double keL = fma(uL[1], vL, fma(uL[2], uL[2] * invL, uL[3] * (uL[3] * invL)));
+    const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
+    const double pL = dmax(e.gm1 * fma(-0.5, keL, uL[4]), e.p_floor);
+    const double pR = dmax(e.gm1 * fma(-0.5, keR, uR[4]), e.p_floor);
+    const double aL = fabs(vL) + sqrt((e.gamma * pL) * invL);
+    const double aR = fabs(vR) + sqrt((e.gamma * pR) * invR);
+    a = dmax(aL, aR);
+    F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
+    F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
+    F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+    F[3] = kt(a, uL[3], uR[3], uL[3] * vL, uR[3] * vR);
+    F[4] = kt(a, uL[4], uR[4], (uL[4] + pL) * vL, (uR[4] + pR) * vR);
+    F[5] = kt(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
+}
+
 template <int NF, int RECON, int STAGE>
 __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mode, const int (&fm)[kFA],
                                       double& amax) {
@@ -217,27 +281,12 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
             up[k] = r[k].wp;  // U^(k-1) of cell j-1, the one retired at this face
             recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
         }
-        // Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
-        const double invL = 1.0 / uL[0], invR = 1.0 / uR[0];
-        const double vL = uL[1] * invL, vR = uR[1] * invR;
-        const double keL = fma(uL[1], vL, fma(uL[2], uL[2] * invL, uL[3] * (uL[3] * invL)));
-        const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
-        const double pL = dmax(c.e.gm1 * fma(-0.5, keL, uL[4]), c.e.p_floor);
-        const double pR = dmax(c.e.gm1 * fma(-0.5, keR, uR[4]), c.e.p_floor);
-        const double aL = fabs(vL) + sqrt((c.e.gamma * pL) * invL);
-        const double aR = fabs(vR) + sqrt((c.e.gamma * pR) * invR);
-        const double a = dmax(aL, aR);
-        double F[kFA];
-        F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
-        F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
-        F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
-        F[3] = kt(a, uL[3], uR[3], uL[3] * vL, uR[3] * vR);
-        F[4] = kt(a, uL[4], uR[4], (uL[4] + pL) * vL, (uR[4] + pR) * vR);
-        F[5] = kt(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
+        double F[kFA], vL, vR, a;
+        kt_face(c.e, uL, uR, F, vL, vR, a);
         if (NF > kFA) {
-            c.cache[(j * 3 + 0) * kThreads + t] = vL;
-            c.cache[(j * 3 + 1) * kThreads + t] = vR;
-            c.cache[(j * 3 + 2) * kThreads + t] = a;
+            c.cache[(j * 3 + 0) * kPencils + t] = vL;
+            c.cache[(j * 3 + 1) * kPencils + t] = vR;
+            c.cache[(j * 3 + 2) * kPencils + t] = a;
         }
         if (j > 0) {
             const int o = p.base + (j - 1) * p.ss;
@@ -269,9 +318,128 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
                 double uL, uR;
                 const double upf = q.wp;
                 recon_step<RECON>(next, fof, q, uL, uR);
-                const double vL = c.cache[(j * 3 + 0) * kThreads + t];
-                const double vR = c.cache[(j * 3 + 1) * kThreads + t];
-                const double a = c.cache[(j * 3 + 2) * kThreads + t];
+                const double vL = c.cache[(j * 3 + 0) * kPencils + t];
+                const double vR = c.cache[(j * 3 + 1) * kPencils + t];
+                const double a = c.cache[(j * 3 + 2) * kPencils + t];
+                const double F = kt(a, uL, uR, uL * vL, uR * vR);
+                if (j > 0) {
+                    retire<STAGE>(c, mode, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                    if (need_un && j < N) unf = __ldg(un_row + j * p.ss + fof);
+                }
+                Fq = F;
+            }
+        }
+    }
+}
+
+// Lane-pair march.  Lane role 0 owns (rho, s_n, s_t1), role 1 owns (s_t2, E,
+// tau) of the same pencil.  Per face: each lane advances its 3 fields, the
+// pair swaps the face states the other side needs (one shuffle round), role 0
+// evaluates the EOS of the LEFT state and role 1 of the RIGHT state (the
+// division -> square-root chain is split, not duplicated), they swap
+// (v, p, a) and each lane forms the KT fluxes of its own fields.  Same
+// arithmetic, operation by operation, as the single-lane march (bitwise).
+__device__ __forceinline__ double xlane(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+
+template <int NF, int RECON, int STAGE>
+__device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, int mode, const int (&fm)[kFA],
+                                           double& amax) {
+    const int role = threadIdx.x & 1;
+    const int pen = threadIdx.x >> 1;
+    int fmo[3], fo[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        fmo[k] = role ? fm[3 + k] : fm[k];
+        fo[k] = fmo[k] * NC;
+    }
+    Recon r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) recon_begin<RECON>(p, fo[k], r[k]);
+    const bool need_un = STAGE > 1 && mode == 2;
+    const double* un_row = c.Un + c.own + p.base;
+    double un[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) un[k] = need_un ? __ldg(un_row + fo[k]) : 0.0;
+    double Fp[3];
+#pragma unroll kFaceUnroll
+    for (int j = 0; j < kFaces; ++j) {
+        const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+        double uL[3], uR[3], up[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            up[k] = r[k].wp;
+            recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+        }
+        // role 0 needs (s_t2, E) of the left state, role 1 (rho, s_n, s_t1) of the right
+        double y[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y[k] = xlane(role ? uL[k] : uR[k]);
+        const double S0 = role ? y[0] : uL[0];
+        const double S1 = role ? y[1] : uL[1];
+        const double S2 = role ? y[2] : uL[2];
+        const double S3 = role ? uR[0] : y[0];
+        const double S4 = role ? uR[1] : y[1];
+        const double inv = 1.0 / S0;
+        const double v = S1 * inv;
+        const double ke = fma(S1, v, fma(S2, S2 * inv, S3 * (S3 * inv)));
+        const double pr = dmax(c.e.gm1 * fma(-0.5, ke, S4), c.e.p_floor);
+        const double as = fabs(v) + sqrt((c.e.gamma * pr) * inv);
+        const double vo = xlane(v), po = xlane(pr), ao = xlane(as);
+        const double vL = role ? vo : v, vR = role ? v : vo;
+        const double pL = role ? po : pr, pR = role ? pr : po;
+        const double a = dmax(role ? ao : as, role ? as : ao);
+        // physical fluxes of the own fields
+        //   role 0: (s_n, fma(s_n, v, p), s_t1 v)      role 1: (s_t2 v, (E + p) v, tau v)
+        const double fL0 = role ? uL[0] * vL : uL[1];
+        const double fR0 = role ? uR[0] * vR : uR[1];
+        const double fL1 = role ? (uL[1] + pL) * vL : fma(uL[1], vL, pL);
+        const double fR1 = role ? (uR[1] + pR) * vR : fma(uR[1], vR, pR);
+        double F[3];
+        F[0] = kt(a, uL[0], uR[0], fL0, fR0);
+        F[1] = kt(a, uL[1], uR[1], fL1, fR1);
+        F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+        if (NF > kFA && role == 0) {
+            c.cache[(j * 3 + 0) * kPencils + pen] = vL;
+            c.cache[(j * 3 + 1) * kPencils + pen] = vR;
+            c.cache[(j * 3 + 2) * kPencils + pen] = a;
+        }
+        if (j > 0) {
+            const int o = p.base + (j - 1) * p.ss;
+            double out[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) out[k] = retire<STAGE>(c, mode, fmo[k], o, Fp[k] - F[k], up[k], un[k]);
+            if (STAGE == 3 && mode == 2) {
+                // z sweep: role 0 holds (rho, sz, sx), role 1 (sy, E, tau)
+                const double sy = xlane(out[0]), E = xlane(out[1]);
+                if (role == 0) amax = fmax(amax, cell_signal_speed(out[0], out[2], sy, out[1], E, c.e));
+            }
+            if (need_un && j < N) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + j * p.ss + fo[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Fp[k] = F[k];
+    }
+    if (NF > kFA) {
+        __syncwarp();
+        // passive species, alternating between the two lanes of the pair
+#pragma unroll 1
+        for (int f = kFA + role; f < NF; f += 2) {
+            const int fof = f * NC;
+            Recon q;
+            recon_begin<RECON>(p, fof, q);
+            double unf = need_un ? __ldg(un_row + fof) : 0.0;
+            double Fq = 0.0;
+#pragma unroll 1
+            for (int j = 0; j < kFaces; ++j) {
+                const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+                double uL, uR;
+                const double upf = q.wp;
+                recon_step<RECON>(next, fof, q, uL, uR);
+                const double vL = c.cache[(j * 3 + 0) * kPencils + pen];
+                const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
+                const double a = c.cache[(j * 3 + 2) * kPencils + pen];
                 const double F = kt(a, uL, uR, uL * vL, uR * vR);
                 if (j > 0) {
                     retire<STAGE>(c, mode, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
@@ -284,7 +452,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
 }
 
 template <int NF, int RECON, int STAGE>
-__global__ void __launch_bounds__(kThreads, TS_MINB) stage_kernel(StageArgs A) {
+__global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(StageArgs A) {
     extern __shared__ double smem[];
     if (A.stamp != nullptr && threadIdx.x == 0)
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
@@ -297,10 +465,6 @@ __global__ void __launch_bounds__(kThreads, TS_MINB) stage_kernel(StageArgs A) {
         if (A.dt_out != nullptr) *A.dt_out = dt;
         if (A.amax_reset != nullptr) *A.amax_reset = 0.0;
     }
-    int nb[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) nb[k] = __ldg(A.nbr + 6 * g + k);
-
     StageCtx c;
     c.Un = A.Un;
     c.Uout = A.Uout;
@@ -310,13 +474,14 @@ __global__ void __launch_bounds__(kThreads, TS_MINB) stage_kernel(StageArgs A) {
     c.dtdx = dtdx;
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
     const double* own = A.Uprev + c.own;
-    const int a = t & (N - 1), b = t >> 3;
+    const int pen = Lanes<NF>::pair ? t >> 1 : t;
+    const int a = pen & (N - 1), b = pen >> 3;
     double amax = 0.0;
 
 #pragma unroll 1
     for (int axis = 0; axis < 3; ++axis) {
-        const int nlo = axis == 0 ? nb[0] : (axis == 1 ? nb[2] : nb[4]);
-        const int nhi = axis == 0 ? nb[1] : (axis == 1 ? nb[3] : nb[5]);
+        const int nlo = __ldg(A.nbr + 6 * g + 2 * axis);
+        const int nhi = __ldg(A.nbr + 6 * g + 2 * axis + 1);
         Pencil p;
         p.own = own;
         p.lo = nlo >= 0 ? A.Uprev + (size_t)nlo * NF * NC : nullptr;
@@ -325,7 +490,10 @@ __global__ void __launch_bounds__(kThreads, TS_MINB) stage_kernel(StageArgs A) {
         p.ss = axis == 0 ? 1 : (axis == 1 ? N : N * N);
         // fields in (rho, s_normal, s_t1, s_t2, E, tau) order, t1 < t2
         const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
-        sweep<NF, RECON, STAGE>(c, p, axis, fm, amax);
+        if (Lanes<NF>::pair)
+            sweep_pair<NF, RECON, STAGE>(c, p, axis, fm, amax);
+        else
+            sweep<NF, RECON, STAGE>(c, p, axis, fm, amax);
         if (axis < 2) __syncthreads();
     }
 
@@ -350,7 +518,7 @@ inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    stage_kernel<NF, RECON, STAGE><<<n_ctas, kThreads, smem, s>>>(a);
+    stage_kernel<NF, RECON, STAGE><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
