@@ -236,6 +236,26 @@ def main(argv=None):
     achieved = (b_alg_step * a.steps) / (kernel_ns * 1e-9) / 1e9 if kernel_ns > 0 else None
     stage_share = kernel_ns * 1e-6 / ms if ms > 0 else None
 
+    # FP64-pipe view of the same kernel (the limiter in practice)
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_model.json")) as f:
+            fm = json.load(f)
+        per = fm["fp64_instr_per_cell_update"].get(f"{a.recon}_nf{nf}")
+        if per:
+            peak_i = float(fm["fp64_peak_instr_per_s"])
+            fp64 = {"instr_per_cell_update": per, "peak_instr_per_s": peak_i,
+                    "achieved_instr_per_s": value / world * per, "frac": value / world * per / peak_i,
+                    "source": "profiles/fp64_model.json (ncu instruction count x measured FP64 peak)"}
+    except Exception:
+        fp64 = None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{a.workload}_{a.recon}_nf{nf}")
+    except Exception:
+        traffic = None
+
     # end to end: host buffers through the C ABI, H2D + step + D2H every step
     e2e = None
     if not a.no_e2e:
@@ -281,11 +301,12 @@ def main(argv=None):
                        "parallelism": f"domain decomposition over {world} GPU(s), NCCL halos",
                        "l2": f"working set {state_bytes / 2**20:.0f} MiB (3 state buffers) > 126 MiB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "peak_source": peak_kind,
                          "alg_bytes_per_cell_update": 64 * nf,
                          "kernel": "stage_kernel (fused reconstruct + KT flux + RK update)",
-                         "stage_launches": n_stage_launches, "stage_share_of_step": stage_share},
+                         "stage_launches": n_stage_launches, "stage_share_of_step": stage_share,
+                         "fp64": fp64},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e,
