@@ -151,6 +151,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 halo transport: copy engines + stream memory ops over NVLink, or NCCL")
     a = ap.parse_args(argv)
     a.warmup = max(a.warmup, 3)
 
@@ -188,9 +190,14 @@ def main(argv=None):
     session = H.WorkloadSession(mesh, dev, H.StepConfig(num_steps=a.steps), rank=rank)
     if world > 1:
         import torch.distributed as dist
-        obj = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        dev.comm_init(obj[0], world, rank)
+        if a.transport == "nccl":
+            obj = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            dev.comm_init(obj[0], world, rank)
+        else:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, dev.p2p_export())
+            dev.p2p_import(blobs)
     session.load_problem(problem)
     n_owned = dev.local_counts()[0]
     cells_local = n_owned * 512
@@ -298,7 +305,8 @@ def main(argv=None):
             "config": {"workload": f"{a.workload}: {sub_per_gpu} sub-grids (8^3 + 3-deep halo) per GPU, "
                                    f"domain {dims[0]}x{dims[1]}x{dims[2]} sub-grids",
                        "problem": problem, "nf": nf, "recon": a.recon, "total_cells": total_cells,
-                       "parallelism": f"domain decomposition over {world} GPU(s), NCCL halos",
+                       "parallelism": f"domain decomposition over {world} GPU(s)"
+                                      + (f", {a.transport} halos" if world > 1 else ""),
                        "l2": f"working set {state_bytes / 2**20:.0f} MiB (3 state buffers) > 126 MiB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,

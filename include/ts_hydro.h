@@ -190,7 +190,18 @@ int ts_hydro_fill_halo(ts_hydro_ctx* ctx, int32_t depth, double* tiles_host);
 /* Cross-GPU halo transport (NCCL, loaded at run time). */
 int ts_hydro_nccl_unique_id(uint8_t id[128]);
 int ts_hydro_comm_init(ts_hydro_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
-/* One packed-halo exchange of U^n (pack -> grouped send/recv -> unpack). */
+/* NVLink-native transport inside one node (alternative to NCCL): every rank
+ * exports a blob (CUDA IPC handles of its halo receive buffer, flag array and
+ * dt gather array, and where each source rank's slabs land), the blobs are
+ * all-gathered by the host, and each rank imports all of them.  Halos then
+ * move with copy engines straight into the peer's receive buffer, ordered by
+ * stream memory operations (flag write / wait): no SM and no NCCL kernel on
+ * the step's critical path.  Replaces the parcel transport of
+ * send_boundary / handle_boundary (workload.cpp:487-517). */
+uint64_t ts_hydro_p2p_blob_size(void);
+int ts_hydro_p2p_export(ts_hydro_ctx* ctx, void* blob);
+int ts_hydro_p2p_import(ts_hydro_ctx* ctx, const void* blobs, int32_t world);
+/* One packed-halo exchange of U^n (pack -> transfer -> unpack). */
 int ts_hydro_halo_exchange(ts_hydro_ctx* ctx);
 
 /* ---- timing hook -------------------------------------------------------------- */

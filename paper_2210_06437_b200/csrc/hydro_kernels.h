@@ -14,11 +14,27 @@ struct StageArgs {
     const int* nbr;             // [local][6] local neighbour index, -1 = outflow
     const int* list;            // CTA -> local sub-grid (nullable: first + blockIdx.x)
     int first;
-    const double* amax_in;      // signal speed behind this step's dt
+    const double* amax_in;      // signal speed(s) behind this step's dt (max over amax_n values:
+    int amax_n;                 //   one per rank when the P2P transport gathered them)
     double* amax_out;           // stage 3: max signal speed of U^{n+1}
     double* amax_reset;         // stage 1: zeroed (the slot stage 3 accumulates into)
     double* dt_out;             // stage 1: dt of this step
     unsigned long long* stamp;  // [start, end] globaltimer ns of this launch (nullable)
+    // Stage 3, P2P transport: the last CTA of the stage (across the interior
+    // and boundary launches, counted in done_ctr) pushes the rank's final
+    // amax into slot `rank` of every rank's gather array and raises their flags.
+    int push_n;                          // ranks to push to (0: no push)
+    int rank;
+    int total_ctas;
+    unsigned int* done_ctr;
+    double* const* push_gather;          // [push_n] gather arrays (this step's half)
+    unsigned int* const* push_flag;      // [push_n] flag words (nullptr for self)
+    unsigned int seq;
+    // Stage 1, P2P transport, device-side wait: thread 0 of every CTA
+    // acquires the wait_n flag words (>= wait_seq) before reading amax_in.
+    const unsigned int* wait_flags;
+    int wait_n;
+    unsigned int wait_seq;
     double gamma, gm1, cfl, dx, p_floor;
 };
 

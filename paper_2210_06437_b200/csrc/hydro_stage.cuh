@@ -458,7 +458,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
     const int g = A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x;
     const int t = threadIdx.x;
-    const double amax_in = *A.amax_in;
+    if (STAGE == 1 && A.wait_n > 0) {
+        // the peers' stage-3 kernels push their signal-speed maxima and release
+        // these flags (other GPUs, so no same-device kernel interdependence)
+        if (t == 0)
+            for (int q = 0; q < A.wait_n; ++q)
+                if (q != A.rank)
+                    while ((int)(ld_acquire_sys(A.wait_flags + q) - A.wait_seq) < 0) {
+                    }
+        __syncthreads();
+    }
+    double amax_in = A.amax_in[0];
+    for (int i = 1; i < A.amax_n; ++i) amax_in = fmax(amax_in, A.amax_in[i]);
     const double dt = (A.cfl * A.dx) / amax_in;
     const double dtdx = dt / A.dx;
     if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
@@ -501,6 +512,25 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         if ((t & 31) == 0) atomic_max_nonneg(A.amax_out, amax);
+        if (A.push_n > 0) {
+            // dt all-reduce fused into the stage: threadfence-reduction to find
+            // the last CTA, which writes the rank's max into every rank's gather
+            // slot over NVLink and releases their flags (system scope).
+            __syncthreads();
+            if (t == 0) {
+                __threadfence();
+                if (atomicAdd(A.done_ctr, 1u) == (unsigned)A.total_ctas - 1u) {
+                    __threadfence();
+                    const double am = __longlong_as_double(
+                        (long long)atomicAdd(reinterpret_cast<unsigned long long*>(A.amax_out), 0ull));
+                    for (int q = 0; q < A.push_n; ++q) A.push_gather[q][A.rank] = am;
+                    __threadfence_system();
+                    for (int q = 0; q < A.push_n; ++q)
+                        if (A.push_flag[q] != nullptr) atomicExch_system(A.push_flag[q], A.seq);
+                    *A.done_ctr = 0u;
+                }
+            }
+        }
     }
     if (A.stamp != nullptr) {
         __syncthreads();

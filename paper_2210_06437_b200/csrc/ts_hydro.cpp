@@ -14,6 +14,7 @@
 //     reference's ActivityRecord feed (device.cpp:75-103, profiler.cpp:298-318).
 #include "../../include/ts_hydro.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -23,6 +24,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -113,6 +115,52 @@ struct PendingLaunch {
     uint32_t slot;  // stamp slot
 };
 
+// Stream memory operations (driver API, resolved through the runtime so the
+// library needs no link-time libcuda): the P2P transport orders copy-engine
+// halo transfers with flag writes / waits that use no SM at all.
+struct StreamMemOps {
+    bool ok = false;
+    CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+};
+
+StreamMemOps& memops() {
+    static StreamMemOps m;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* w = nullptr;
+        void* v = nullptr;
+        cudaDriverEntryPointQueryResult q1, q2;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess && w && v) {
+            m.write32 = reinterpret_cast<decltype(m.write32)>(w);
+            m.wait32 = reinterpret_cast<decltype(m.wait32)>(v);
+            m.ok = true;
+        }
+    });
+    return m;
+}
+
+constexpr int kMaxRanks = 64;
+constexpr uint32_t kBlobMagic = 0x54535032;  // "TSP2"
+
+// What one rank publishes so its peers can write straight into its memory.
+struct P2PBlob {
+    uint32_t magic;
+    int32_t rank, world, device;
+    cudaIpcMemHandle_t recv, flags, gather;
+    int64_t n_recv_total;
+    int64_t recv_off[kMaxRanks];  // slab offset of the data from source rank q in my receive buffer
+};
+
+struct PeerMap {
+    double* recv = nullptr;    // peer's receive buffer (2 halves)
+    int32_t* flags = nullptr;  // peer's flags: [0, world) halo by source, [world, 2 world) dt gather
+    double* gather = nullptr;  // peer's dt gather: [2][world]
+    int64_t n_recv_total = 0;
+    int64_t recv_off_for_me = 0;
+};
+
 struct Peer {
     int rank = -1;
     std::vector<int64_t> send_pairs;  // (global id, face) flattened
@@ -168,6 +216,18 @@ struct ts_hydro_ctx {
     // comm
     ncclComm_t comm = nullptr;
     int comm_size = 1;
+    bool p2p = false;                 // copy-engine halos + stream memory ops (single node)
+    int32_t* d_flags = nullptr;       // [2 world]
+    double* d_gather = nullptr;       // [2][world]
+    std::vector<PeerMap> pm;          // by rank
+    unsigned int* d_ctr = nullptr;    // stage-3 CTA counter of the fused dt push
+    double** d_push_gather = nullptr; // [2][world] gather arrays (parity halves) of every rank
+    unsigned int** d_push_flag = nullptr;  // [world] dt flag word of every peer (nullptr for self)
+    uint32_t xseq = 0, aseq = 0;      // exchange / dt-gather sequence numbers (same on every rank)
+    bool dt_wait_device = true;       // P2P dt flags acquired by the stage-1 CTAs (else a stream wait)
+    bool dt_pending_device = false;   // the next stage 1 must acquire the flags of aseq
+    const double* amax_src = nullptr; // where this step's dt comes from
+    int amax_n = 1;
 
     // stepping
     uint64_t steps_done = 0;
@@ -274,7 +334,24 @@ void dfree(ts_hydro_ctx* c, T** p) {
     *p = nullptr;
 }
 
+void close_peers(ts_hydro_ctx* c) {
+    for (PeerMap& q : c->pm) {
+        if (q.recv) cudaIpcCloseMemHandle(q.recv);
+        if (q.flags) cudaIpcCloseMemHandle(q.flags);
+        if (q.gather) cudaIpcCloseMemHandle(q.gather);
+        q = PeerMap{};
+    }
+    c->pm.clear();
+    c->p2p = false;
+    dfree(c, &c->d_push_gather);
+    dfree(c, &c->d_push_flag);
+}
+
 void free_mesh(ts_hydro_ctx* c) {
+    close_peers(c);
+    dfree(c, &c->d_flags);
+    dfree(c, &c->d_gather);
+    dfree(c, &c->d_ctr);
     for (auto& b : c->U) dfree(c, &b);
     dfree(c, &c->d_nbr);
     dfree(c, &c->d_interior);
@@ -455,7 +532,8 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     a.list = nullptr;
     a.first = 0;
     const int par = (int)(c->steps_done & 1);
-    a.amax_in = c->d_scal + par;
+    a.amax_in = c->amax_src != nullptr ? c->amax_src : c->d_scal + par;
+    a.amax_n = c->amax_src != nullptr ? c->amax_n : 1;
     a.amax_out = c->d_scal + (par ^ 1);
     a.amax_reset = nullptr;
     a.dt_out = nullptr;
@@ -483,8 +561,10 @@ int launch_stage_list(ts_hydro_ctx* c, tsh::StageArgs a, int stage, const int32_
     return TS_OK;
 }
 
-// Pack -> grouped NCCL send/recv -> unpack of buffer `buf` on the comm stream.
-int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
+// Pack -> transfer -> unpack of buffer `buf` on the comm stream.  Transport:
+// P2P (copy engines into the peer's receive buffer, flag write / wait stream
+// memory ops; double-buffered by exchange parity) or NCCL grouped send/recv.
+int pack_on_comm(ts_hydro_ctx* c, const double* buf) {
     cudaStream_t cs;
     int rc = ensure_stream(c, 1, &cs);
     if (rc) return rc;
@@ -494,9 +574,40 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
         if (rc) return rc;
         TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs, stamp));
     }
-    if (c->comm != nullptr) {
+    return TS_OK;
+}
+
+int exchange_on_comm(ts_hydro_ctx* c, double* buf, bool packed = false) {
+    cudaStream_t cs;
+    int rc = ensure_stream(c, 1, &cs);
+    if (rc) return rc;
+    if (!packed) {
+        rc = pack_on_comm(c, buf);
+        if (rc) return rc;
+    }
+    const size_t per = (size_t)c->nf * kSlab;
+    double* recv = c->d_recv;
+    if (c->p2p) {
+        StreamMemOps& m = memops();
+        const uint32_t seq = ++c->xseq;
+        const int h = (int)(seq & 1);
+        for (const Peer& p : c->peers) {
+            if (p.rank == c->rank || p.n_send == 0) continue;
+            const PeerMap& q = c->pm[(size_t)p.rank];
+            double* dst = q.recv + ((size_t)h * (size_t)q.n_recv_total + (size_t)q.recv_off_for_me) * per;
+            TS_CUDA(c, cudaMemcpyAsync(dst, c->d_send + (size_t)p.send_off * per, (size_t)p.n_send * per * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, cs));
+            if (m.write32(cs, (CUdeviceptr)(q.flags + c->rank), seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWriteValue32 to a peer flag failed");
+        }
+        for (const Peer& p : c->peers) {
+            if (p.rank == c->rank || p.n_recv == 0) continue;
+            if (m.wait32(cs, (CUdeviceptr)(c->d_flags + p.rank), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a halo flag failed");
+        }
+        recv = c->d_recv + (size_t)h * (size_t)c->n_recv_total * per;
+    } else if (c->comm != nullptr) {
         Nccl& n = nccl();
-        const size_t per = (size_t)c->nf * kSlab;
         TS_NCCL(c, n.GroupStart());
         for (const Peer& p : c->peers) {
             if (p.rank == c->rank) continue;
@@ -513,7 +624,47 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf) {
         unsigned long long* stamp = nullptr;
         rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameUnpack, 1, 0, &stamp);
         if (rc) return rc;
-        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, c->d_recv, c->sms, cs, stamp));
+        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, recv, c->sms, cs, stamp));
+    }
+    return TS_OK;
+}
+
+// Global max of one signal speed per rank, on stream `s`.  NCCL: in-place
+// all-reduce (amax_src = slot).  P2P: every rank copies its value into slot
+// `rank` of every peer's gather array (parity-double-buffered) and waits for
+// the peers' flags; the stage kernel takes the max over the gathered values.
+int reduce_amax(ts_hydro_ctx* c, double* slot, cudaStream_t s) {
+    c->amax_src = nullptr;
+    c->amax_n = 1;
+    c->dt_pending_device = false;
+    if (c->world <= 1) return TS_OK;
+    if (c->p2p) {
+        StreamMemOps& m = memops();
+        const uint32_t seq = ++c->aseq;
+        const int h = (int)(seq & 1);
+        double* mine = c->d_gather + (size_t)h * c->world;
+        TS_CUDA(c, cudaMemcpyAsync(mine + c->rank, slot, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        for (int r = 0; r < c->world; ++r) {
+            if (r == c->rank) continue;
+            const PeerMap& q = c->pm[(size_t)r];
+            TS_CUDA(c, cudaMemcpyAsync(q.gather + (size_t)h * c->world + c->rank, slot, sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s));
+            if (m.write32(s, (CUdeviceptr)(q.flags + c->world + c->rank), seq, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWriteValue32 to a peer flag failed");
+        }
+        for (int r = 0; r < c->world; ++r) {
+            if (r == c->rank) continue;
+            if (m.wait32(s, (CUdeviceptr)(c->d_flags + c->world + r), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a dt flag failed");
+        }
+        c->amax_src = mine;
+        c->amax_n = c->world;
+        return TS_OK;
+    }
+    if (c->comm != nullptr && c->comm_size > 1) {
+        Nccl& n = nccl();
+        TS_NCCL(c, n.AllReduce(slot, slot, 1, ncclFloat64, ncclMax, c->comm, s));
     }
     return TS_OK;
 }
@@ -529,10 +680,8 @@ int do_compute_dt(ts_hydro_ctx* c) {
     if (rc) return rc;
     TS_CUDA(c, tsh::launch_signal(c->U[0], c->nf, c->n_owned, c->cfg.gamma, c->cfg.p_floor, slot, stamp,
                                   c->sms, s));
-    if (c->comm != nullptr && c->comm_size > 1) {
-        Nccl& n = nccl();
-        TS_NCCL(c, n.AllReduce(slot, slot, 1, ncclFloat64, ncclMax, c->comm, s));
-    }
+    rc = reduce_amax(c, slot, s);
+    if (rc) return rc;
     c->dt_valid = true;
     return TS_OK;
 }
@@ -547,11 +696,30 @@ int do_step(ts_hydro_ctx* c) {
         if (!rc) rc = ensure_stream(c, 2, &bs);
         if (rc) return rc;
     }
+    const bool fused_push = multi && c->p2p;
+    const uint32_t push_seq = c->aseq + 1;
+    const bool wait_dt = c->dt_pending_device;
+    c->dt_pending_device = false;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
         if (stage == 1) {
             a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+        }
+        if (stage == 1 && wait_dt) {
+            a.wait_flags = reinterpret_cast<const unsigned int*>(c->d_flags + c->world);
+            a.wait_n = c->world;
+            a.wait_seq = c->aseq;
+            a.rank = c->rank;
+        }
+        if (stage == 3 && fused_push) {
+            a.push_n = c->world;
+            a.rank = c->rank;
+            a.total_ctas = (int)c->n_owned;
+            a.done_ctr = c->d_ctr;
+            a.push_gather = c->d_push_gather + (size_t)(push_seq & 1) * c->world;
+            a.push_flag = c->d_push_flag;
+            a.seq = push_seq;
         }
         if (!multi) {
             rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0);
@@ -567,9 +735,13 @@ int do_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
         TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
         TS_CUDA(c, cudaStreamWaitEvent(bs, c->ev_in, 0));
+        // the (tiny) pack kernel is issued first so it is not queued behind a
+        // GPU-filling interior launch for an SM slot
+        rc = pack_on_comm(c, in);
+        if (rc) return rc;
         rc = launch_stage_list(c, a, stage, c->d_interior, (int64_t)c->interior.size(), 0, 0, 0);
         if (rc) return rc;
-        rc = exchange_on_comm(c, in);
+        rc = exchange_on_comm(c, in, /*packed=*/true);
         if (rc) return rc;
         TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
         TS_CUDA(c, cudaStreamWaitEvent(bs, c->ev_halo, 0));
@@ -581,14 +753,32 @@ int do_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaEventRecord(c->ev_bnd, bs));
         TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_bnd, 0));
     }
-    if (multi && c->comm != nullptr) {
+    if (fused_push) {
+        // the stage-3 kernels pushed this rank's max; wait (no SM) for the peers'
+        c->aseq = push_seq;
+        if (c->dt_wait_device) {
+            c->dt_pending_device = true;  // the next stage-1 CTAs acquire the peers' flags
+        } else {
+            StreamMemOps& m = memops();
+            for (int r = 0; r < c->world; ++r) {
+                if (r == c->rank) continue;
+                if (m.wait32(s, (CUdeviceptr)(c->d_flags + c->world + r), push_seq, CU_STREAM_WAIT_VALUE_GEQ) !=
+                    CUDA_SUCCESS)
+                    return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a dt flag failed");
+            }
+        }
+        c->amax_src = c->d_gather + (size_t)(push_seq & 1) * c->world;
+        c->amax_n = c->world;
+    } else if (multi) {
         double* slot = c->d_scal + ((c->steps_done & 1) ^ 1);
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
         TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
-        Nccl& n = nccl();
-        TS_NCCL(c, n.AllReduce(slot, slot, 1, ncclFloat64, ncclMax, c->comm, cs));
+        rc = reduce_amax(c, slot, cs);
+        if (rc) return rc;
         TS_CUDA(c, cudaEventRecord(c->ev_red, cs));
         TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_red, 0));
+    } else {
+        c->amax_src = nullptr;
     }
     c->steps_done++;
     return TS_OK;
@@ -682,6 +872,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->cfg = *cfg;
     c->nf = 6 + cfg->n_species;
     c->dev = cfg->device_id;
+    if (const char* w = std::getenv("TS_HYDRO_DT_WAIT")) c->dt_wait_device = std::strcmp(w, "stream") != 0;
     if (cfg->device_id < 0) {
         c->host_only = true;
         *out = c;
@@ -759,6 +950,7 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
             deliver_to_sink(ctx);
             ctx->shut = true;
         }
+        close_peers(ctx);
         if (ctx->comm != nullptr && nccl().loaded) nccl().CommDestroy(ctx->comm);
         ctx->comm = nullptr;
         free_mesh(ctx);
@@ -930,8 +1122,15 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
         rc = dalloc(c, &c->d_send_entries, se.size());
         if (!rc) rc = dalloc(c, &c->d_recv_entries, re.size());
         if (!rc) rc = dalloc(c, &c->d_send, (size_t)c->n_send_total * c->nf * kSlab);
-        if (!rc) rc = dalloc(c, &c->d_recv, (size_t)c->n_recv_total * c->nf * kSlab);
+        // two halves: the P2P transport alternates them by exchange parity
+        if (!rc) rc = dalloc(c, &c->d_recv, 2 * (size_t)c->n_recv_total * c->nf * kSlab);
+        if (!rc) rc = dalloc(c, &c->d_flags, 2 * (size_t)world);
+        if (!rc) rc = dalloc(c, &c->d_gather, 2 * (size_t)world);
+        if (!rc) rc = dalloc(c, &c->d_ctr, 1);
         if (rc) return rc;
+        TS_CUDA(c, cudaMemset(c->d_ctr, 0, sizeof(unsigned int)));
+        TS_CUDA(c, cudaMemset(c->d_flags, 0, 2 * (size_t)world * sizeof(int32_t)));
+        TS_CUDA(c, cudaMemset(c->d_gather, 0, 2 * (size_t)world * sizeof(double)));
         if (!se.empty())
             TS_CUDA(c, cudaMemcpy(c->d_send_entries, se.data(), se.size() * sizeof(int2), cudaMemcpyHostToDevice));
         if (!re.empty())
@@ -941,6 +1140,8 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     TS_CUDA(c, cudaDeviceSynchronize());
     c->steps_done = 0;
     c->dt_valid = false;
+    c->amax_src = nullptr;
+    c->xseq = c->aseq = 0;
     c->have_mesh = true;
     return TS_OK;
 }
@@ -1066,10 +1267,13 @@ int ts_hydro_compute_dt(ts_hydro_ctx* c, double* dt_out) {
     rc = do_compute_dt(c);
     if (rc) return rc;
     if (dt_out != nullptr) {
-        double amax = 0.0;
         cudaStream_t s = c->streams[0];
-        TS_CUDA(c, cudaMemcpyAsync(&amax, c->d_scal + (c->steps_done & 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+        const double* src = c->amax_src != nullptr ? c->amax_src : c->d_scal + (c->steps_done & 1);
+        std::vector<double> v((size_t)(c->amax_src != nullptr ? c->amax_n : 1));
+        TS_CUDA(c, cudaMemcpyAsync(v.data(), src, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
         TS_CUDA(c, cudaStreamSynchronize(s));
+        double amax = v[0];
+        for (double x : v) amax = std::fmax(amax, x);
         *dt_out = (c->cfg.cfl * c->cfg.dx) / amax;
     }
     return TS_OK;
@@ -1080,8 +1284,8 @@ int ts_hydro_step(ts_hydro_ctx* c, uint64_t nsteps) {
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     cudaSetDevice(c->dev);
-    if (c->world > 1 && c->comm == nullptr)
-        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init before stepping");
+    if (c->world > 1 && c->comm == nullptr && !c->p2p)
+        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init or ts_hydro_p2p_import before stepping");
     if (!c->dt_valid) {
         rc = do_compute_dt(c);
         if (rc) return rc;
@@ -1120,8 +1324,8 @@ int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if (ms == nullptr) return fail(c, TS_EINVAL, "null output");
-    if (c->world > 1 && c->comm == nullptr)
-        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init before stepping");
+    if (c->world > 1 && c->comm == nullptr && !c->p2p)
+        return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init or ts_hydro_p2p_import before stepping");
     cudaSetDevice(c->dev);
     cudaStream_t s;
     rc = ensure_stream(c, 0, &s);
@@ -1330,12 +1534,85 @@ int ts_hydro_comm_init(ts_hydro_ctx* c, const uint8_t id[128], int32_t nranks, i
     return TS_OK;
 }
 
+uint64_t ts_hydro_p2p_blob_size(void) { return sizeof(P2PBlob); }
+
+int ts_hydro_p2p_export(ts_hydro_ctx* c, void* blob) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (blob == nullptr) return fail(c, TS_EINVAL, "null blob");
+    if (c->world < 2) return fail(c, TS_ESTATE, "P2P transport needs a multi-rank mesh");
+    if (c->world > kMaxRanks) return fail(c, TS_EINVAL, "too many ranks for the P2P transport");
+    if (!memops().ok) return fail(c, TS_ECUDA, "stream memory operations unavailable");
+    cudaSetDevice(c->dev);
+    P2PBlob b{};
+    b.magic = kBlobMagic;
+    b.rank = c->rank;
+    b.world = c->world;
+    b.device = c->dev;
+    TS_CUDA(c, cudaIpcGetMemHandle(&b.recv, c->d_recv));
+    TS_CUDA(c, cudaIpcGetMemHandle(&b.flags, c->d_flags));
+    TS_CUDA(c, cudaIpcGetMemHandle(&b.gather, c->d_gather));
+    b.n_recv_total = c->n_recv_total;
+    for (const Peer& p : c->peers)
+        if (p.rank >= 0 && p.rank < kMaxRanks) b.recv_off[p.rank] = p.recv_off;
+    std::memcpy(blob, &b, sizeof(b));
+    return TS_OK;
+}
+
+int ts_hydro_p2p_import(ts_hydro_ctx* c, const void* blobs, int32_t world) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (blobs == nullptr || world != c->world) return fail(c, TS_EINVAL, "need one blob per rank of the mesh");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    close_peers(c);
+    c->pm.assign((size_t)world, PeerMap{});
+    const auto* all = static_cast<const P2PBlob*>(blobs);
+    for (int r = 0; r < world; ++r) {
+        const P2PBlob& b = all[r];
+        if (b.magic != kBlobMagic || b.rank != r || b.world != world)
+            return fail(c, TS_EINVAL, "malformed P2P blob for rank " + std::to_string(r));
+        if (r == c->rank) continue;
+        PeerMap& q = c->pm[(size_t)r];
+        void* p = nullptr;
+        TS_CUDA(c, cudaIpcOpenMemHandle(&p, b.recv, cudaIpcMemLazyEnablePeerAccess));
+        q.recv = static_cast<double*>(p);
+        TS_CUDA(c, cudaIpcOpenMemHandle(&p, b.flags, cudaIpcMemLazyEnablePeerAccess));
+        q.flags = static_cast<int32_t*>(p);
+        TS_CUDA(c, cudaIpcOpenMemHandle(&p, b.gather, cudaIpcMemLazyEnablePeerAccess));
+        q.gather = static_cast<double*>(p);
+        q.n_recv_total = b.n_recv_total;
+        q.recv_off_for_me = b.recv_off[c->rank];
+    }
+    {
+        std::vector<double*> pg(2 * (size_t)world);
+        std::vector<unsigned int*> pf((size_t)world, nullptr);
+        for (int h = 0; h < 2; ++h)
+            for (int r = 0; r < world; ++r)
+                pg[(size_t)h * world + r] =
+                    (r == c->rank ? c->d_gather : c->pm[(size_t)r].gather) + (size_t)h * world;
+        for (int r = 0; r < world; ++r)
+            if (r != c->rank) pf[(size_t)r] = reinterpret_cast<unsigned int*>(c->pm[(size_t)r].flags + world + c->rank);
+        rc = dalloc(c, &c->d_push_gather, pg.size());
+        if (!rc) rc = dalloc(c, &c->d_push_flag, pf.size());
+        if (rc) return rc;
+        TS_CUDA(c, cudaMemcpy(c->d_push_gather, pg.data(), pg.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaMemcpy(c->d_push_flag, pf.data(), pf.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaDeviceSynchronize());
+    }
+    c->p2p = true;
+    return TS_OK;
+}
+
 int ts_hydro_halo_exchange(ts_hydro_ctx* c) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if (c->world <= 1) return TS_OK;
-    if (c->comm == nullptr) return fail(c, TS_ESTATE, "ts_hydro_comm_init not called");
+    if (c->comm == nullptr && !c->p2p) return fail(c, TS_ESTATE, "no transport (ts_hydro_comm_init / ts_hydro_p2p_import)");
     cudaSetDevice(c->dev);
     cudaStream_t s;
     rc = ensure_stream(c, 0, &s);

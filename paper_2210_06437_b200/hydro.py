@@ -135,6 +135,9 @@ _SIGNATURES = {
     "ts_hydro_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "ts_hydro_comm_init": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]),
     "ts_hydro_halo_exchange": (ctypes.c_int, [_vp]),
+    "ts_hydro_p2p_blob_size": (ctypes.c_uint64, []),
+    "ts_hydro_p2p_export": (ctypes.c_int, [_vp, ctypes.c_void_p]),
+    "ts_hydro_p2p_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32]),
     "ts_hydro_set_activity_sink": (ctypes.c_int, [_vp, SINK_FN, _vp]),
     "ts_hydro_flush_activity": (ctypes.c_int, [_vp, ctypes.POINTER(_Record), ctypes.c_uint64, _u64p]),
     "ts_hydro_memory_state": (ctypes.c_int, [_vp, ctypes.POINTER(_MemState)]),
@@ -554,6 +557,18 @@ class CudaDevice:
 
     def comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
         self._check(lib().ts_hydro_comm_init(self._h, uid, nranks, rank), "comm_init")
+
+    def p2p_export(self) -> bytes:
+        """This rank's P2P blob (IPC handles + receive offsets) for the all-gather."""
+        n = lib().ts_hydro_p2p_blob_size()
+        buf = ctypes.create_string_buffer(n)
+        self._check(lib().ts_hydro_p2p_export(self._h, buf), "p2p_export")
+        return buf.raw
+
+    def p2p_import(self, blobs: Sequence[bytes]) -> None:
+        """Open every rank's blob (rank order) and switch the halo/dt transport to P2P."""
+        data = b"".join(blobs)
+        self._check(lib().ts_hydro_p2p_import(self._h, data, len(blobs)), "p2p_import")
 
     def halo_exchange(self) -> None:
         self._check(lib().ts_hydro_halo_exchange(self._h), "halo_exchange")

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--species", type=int, default=0)
     ap.add_argument("--recon", default="ppm")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -38,9 +39,14 @@ def main():
     mesh = H.uniform_mesh(*a.dims, periodic=a.periodic, world=world)
     dev = H.CudaDevice(cfg)
     dev.set_mesh(mesh, rank)
-    uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    dev.comm_init(uid[0], world, rank)
+    if a.transport == "nccl":
+        uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.comm_init(uid[0], world, rank)
+    else:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dev.p2p_export())
+        dev.p2p_import(blobs)
     dev.init_random(2210)
     owned = dev.owned_ids()
     n_owned, n_proxy, n_interior = dev.local_counts()
@@ -70,7 +76,7 @@ def main():
     dist.barrier()
     if rank == 0:
         print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
-              f" world={world} dims={a.dims} steps={a.steps} species={a.species}", flush=True)
+              f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}", flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 1 else 1
 

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--edge", type=int, default=16)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--species", type=int, default=0)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -29,10 +30,14 @@ def main():
     mesh = H.uniform_mesh(a.edge, a.edge, a.edge * world, world=world)
     dev = H.CudaDevice(H.HydroConfig(device_id=local, dx=1.0 / (8 * a.edge), n_species=a.species))
     dev.set_mesh(mesh, rank)
-    if world > 1:
+    if world > 1 and a.transport == "nccl":
         uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dev.comm_init(uid[0], world, rank)
+    elif world > 1:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dev.p2p_export())
+        dev.p2p_import(blobs)
     dev.init_random(1)
     dev.step(10)
     dev.synchronize()
