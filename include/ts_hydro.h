@@ -204,6 +204,12 @@ int ts_hydro_p2p_import(ts_hydro_ctx* ctx, const void* blobs, int32_t world);
 /* One packed-halo exchange of U^n (pack -> transfer -> unpack). */
 int ts_hydro_halo_exchange(ts_hydro_ctx* ctx);
 
+/* Diagnostic: bitwise check of the kernels' branch-free reciprocal and square
+ * root against IEEE 1.0/x and sqrt(x) on n random positive doubles with
+ * binary exponents in [-emax, emax]; returns the mismatch counts. */
+int ts_hydro_selftest_math(ts_hydro_ctx* ctx, uint64_t n, uint64_t seed, int32_t emax, uint64_t* bad_rcp,
+                           uint64_t* bad_sqrt);
+
 /* ---- timing hook -------------------------------------------------------------- */
 int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void* user);
 /* SimDevice::flush_activity: waits for in-flight work, returns completed

@@ -202,6 +202,25 @@ __global__ void fill_halo_kernel(const double* __restrict__ U, int nf, const int
 
 __global__ void clock_kernel(unsigned long long* out) { *out = globaltimer(); }
 
+// Bitwise check of the branch-free reciprocal / square root against IEEE
+// 1.0/x and sqrt(x) on mix64-random positive operands with exponents in
+// [-emax, emax] (and a physically typical band when emax is small).
+__global__ void selftest_math_kernel(unsigned long long n, unsigned long long seed, int emax,
+                                     unsigned long long* bad) {
+    unsigned long long nb_rcp = 0, nb_sqrt = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint64_t h = mix64(seed, i);
+        const int ex = (int)((h >> 52) % (2u * (unsigned)emax + 1u)) - emax;
+        const uint64_t bits = ((uint64_t)(ex + 1023) << 52) | (h & 0xFFFFFFFFFFFFFull);
+        const double x = __longlong_as_double((long long)bits);
+        if (__double_as_longlong(rcp_rn(x)) != __double_as_longlong(1.0 / x)) ++nb_rcp;
+        if (__double_as_longlong(sqrt_rn(x)) != __double_as_longlong(sqrt(x))) ++nb_sqrt;
+    }
+    if (nb_rcp) atomicAdd(bad, nb_rcp);
+    if (nb_sqrt) atomicAdd(bad + 1, nb_sqrt);
+}
+
 // ---------------------------------------------------------------------------
 // Host-side launchers
 // ---------------------------------------------------------------------------
@@ -292,6 +311,12 @@ cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long 
     const long long pe = N + 2 * h;
     fill_halo_kernel<<<grid_for(n_owned * nf * pe * pe * pe, 256, sms), 256, 0, s>>>(U, nf, nbr, n_owned, h,
                                                                                     tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
+                                 int sms, cudaStream_t s) {
+    selftest_math_kernel<<<sms * 8, 256, 0, s>>>(n, seed, emax, bad);
     return cudaGetLastError();
 }
 

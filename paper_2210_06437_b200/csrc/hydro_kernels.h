@@ -52,5 +52,7 @@ cudaError_t launch_face_exchange(const double* U, int nf, const int* nbr, long l
 cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long n_owned, int h,
                              double* tiles, int sms, cudaStream_t s);
 cudaError_t launch_clock(unsigned long long* out, cudaStream_t s);
+cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
+                                 int sms, cudaStream_t s);
 
 }  // namespace tsh

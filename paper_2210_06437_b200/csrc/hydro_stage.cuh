@@ -237,15 +237,15 @@ __device__ __forceinline__ double retire(const StageCtx& c, int mode, int f, int
 // Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
 __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[kFA], const double (&uR)[kFA],
                                         double (&F)[kFA], double& vL, double& vR, double& a) {
-    const double invL = 1.0 / uL[0], invR = 1.0 / uR[0];
+    const double invL = eos_rcp(uL[0]), invR = eos_rcp(uR[0]);
     vL = uL[1] * invL;
     vR = uR[1] * invR;
     const double keL = fma(uL[1], vL, fma(uL[2], uL[2] * invL, uL[3] * (uL[3] * invL)));
     const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
     const double pL = dmax(e.gm1 * fma(-0.5, keL, uL[4]), e.p_floor);
     const double pR = dmax(e.gm1 * fma(-0.5, keR, uR[4]), e.p_floor);
-    const double aL = fabs(vL) + sqrt((e.gamma * pL) * invL);
-    const double aR = fabs(vR) + sqrt((e.gamma * pR) * invR);
+    const double aL = fabs(vL) + eos_sqrt((e.gamma * pL) * invL);
+    const double aR = fabs(vR) + eos_sqrt((e.gamma * pR) * invR);
     a = dmax(aL, aR);
     F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
     F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
@@ -379,11 +379,11 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
         const double S2 = role ? y[2] : uL[2];
         const double S3 = role ? uR[0] : y[0];
         const double S4 = role ? uR[1] : y[1];
-        const double inv = 1.0 / S0;
+        const double inv = eos_rcp(S0);
         const double v = S1 * inv;
         const double ke = fma(S1, v, fma(S2, S2 * inv, S3 * (S3 * inv)));
         const double pr = dmax(c.e.gm1 * fma(-0.5, ke, S4), c.e.p_floor);
-        const double as = fabs(v) + sqrt((c.e.gamma * pr) * inv);
+        const double as = fabs(v) + eos_sqrt((c.e.gamma * pr) * inv);
         const double vo = xlane(v), po = xlane(pr), ao = xlane(as);
         const double vL = role ? vo : v, vR = role ? v : vo;
         const double pL = role ? po : pr, pR = role ? pr : po;
@@ -538,8 +538,16 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     }
 }
 
+// Phased variant for nf = 6 (hydro_stage_phased.cuh).
+#ifndef TS_PHASED
+#define TS_PHASED 0
+#endif
+template <int NF, int RECON, int STAGE>
+inline cudaError_t launch_stage_phased_t(const StageArgs& a, int n_ctas, cudaStream_t s);
+
 template <int NF, int RECON, int STAGE>
 inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s) {
+    if constexpr (NF == 6 && TS_PHASED) return launch_stage_phased_t<NF, RECON, STAGE>(a, n_ctas, s);
     const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
     static bool configured = false;
     if (!configured) {

@@ -1534,6 +1534,33 @@ int ts_hydro_comm_init(ts_hydro_ctx* c, const uint8_t id[128], int32_t nranks, i
     return TS_OK;
 }
 
+int ts_hydro_selftest_math(ts_hydro_ctx* c, uint64_t n, uint64_t seed, int32_t emax, uint64_t* bad_rcp,
+                           uint64_t* bad_sqrt) {
+    int rc = guard(c);
+    if (rc) return rc;
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    if (bad_rcp == nullptr || bad_sqrt == nullptr || emax < 1 || emax > 1020)
+        return fail(c, TS_EINVAL, "emax must be in [1, 1020]");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    unsigned long long* d = nullptr;
+    rc = dalloc(c, &d, 2);
+    if (rc) return rc;
+    unsigned long long h[2] = {0, 0};
+    cudaError_t e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = tsh::launch_selftest_math(n, seed, emax, d, c->sms, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    dfree(c, &d);
+    if (e != cudaSuccess) return cuda_fail(c, e, "selftest_math");
+    *bad_rcp = h[0];
+    *bad_sqrt = h[1];
+    return TS_OK;
+}
+
 uint64_t ts_hydro_p2p_blob_size(void) { return sizeof(P2PBlob); }
 
 int ts_hydro_p2p_export(ts_hydro_ctx* c, void* blob) {

@@ -136,6 +136,7 @@ _SIGNATURES = {
     "ts_hydro_comm_init": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]),
     "ts_hydro_halo_exchange": (ctypes.c_int, [_vp]),
     "ts_hydro_p2p_blob_size": (ctypes.c_uint64, []),
+    "ts_hydro_selftest_math": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, _u64p, _u64p]),
     "ts_hydro_p2p_export": (ctypes.c_int, [_vp, ctypes.c_void_p]),
     "ts_hydro_p2p_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32]),
     "ts_hydro_set_activity_sink": (ctypes.c_int, [_vp, SINK_FN, _vp]),
@@ -569,6 +570,13 @@ class CudaDevice:
         """Open every rank's blob (rank order) and switch the halo/dt transport to P2P."""
         data = b"".join(blobs)
         self._check(lib().ts_hydro_p2p_import(self._h, data, len(blobs)), "p2p_import")
+
+    def selftest_math(self, n: int, seed: int = 1, emax: int = 1000):
+        """(rcp mismatches, sqrt mismatches) of the branch-free EOS math vs IEEE on n samples."""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(lib().ts_hydro_selftest_math(self._h, n, seed, emax, ctypes.byref(a), ctypes.byref(b)),
+                    "selftest_math")
+        return a.value, b.value
 
     def halo_exchange(self) -> None:
         self._check(lib().ts_hydro_halo_exchange(self._h), "halo_exchange")
