@@ -154,11 +154,11 @@ __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
 
 // Advance to face j: returns uL (right edge of cell j-1) and uR (left edge
 // of cell j); `next` is the address (field 0) of the pencil value the next
-// face needs, nullptr after the last.
+// face needs (any valid address after the last face).
 template <int RECON>
 __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r, double& uL, double& uR) {
     const double q = r.qn;
-    r.qn = next != nullptr ? __ldg(next + fo) : 0.0;
+    r.qn = __ldg(next + fo);  // `next` is always a valid address (the value is unused after the last face)
     if (RECON == 0) {
         const double dn = q - r.w1;
         const double Dn = mc_slope(dn, recon_dl(r));
@@ -234,6 +234,38 @@ __device__ __forceinline__ double retire(const StageCtx& c, int mode, int f, int
     return out;
 }
 
+template <int MODE, int STAGE>
+__device__ __forceinline__ double retire_m(const StageCtx& c, int f, int o, double d, double uprev, double un) {
+    double* slot = c.dU + f * NC + sm_slot(o);
+    if (MODE == 0) {
+        *slot = d;
+        return 0.0;
+    } else if (MODE == 1) {
+        *slot = *slot + d;
+        return 0.0;
+    } else {
+        const double tot = *slot + d;
+        const double ustar = fma(c.dtdx, tot, uprev);
+        double out;
+        if (STAGE == 1) {
+            out = ustar;
+        } else if (STAGE == 2) {
+            out = fma(0.75, un, 0.25 * ustar);
+        } else {
+            out = fma(1.0 / 3.0, un, (2.0 / 3.0) * ustar);
+        }
+        c.Uout[c.own + (size_t)f * NC + o] = out;
+        return out;
+    }
+}
+
+// Pencil value address for the face after face j (clamped to a valid cell).
+template <int RECON>
+__device__ __forceinline__ const double* next_addr(const Pencil& p, int j) {
+    const int s = j + 3 - RECON;
+    return paddr(p, s < N + 2 ? s : N + 2);
+}
+
 // Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
 __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[kFA], const double (&uR)[kFA],
                                         double (&F)[kFA], double& vL, double& vR, double& a) {
@@ -255,26 +287,42 @@ __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[k
     F[5] = kt(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
 }
 
-template <int NF, int RECON, int STAGE>
-__device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mode, const int (&fm)[kFA],
-                                      double& amax) {
+// Single-lane march, one instantiation per sweep mode (x: init, y:
+// accumulate, z: RK update) so the face loop carries no mode branches; face 0
+// is peeled (it retires nothing) and every prefetch is unconditional.
+template <int NF, int RECON, int STAGE, int MODE>
+__device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
     const int t = threadIdx.x;
+    constexpr bool kUn = STAGE > 1 && MODE == 2;  // U^n needed by the update
     int fo[kFA];
 #pragma unroll
     for (int k = 0; k < kFA; ++k) fo[k] = fm[k] * NC;
     Recon r[kFA];
 #pragma unroll
     for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
-    // U^n of the cell retired at the next face (z sweep, stages 2 and 3)
-    const bool need_un = STAGE > 1 && mode == 2;
     const double* un_row = c.Un + c.own + p.base;
     double un[kFA];
+    if (kUn) {
 #pragma unroll
-    for (int k = 0; k < kFA; ++k) un[k] = need_un ? __ldg(un_row + fo[k]) : 0.0;
+        for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + fo[k]);
+    }
     double Fp[kFA];
+    {  // face 0
+        const double* next = next_addr<RECON>(p, 0);
+        double uL[kFA], uR[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+        double vL, vR, a;
+        kt_face(c.e, uL, uR, Fp, vL, vR, a);
+        if (NF > kFA) {
+            c.cache[(0 * 3 + 0) * kPencils + t] = vL;
+            c.cache[(0 * 3 + 1) * kPencils + t] = vR;
+            c.cache[(0 * 3 + 2) * kPencils + t] = a;
+        }
+    }
 #pragma unroll kFaceUnroll
-    for (int j = 0; j < kFaces; ++j) {
-        const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+    for (int j = 1; j < kFaces; ++j) {
+        const double* next = next_addr<RECON>(p, j);
         double uL[kFA], uR[kFA], up[kFA];
 #pragma unroll
         for (int k = 0; k < kFA; ++k) {
@@ -288,17 +336,16 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
             c.cache[(j * 3 + 1) * kPencils + t] = vR;
             c.cache[(j * 3 + 2) * kPencils + t] = a;
         }
-        if (j > 0) {
-            const int o = p.base + (j - 1) * p.ss;
-            double out[kFA];
+        const int o = p.base + (j - 1) * p.ss;
+        double out[kFA];
 #pragma unroll
-            for (int k = 0; k < kFA; ++k) out[k] = retire<STAGE>(c, mode, fm[k], o, Fp[k] - F[k], up[k], un[k]);
-            if (STAGE == 3 && mode == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
-                amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
-            if (need_un && j < N) {
+        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+        if (STAGE == 3 && MODE == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
+            amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
+        if (kUn) {
+            const int jn = j < N ? j : N - 1;  // cell retired at the next face (a dummy reload after the last)
 #pragma unroll
-                for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + j * p.ss + fo[k]);
-            }
+            for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + jn * p.ss + fo[k]);
         }
 #pragma unroll
         for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
@@ -310,22 +357,24 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, int mo
             const int fof = f * NC;
             Recon q;
             recon_begin<RECON>(p, fof, q);
-            double unf = need_un ? __ldg(un_row + fof) : 0.0;
-            double Fq = 0.0;
+            double unf = kUn ? __ldg(un_row + fof) : 0.0;
+            double Fq;
+            {
+                double uL, uR;
+                recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
+                Fq = kt(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
+            }
 #pragma unroll 1
-            for (int j = 0; j < kFaces; ++j) {
-                const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+            for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
                 const double upf = q.wp;
-                recon_step<RECON>(next, fof, q, uL, uR);
+                recon_step<RECON>(next_addr<RECON>(p, j), fof, q, uL, uR);
                 const double vL = c.cache[(j * 3 + 0) * kPencils + t];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
                 const double a = c.cache[(j * 3 + 2) * kPencils + t];
                 const double F = kt(a, uL, uR, uL * vL, uR * vR);
-                if (j > 0) {
-                    retire<STAGE>(c, mode, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
-                    if (need_un && j < N) unf = __ldg(un_row + j * p.ss + fof);
-                }
+                retire_m<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
         }
@@ -363,7 +412,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
     double Fp[3];
 #pragma unroll kFaceUnroll
     for (int j = 0; j < kFaces; ++j) {
-        const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+        const double* next = next_addr<RECON>(p, j);
         double uL[3], uR[3], up[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -433,7 +482,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
             double Fq = 0.0;
 #pragma unroll 1
             for (int j = 0; j < kFaces; ++j) {
-                const double* next = j < N ? paddr(p, j + 3 - RECON) : nullptr;
+                const double* next = next_addr<RECON>(p, j);
                 double uL, uR;
                 const double upf = q.wp;
                 recon_step<RECON>(next, fof, q, uL, uR);
@@ -503,8 +552,12 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
         if (Lanes<NF>::pair)
             sweep_pair<NF, RECON, STAGE>(c, p, axis, fm, amax);
+        else if (axis == 0)
+            sweep<NF, RECON, STAGE, 0>(c, p, fm, amax);
+        else if (axis == 1)
+            sweep<NF, RECON, STAGE, 1>(c, p, fm, amax);
         else
-            sweep<NF, RECON, STAGE>(c, p, axis, fm, amax);
+            sweep<NF, RECON, STAGE, 2>(c, p, fm, amax);
         if (axis < 2) __syncthreads();
     }
 
