@@ -206,34 +206,8 @@ struct StageCtx {
 
 // Retire the flux difference d of cell offset `o`, field f (uprev = U^(k-1)
 // of that cell, un = its U^n).
-//   mode 0 (x): dU  = d;  mode 1 (y): dU += d;
-//   mode 2 (z): U_out = RK(U_n, U_prev + dtdx (dU + d)).
-template <int STAGE>
-__device__ __forceinline__ double retire(const StageCtx& c, int mode, int f, int o, double d, double uprev,
-                                         double un) {
-    double* slot = c.dU + f * NC + sm_slot(o);
-    if (mode == 0) {
-        *slot = d;
-        return 0.0;
-    }
-    if (mode == 1) {
-        *slot = *slot + d;
-        return 0.0;
-    }
-    const double tot = *slot + d;
-    const double ustar = fma(c.dtdx, tot, uprev);
-    double out;
-    if (STAGE == 1) {
-        out = ustar;
-    } else if (STAGE == 2) {
-        out = fma(0.75, un, 0.25 * ustar);
-    } else {
-        out = fma(1.0 / 3.0, un, (2.0 / 3.0) * ustar);
-    }
-    c.Uout[c.own + (size_t)f * NC + o] = out;
-    return out;
-}
-
+//   MODE 0 (x): dU  = d;  MODE 1 (y): dU += d;
+//   MODE 2 (z): U_out = RK(U_n, U_prev + dtdx (dU + d)).
 template <int MODE, int STAGE>
 __device__ __forceinline__ double retire_m(const StageCtx& c, int f, int o, double d, double uprev, double un) {
     double* slot = c.dU + f * NC + sm_slot(o);
@@ -390,11 +364,11 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 // arithmetic, operation by operation, as the single-lane march (bitwise).
 __device__ __forceinline__ double xlane(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
 
-template <int NF, int RECON, int STAGE>
-__device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, int mode, const int (&fm)[kFA],
-                                           double& amax) {
+template <int NF, int RECON, int STAGE, int MODE>
+__device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
     const int role = threadIdx.x & 1;
     const int pen = threadIdx.x >> 1;
+    constexpr bool kUn = STAGE > 1 && MODE == 2;
     int fmo[3], fo[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -404,13 +378,14 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
     Recon r[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) recon_begin<RECON>(p, fo[k], r[k]);
-    const bool need_un = STAGE > 1 && mode == 2;
     const double* un_row = c.Un + c.own + p.base;
     double un[3];
+    if (kUn) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) un[k] = need_un ? __ldg(un_row + fo[k]) : 0.0;
+        for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + fo[k]);
+    }
     double Fp[3];
-#pragma unroll kFaceUnroll
+#pragma unroll 1
     for (int j = 0; j < kFaces; ++j) {
         const double* next = next_addr<RECON>(p, j);
         double uL[3], uR[3], up[3];
@@ -456,15 +431,16 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
             const int o = p.base + (j - 1) * p.ss;
             double out[3];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) out[k] = retire<STAGE>(c, mode, fmo[k], o, Fp[k] - F[k], up[k], un[k]);
-            if (STAGE == 3 && mode == 2) {
+            for (int k = 0; k < 3; ++k) out[k] = retire_m<MODE, STAGE>(c, fmo[k], o, Fp[k] - F[k], up[k], un[k]);
+            if (STAGE == 3 && MODE == 2) {
                 // z sweep: role 0 holds (rho, sz, sx), role 1 (sy, E, tau)
                 const double sy = xlane(out[0]), E = xlane(out[1]);
                 if (role == 0) amax = fmax(amax, cell_signal_speed(out[0], out[2], sy, out[1], E, c.e));
             }
-            if (need_un && j < N) {
+            if (kUn) {
+                const int jn = j < N ? j : N - 1;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + j * p.ss + fo[k]);
+                for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + jn * p.ss + fo[k]);
             }
         }
 #pragma unroll
@@ -478,22 +454,24 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, i
             const int fof = f * NC;
             Recon q;
             recon_begin<RECON>(p, fof, q);
-            double unf = need_un ? __ldg(un_row + fof) : 0.0;
-            double Fq = 0.0;
+            double unf = kUn ? __ldg(un_row + fof) : 0.0;
+            double Fq;
+            {
+                double uL, uR;
+                recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
+                Fq = kt(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
+            }
 #pragma unroll 1
-            for (int j = 0; j < kFaces; ++j) {
-                const double* next = next_addr<RECON>(p, j);
+            for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
                 const double upf = q.wp;
-                recon_step<RECON>(next, fof, q, uL, uR);
+                recon_step<RECON>(next_addr<RECON>(p, j), fof, q, uL, uR);
                 const double vL = c.cache[(j * 3 + 0) * kPencils + pen];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
                 const double a = c.cache[(j * 3 + 2) * kPencils + pen];
                 const double F = kt(a, uL, uR, uL * vL, uR * vR);
-                if (j > 0) {
-                    retire<STAGE>(c, mode, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
-                    if (need_un && j < N) unf = __ldg(un_row + j * p.ss + fof);
-                }
+                retire_m<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
         }
@@ -550,9 +528,14 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         p.ss = axis == 0 ? 1 : (axis == 1 ? N : N * N);
         // fields in (rho, s_normal, s_t1, s_t2, E, tau) order, t1 < t2
         const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
-        if (Lanes<NF>::pair)
-            sweep_pair<NF, RECON, STAGE>(c, p, axis, fm, amax);
-        else if (axis == 0)
+        if (Lanes<NF>::pair) {
+            if (axis == 0)
+                sweep_pair<NF, RECON, STAGE, 0>(c, p, fm, amax);
+            else if (axis == 1)
+                sweep_pair<NF, RECON, STAGE, 1>(c, p, fm, amax);
+            else
+                sweep_pair<NF, RECON, STAGE, 2>(c, p, fm, amax);
+        } else if (axis == 0)
             sweep<NF, RECON, STAGE, 0>(c, p, fm, amax);
         else if (axis == 1)
             sweep<NF, RECON, STAGE, 1>(c, p, fm, amax);
@@ -591,16 +574,8 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     }
 }
 
-// Phased variant for nf = 6 (hydro_stage_phased.cuh).
-#ifndef TS_PHASED
-#define TS_PHASED 0
-#endif
-template <int NF, int RECON, int STAGE>
-inline cudaError_t launch_stage_phased_t(const StageArgs& a, int n_ctas, cudaStream_t s);
-
 template <int NF, int RECON, int STAGE>
 inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s) {
-    if constexpr (NF == 6 && TS_PHASED) return launch_stage_phased_t<NF, RECON, STAGE>(a, n_ctas, s);
     const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
     static bool configured = false;
     if (!configured) {
