@@ -79,7 +79,27 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if not VARIANT:
+        _build_driver(force)
     return LIB
+
+
+DRIVER_SRC = os.path.join(os.path.dirname(PKG), "tools", "ts_hydro_run.cpp")
+DRIVER = os.path.join(os.path.dirname(PKG), "tools", "ts_hydro_run")
+
+
+def _build_driver(force: bool) -> None:
+    """The native C++ host driver over the C ABI (tools/ts_hydro_run.cpp)."""
+    if not os.path.exists(DRIVER_SRC):
+        return
+    if not force and os.path.exists(DRIVER) and os.path.getmtime(DRIVER) >= max(
+            os.path.getmtime(DRIVER_SRC), os.path.getmtime(LIB)):
+        return
+    cmd = ["g++", "-O2", "-std=c++17", "-Wall", f"-I{INCLUDE}", DRIVER_SRC, f"-L{PKG}", "-l:libts_hydro.so",
+           f"-Wl,-rpath,{PKG}", "-o", DRIVER]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"driver build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
 
 
 def main(argv=None) -> int:

@@ -179,3 +179,16 @@ def test_invalid_configs_are_rejected(hydro):
     for kw in ({"cells_per_edge": 16}, {"n_species": 9}, {"gamma": 1.0}, {"cfl": 0.0}, {"stream_count": 1}):
         with pytest.raises(ValueError):
             hydro.CudaDevice(hydro.HydroConfig(device_id=-1, **kw))
+
+
+def test_native_driver_parses_config_like_the_reference(hydro, tmp_path):
+    """tools/ts_hydro_run (C++ host over the C ABI) rejects unknown keys with the
+    line number, exit code 2 (the reference CLI's usage-error code)."""
+    import subprocess
+    exe = os.path.join(ROOT, "tools", "ts_hydro_run")
+    if not os.path.exists(exe):
+        pytest.skip("driver not built")
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("nx=4\nbogus=1\n")
+    r = subprocess.run([exe, str(bad)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 2 and "line 2: unknown key 'bogus'" in r.stderr
