@@ -11,6 +11,7 @@ struct StageArgs {
     const double* Uprev;        // U^{(k-1)}: owned + proxy sub-grids
     const double* Un;           // U^n (stages 2, 3)
     double* Uout;               // U^{(k)}
+    double* scratch;            // a state buffer free during this stage (species accumulators, nf > 6)
     const int* nbr;             // [local][6] local neighbour index, -1 = outflow
     const int* list;            // CTA -> local sub-grid (nullable: first + blockIdx.x)
     int first;

@@ -66,7 +66,10 @@ constexpr int kFaceUnroll = TS_FACE_UNROLL;
 
 template <int NF>
 struct StageSmem {
-    static constexpr int dU = NF * NC;                           // flux-difference accumulator
+    // Flux-difference accumulator of the marched fields; passive species
+    // (nf > 6) accumulate in a free state buffer instead (StageArgs::scratch)
+    // so the CTA's shared memory stays small enough for 4 resident CTAs.
+    static constexpr int dU = (NF > kFA ? kFA : NF) * NC;
     static constexpr int cache = NF > kFA ? kFaces * 3 * kPencils : 0;  // (vL, vR, a) per face
     static constexpr int doubles = dU + cache;
 };
@@ -197,6 +200,7 @@ __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r,
 struct StageCtx {
     const double* __restrict__ Un;
     double* __restrict__ Uout;
+    double* scr;  // species accumulator of this sub-grid (field-major, like the state)
     double* __restrict__ dU;     // shared accumulator
     double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
     size_t own;                  // element offset of the sub-grid's field 0
@@ -230,6 +234,31 @@ __device__ __forceinline__ double retire_m(const StageCtx& c, int f, int o, doub
         }
         c.Uout[c.own + (size_t)f * NC + o] = out;
         return out;
+    }
+}
+
+// Species retire: the accumulator lives in global scratch; `acc` is this
+// cell's prefetched partial sum (modes 1, 2).
+template <int MODE, int STAGE>
+__device__ __forceinline__ void retire_species(const StageCtx& c, int f, int o, double d, double acc, double uprev,
+                                               double un) {
+    double* slot = c.scr + (size_t)f * NC + o;
+    if (MODE == 0) {
+        *slot = d;
+    } else if (MODE == 1) {
+        *slot = acc + d;
+    } else {
+        const double tot = acc + d;
+        const double ustar = fma(c.dtdx, tot, uprev);
+        double out;
+        if (STAGE == 1) {
+            out = ustar;
+        } else if (STAGE == 2) {
+            out = fma(0.75, un, 0.25 * ustar);
+        } else {
+            out = fma(1.0 / 3.0, un, (2.0 / 3.0) * ustar);
+        }
+        c.Uout[c.own + (size_t)f * NC + o] = out;
     }
 }
 
@@ -329,6 +358,12 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll 1
         for (int f = kFA; f < NF; ++f) {
             const int fof = f * NC;
+            double acc[N];
+            if (MODE > 0) {
+                const double* sp = c.scr + fof + p.base;
+#pragma unroll
+                for (int i = 0; i < N; ++i) acc[i] = sp[i * p.ss];
+            }
             Recon q;
             recon_begin<RECON>(p, fof, q);
             double unf = kUn ? __ldg(un_row + fof) : 0.0;
@@ -338,7 +373,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
             }
-#pragma unroll 1
+#pragma unroll
             for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
                 const double upf = q.wp;
@@ -347,7 +382,8 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
                 const double a = c.cache[(j * 3 + 2) * kPencils + t];
                 const double F = kt(a, uL, uR, uL * vL, uR * vR);
-                retire_m<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
+                                            unf);
                 if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
@@ -452,6 +488,13 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
 #pragma unroll 1
         for (int f = kFA + role; f < NF; f += 2) {
             const int fof = f * NC;
+            // partial sums of this pencil's 8 cells (plain loads: written by this CTA)
+            double acc[N];
+            if (MODE > 0) {
+                const double* sp = c.scr + fof + p.base;
+#pragma unroll
+                for (int i = 0; i < N; ++i) acc[i] = sp[i * p.ss];
+            }
             Recon q;
             recon_begin<RECON>(p, fof, q);
             double unf = kUn ? __ldg(un_row + fof) : 0.0;
@@ -461,7 +504,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
             }
-#pragma unroll 1
+#pragma unroll
             for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
                 const double upf = q.wp;
@@ -470,7 +513,8 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
                 const double a = c.cache[(j * 3 + 2) * kPencils + pen];
                 const double F = kt(a, uL, uR, uL * vL, uR * vR);
-                retire_m<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, upf, unf);
+                retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
+                                            unf);
                 if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
@@ -509,6 +553,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     c.dU = smem;
     c.cache = smem + StageSmem<NF>::dU;
     c.own = (size_t)g * NF * NC;
+    c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
     c.dtdx = dtdx;
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
     const double* own = A.Uprev + c.own;

@@ -528,6 +528,9 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     a.Uprev = stage == 1 ? A : (stage == 2 ? B : C);
     a.Un = A;
     a.Uout = stage == 1 ? B : (stage == 2 ? C : A);
+    // free during the stage: stage 1 writes B (C unused), stage 2 writes C,
+    // stage 3 writes A = U^n in place (B unused)
+    a.scratch = stage == 1 ? C : (stage == 2 ? C : B);
     a.nbr = c->d_nbr;
     a.list = nullptr;
     a.first = 0;
