@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -35,12 +36,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (sub-grids per GPU edge, n_species, problem)
-    "sedov": (16, 0, "sedov"),
-    "polytrope": (32, 5, "polytrope"),
+    # name: (sub-grids per GPU edge, n_species, problem)          weak-scaled along z
+    "sedov": (16, 0, "sedov"),          # configs[1]
+    "polytrope": (32, 5, "polytrope"),  # configs[2]
     "random": (16, 0, "random_device"),
     "random11": (32, 5, "random_device"),
+    # configs[3]: V1309-like binary, FIXED 64 x 64 x 32 sub-grids (131072) split over
+    # the N GPUs (strong scaling; needs N >= 2 for memory-comfortable runs, fits on 1)
+    "binary": (None, 5, "binary"),
 }
+BINARY_DIMS = (64, 64, 32)
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -117,7 +122,7 @@ def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0,
     oracle.build()
     edge, species, problem = WORKLOADS[workload]
     nf = 6 + species
-    dx = 1.0 / (edge * 8)
+    dx = 1.0 / ((edge or BINARY_DIMS[0]) * 8)
     n = 8
     p = oracle.params(nf=nf, dx=dx, recon={"ppm": 0, "minmod": 1}[recon])
     nbr, pos, _ = oracle.uniform_mesh(n, n, n)
@@ -161,7 +166,8 @@ def main(argv=None):
     nf = 6 + species
     metric = "hydro cell-updates/sec (FP64)"
     unit = "cell-updates/s"
-    sub_per_gpu = edge ** 3
+    strong = edge is None
+    sub_per_gpu = (BINARY_DIMS[0] * BINARY_DIMS[1] * BINARY_DIMS[2]) // world if strong else edge ** 3
 
     if a.impl == "reference":
         if rank != 0:
@@ -182,8 +188,8 @@ def main(argv=None):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo", rank=rank, world_size=world)
-    dims = (edge, edge, edge * world)
-    dx = 1.0 / (edge * 8)
+    dims = BINARY_DIMS if strong else (edge, edge, edge * world)
+    dx = 1.0 / (dims[0] * 8)
     mesh = H.uniform_mesh(*dims, world=world)
     cfg = H.HydroConfig(device_id=local_rank, n_species=species, dx=dx, recon=a.recon)
     dev = H.CudaDevice(cfg)
@@ -209,18 +215,31 @@ def main(argv=None):
             dist.barrier()
 
     # warm-up (untimed): at least W steps and ~0.5 s of GPU work so clocks settle
+    # Stepping is collective across ranks, so the number of warm-up calls is
+    # agreed (max over ranks) rather than decided by each rank's own clock.
     dev.compute_dt()
     t_w = time.perf_counter()
     dev.step(a.warmup)
     dev.synchronize()
-    while time.perf_counter() - t_w < 0.5:
+    t_call = time.perf_counter() - t_w
+    extra = int(math.ceil((0.5 - t_call) / t_call)) if t_call < 0.5 else 0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([extra], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra = int(t.item())
+    for _ in range(extra):
         dev.step(a.warmup)
-        dev.synchronize()
-    dev.flush_activity()
-    barrier()
     dev.synchronize()
-    launches0 = dev.launch_count()
+    dev.flush_activity()
+    # the clock sampler (an nvidia-smi child) starts BEFORE the barrier: its
+    # spawn jitter would otherwise skew the ranks' start of the timed region,
+    # and the max over ranks would absorb the skew
     with ClockSampler(local_rank) as clk:
+        barrier()
+        dev.synchronize()
+        launches0 = dev.launch_count()
         ms = dev.time_steps(a.steps)
     launches = dev.launch_count() - launches0
     barrier()
@@ -300,7 +319,8 @@ def main(argv=None):
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{a.workload}: {sub_per_gpu} sub-grids (8^3 + 3-deep halo) per GPU, "
                                    f"domain {dims[0]}x{dims[1]}x{dims[2]} sub-grids",

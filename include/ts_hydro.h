@@ -43,6 +43,7 @@ extern "C" {
 #define TS_ENCCL 4
 #define TS_ENOMEM 5
 #define TS_ESTATE 6     /* call out of order (e.g. stepping before set_mesh) */
+#define TS_ECOMM 7      /* a peer rank did not arrive at a cross-GPU wait within the deadline */
 
 #define TS_RECON_PPM 0     /* PPM, MC-limited slopes + CW84 monotonicity (Octo-Tiger form) */
 #define TS_RECON_MINMOD 1  /* piecewise-linear minmod */

@@ -325,4 +325,36 @@ cudaError_t launch_clock(unsigned long long* out, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Stream-ordered wait for peer flags (P2P transport): one thread acquires
+// flags[q] >= seq for every rank q in `mask`, giving up after wait_ns and
+// reporting through *err (cf. the stage kernels' wait_flag) — a stream
+// memory-op wait could not time out.
+__global__ void wait_flags_kernel(const unsigned int* flags, unsigned long long mask, unsigned int seq,
+                                  unsigned long long* err, unsigned long long wait_ns) {
+    volatile unsigned long long* e = err;
+    for (int q = 0; q < 64; ++q) {
+        if (!((mask >> q) & 1ull)) continue;
+        unsigned long long t0 = 0ull;
+        unsigned int spins = 0;
+        while ((int)(ld_acquire_sys(flags + q) - seq) < 0) {
+            const unsigned long long now = globaltimer();
+            if (t0 == 0ull) {
+                t0 = now;
+                continue;
+            }
+            if (now - t0 > wait_ns || (now - t0 > 100000ull && (++spins & 255u) == 0u && *e != 0ull)) {
+                *e = 1ull;
+                return;
+            }
+        }
+    }
+}
+
+cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
+                              unsigned long long* err, unsigned long long wait_ns, cudaStream_t s) {
+    if (mask == 0ull) return cudaSuccess;
+    wait_flags_kernel<<<1, 1, 0, s>>>(flags, mask, seq, err, wait_ns);
+    return cudaGetLastError();
+}
+
 }  // namespace tsh

@@ -21,21 +21,49 @@ struct StageArgs {
     double* amax_reset;         // stage 1: zeroed (the slot stage 3 accumulates into)
     double* dt_out;             // stage 1: dt of this step
     unsigned long long* stamp;  // [start, end] globaltimer ns of this launch (nullable)
-    // Stage 3, P2P transport: the last CTA of the stage (across the interior
-    // and boundary launches, counted in done_ctr) pushes the rank's final
-    // amax into slot `rank` of every rank's gather array and raises their flags.
-    int push_n;                          // ranks to push to (0: no push)
-    int rank;
+    // Stage 3, multi-rank P2P transport: every CTA counts out in done_ctr
+    // (across all launches of the stage, total_ctas); the last one pushes the
+    // rank's final amax into slot `rank` of every rank's gather array
+    // (push_gather, this step's half), raises their dt flags (push_flag[q],
+    // nullptr for self) to seq, waits for the peers' dt flags (dt_wait[q] >=
+    // seq) and writes the max over its own gather half (gather_own) to
+    // amax_global, the next stage 1's amax_in.  The dt all-reduce is thereby
+    // one CTA's tail: stage 1 starts with the global dt in place.
+    unsigned int* done_ctr;              // nullptr: single rank (no tail)
     int total_ctas;
-    unsigned int* done_ctr;
+    int rank;
+    int push_n;                          // ranks to push the amax to (0: no dt push)
     double* const* push_gather;          // [push_n] gather arrays (this step's half)
-    unsigned int* const* push_flag;      // [push_n] flag words (nullptr for self)
+    unsigned int* const* push_flag;      // [push_n] dt flag words (nullptr for self)
     unsigned int seq;
-    // Stage 1, P2P transport, device-side wait: thread 0 of every CTA
-    // acquires the wait_n flag words (>= wait_seq) before reading amax_in.
-    const unsigned int* wait_flags;
-    int wait_n;
-    unsigned int wait_seq;
+    const unsigned int* dt_wait;         // own dt flags by source rank (nullptr: no wait)
+    const double* gather_own;            // own gather half [push_n]
+    double* amax_global;
+    // P2P transport, fused halo exchange.  The n_boundary sub-grids with a
+    // foreign face neighbour are spread through the front of the launch
+    // (cta_bnd[cta] = their boundary slot b, -1 for interior CTAs).  Each
+    // stores its 3-deep output slabs straight into the proxy slots of the
+    // peers' U^(k) buffers over NVLink (push_tbl[6 b + face] = {peer rank,
+    // peer-local sub-grid} or {-1, -1}); the last one (halo_ctr) releases
+    // halo_flag[q] = halo_seq on every receiving peer.  Boundary CTAs
+    // acquire their own flags (halo_wait, by source rank, for the ranks in
+    // halo_wait_mask, >= halo_wait_seq) before reading proxies; interior CTAs
+    // run meanwhile, so the wait is off the critical path.
+    int n_boundary;
+    const int* cta_bnd;
+    const int2* push_tbl;                // nullptr: no push
+    double* const* push_out;             // [world] peer's buffer of this stage's U^(k)
+    unsigned int* halo_ctr;
+    unsigned int* const* halo_flag;      // [world] (nullptr: no slabs for that rank)
+    int halo_flag_n;
+    unsigned int halo_seq;
+    const unsigned int* halo_wait;       // own halo flags, by source rank
+    unsigned long long halo_wait_mask;
+    unsigned int halo_wait_seq;
+    // Every cross-GPU spin gives up after wait_ns (globaltimer) and sets
+    // *err (mapped host word) instead of hanging the GPU.
+    unsigned long long* err;
+    unsigned long long wait_ns;
     double gamma, gm1, cfl, dx, p_floor;
 };
 
@@ -53,6 +81,8 @@ cudaError_t launch_face_exchange(const double* U, int nf, const int* nbr, long l
 cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long n_owned, int h,
                              double* tiles, int sms, cudaStream_t s);
 cudaError_t launch_clock(unsigned long long* out, cudaStream_t s);
+cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
+                              unsigned long long* err, unsigned long long wait_ns, cudaStream_t s);
 cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
                                  int sms, cudaStream_t s);
 

@@ -522,6 +522,104 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
     }
 }
 
+// Acquire-spin until *flag >= seq (wrapping compare) or the deadline; a
+// timeout (a peer that never arrives: mismatched collective calls) is
+// reported through *err.  *err is mapped host memory: it is read only once a
+// wait has stalled for 100 us (an earlier timeout then ends this one at once),
+// never on the fast path.
+__device__ __forceinline__ void wait_flag(const StageArgs& A, const unsigned int* flag, unsigned int seq) {
+    unsigned long long t0 = 0ull;
+    unsigned int spins = 0;
+    while ((int)(ld_acquire_sys(flag) - seq) < 0) {
+        const unsigned long long now = globaltimer();
+        if (t0 == 0ull) {
+            t0 = now;
+            continue;
+        }
+        if (now - t0 > A.wait_ns ||
+            (A.err != nullptr && now - t0 > 100000ull && (++spins & 255u) == 0u &&
+             *reinterpret_cast<volatile unsigned long long*>(A.err) != 0ull)) {
+            if (A.err != nullptr) *reinterpret_cast<volatile unsigned long long*>(A.err) = 1ull;
+            return;
+        }
+    }
+}
+
+// Fused halo push of one boundary sub-grid (see StageArgs): copy the 3-deep
+// slab of every face with a foreign neighbour from this CTA's fresh U^(k)
+// into the peer's proxy slot (same in-sub-grid layout), then count the CTA
+// out; the last boundary CTA releases the receivers' flags (system scope).
+// Loads are batched ahead of the remote stores (each is an L2 round trip);
+// z slabs are contiguous per field and move as 16-byte vectors.
+__device__ __forceinline__ int slab_offset(int axis, int d0, int k) {
+    if (axis == 0) {
+        const int l = k % 3, m = k / 3;  // m = y + 8 z
+        return m * N + d0 + l;
+    }
+    const int u = k & (N - 1), m = k >> 3;  // axis 1: m = l + 3 z
+    return ((m / 3) * N + d0 + m % 3) * N + u;
+}
+
+template <int NF>
+__device__ __forceinline__ void halo_push(const StageArgs& A, size_t own, int b) {
+    __syncthreads();  // U^(k) of this sub-grid written by the whole CTA
+    const double* __restrict__ src = A.Uout + own;
+    constexpr int kSlabCells = 3 * N * N;
+    constexpr int kBatch = 8;
+    const int nt = (int)blockDim.x;
+    for (int f = 0; f < 6; ++f) {
+        const int2 e = A.push_tbl[6 * b + f];
+        if (e.x < 0) continue;
+        double* __restrict__ dst = A.push_out[e.x] + (size_t)e.y * NF * NC;
+        const int axis = f >> 1, d0 = (f & 1) ? N - 3 : 0;
+        if (axis == 2) {
+            constexpr int kVec = kSlabCells / 2;  // double2 per field
+            const double2* s2 = reinterpret_cast<const double2*>(src + d0 * N * N);
+            double2* t2 = reinterpret_cast<double2*>(dst + d0 * N * N);
+            for (int base = 0; base < NF * kVec; base += nt * kBatch) {
+                double2 v[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int i = base + u * nt + (int)threadIdx.x;
+                    if (i < NF * kVec) v[u] = s2[(i / kVec) * (NC / 2) + i % kVec];
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int i = base + u * nt + (int)threadIdx.x;
+                    if (i < NF * kVec) t2[(i / kVec) * (NC / 2) + i % kVec] = v[u];
+                }
+            }
+        } else {
+            for (int base = 0; base < NF * kSlabCells; base += nt * kBatch) {
+                double v[kBatch];
+                int o[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int i = base + u * nt + (int)threadIdx.x;
+                    const int fld = i / kSlabCells;
+                    o[u] = fld * NC + slab_offset(axis, d0, i - fld * kSlabCells);
+                    if (i < NF * kSlabCells) v[u] = src[o[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+                    if (base + u * nt + (int)threadIdx.x < NF * kSlabCells) dst[o[u]] = v[u];
+            }
+        }
+    }
+    // CTA barrier, then one system-scope fence publishes the whole CTA's
+    // remote stores before the count (the cooperative-groups grid-sync pattern)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(A.halo_ctr, 1u) == (unsigned)A.n_boundary - 1u) {
+            __threadfence_system();
+            for (int q = 0; q < A.halo_flag_n; ++q)
+                if (A.halo_flag[q] != nullptr) atomicExch_system(A.halo_flag[q], A.halo_seq);
+            *A.halo_ctr = 0u;
+        }
+    }
+}
+
 template <int NF, int RECON, int STAGE>
 __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(StageArgs A) {
     extern __shared__ double smem[];
@@ -529,14 +627,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
     const int g = A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x;
     const int t = threadIdx.x;
-    if (STAGE == 1 && A.wait_n > 0) {
-        // the peers' stage-3 kernels push their signal-speed maxima and release
-        // these flags (other GPUs, so no same-device kernel interdependence)
+    if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0) {
+        // proxies of U^(k-1): pushed by the peers' previous-stage boundary CTAs
+        // (released in their first wave, so this rarely spins)
         if (t == 0)
-            for (int q = 0; q < A.wait_n; ++q)
-                if (q != A.rank)
-                    while ((int)(ld_acquire_sys(A.wait_flags + q) - A.wait_seq) < 0) {
-                    }
+            for (int q = 0; q < 64; ++q)
+                if ((A.halo_wait_mask >> q) & 1ull)
+                    wait_flag(A, A.halo_wait + q, A.halo_wait_seq);
         __syncthreads();
     }
     double amax_in = A.amax_in[0];
@@ -588,28 +685,41 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             sweep<NF, RECON, STAGE, 2>(c, p, fm, amax);
         if (axis < 2) __syncthreads();
     }
+    if (A.push_tbl != nullptr) {
+        const int b = __ldg(A.cta_bnd + blockIdx.x);
+        if (b >= 0) halo_push<NF>(A, c.own, b);
+    }
 
     if (STAGE == 3) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         if ((t & 31) == 0) atomic_max_nonneg(A.amax_out, amax);
-        if (A.push_n > 0) {
-            // dt all-reduce fused into the stage: threadfence-reduction to find
-            // the last CTA, which writes the rank's max into every rank's gather
-            // slot over NVLink and releases their flags (system scope).
-            __syncthreads();
-            if (t == 0) {
+    }
+    if (A.done_ctr != nullptr) {
+        // threadfence reduction to the last CTA of the stage (see StageArgs)
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            if (atomicAdd(A.done_ctr, 1u) == (unsigned)A.total_ctas - 1u) {
                 __threadfence();
-                if (atomicAdd(A.done_ctr, 1u) == (unsigned)A.total_ctas - 1u) {
-                    __threadfence();
+                if (STAGE == 3 && A.push_n > 0) {
+                    // dt all-reduce: this rank's max into every rank's gather slot
                     const double am = __longlong_as_double(
                         (long long)atomicAdd(reinterpret_cast<unsigned long long*>(A.amax_out), 0ull));
                     for (int q = 0; q < A.push_n; ++q) A.push_gather[q][A.rank] = am;
                     __threadfence_system();
                     for (int q = 0; q < A.push_n; ++q)
                         if (A.push_flag[q] != nullptr) atomicExch_system(A.push_flag[q], A.seq);
-                    *A.done_ctr = 0u;
                 }
+                if (STAGE == 3 && A.dt_wait != nullptr) {
+                    for (int q = 0; q < A.push_n; ++q)
+                        if (q != A.rank)
+                            wait_flag(A, A.dt_wait + q, A.seq);
+                    double g = A.gather_own[0];
+                    for (int q = 1; q < A.push_n; ++q) g = fmax(g, A.gather_own[q]);
+                    *A.amax_global = g;
+                }
+                *A.done_ctr = 0u;
             }
         }
     }

@@ -115,13 +115,14 @@ struct PendingLaunch {
     uint32_t slot;  // stamp slot
 };
 
-// Stream memory operations (driver API, resolved through the runtime so the
-// library needs no link-time libcuda): the P2P transport orders copy-engine
-// halo transfers with flag writes / waits that use no SM at all.
+// Stream memory operation (driver API, resolved through the runtime so the
+// library needs no link-time libcuda): the P2P copy-engine exchange raises a
+// peer's flag behind its transfer without an SM.  Waits are a one-thread
+// kernel with a deadline (tsh::launch_wait_flags), not cuStreamWaitValue32,
+// so a missing peer is reported instead of hanging the stream.
 struct StreamMemOps {
     bool ok = false;
     CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
-    CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
 };
 
 StreamMemOps& memops() {
@@ -129,12 +130,9 @@ StreamMemOps& memops() {
     static std::once_flag once;
     std::call_once(once, [] {
         void* w = nullptr;
-        void* v = nullptr;
-        cudaDriverEntryPointQueryResult q1, q2;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
-            cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess && w && v) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q) == cudaSuccess && w) {
             m.write32 = reinterpret_cast<decltype(m.write32)>(w);
-            m.wait32 = reinterpret_cast<decltype(m.wait32)>(v);
             m.ok = true;
         }
     });
@@ -149,6 +147,7 @@ struct P2PBlob {
     uint32_t magic;
     int32_t rank, world, device;
     cudaIpcMemHandle_t recv, flags, gather;
+    cudaIpcMemHandle_t U[3];      // state buffers (proxy slots written by the fused halo push)
     int64_t n_recv_total;
     int64_t recv_off[kMaxRanks];  // slab offset of the data from source rank q in my receive buffer
 };
@@ -157,6 +156,7 @@ struct PeerMap {
     double* recv = nullptr;    // peer's receive buffer (2 halves)
     int32_t* flags = nullptr;  // peer's flags: [0, world) halo by source, [world, 2 world) dt gather
     double* gather = nullptr;  // peer's dt gather: [2][world]
+    double* U[3] = {nullptr, nullptr, nullptr};  // peer's state buffers
     int64_t n_recv_total = 0;
     int64_t recv_off_for_me = 0;
 };
@@ -164,6 +164,7 @@ struct PeerMap {
 struct Peer {
     int rank = -1;
     std::vector<int64_t> send_pairs;  // (global id, face) flattened
+    std::vector<int32_t> send_dst;    // per send entry: the sub-grid's local index on the peer (a proxy)
     std::vector<int64_t> recv_pairs;
     int64_t send_off = 0, recv_off = 0;  // entry offsets into the concatenated tables
     int64_t n_send = 0, n_recv = 0;
@@ -198,17 +199,21 @@ struct ts_hydro_ctx {
     int32_t* d_nbr = nullptr;
     int32_t* d_interior = nullptr;
     int32_t* d_boundary = nullptr;
+    int32_t* d_order = nullptr;       // launch order of the fused P2P stage: boundary spread through the front
+    int32_t* d_cta_bnd = nullptr;     // [n_owned] launch position -> boundary slot (-1: interior)
+    int2* d_push_tbl = nullptr;       // [n_boundary][6] fused halo push targets
     long long* d_gid = nullptr;
     int2* d_send_entries = nullptr;
     int2* d_recv_entries = nullptr;
     double* d_send = nullptr;
     double* d_recv = nullptr;
     int64_t n_send_total = 0, n_recv_total = 0;
-    double* d_scal = nullptr;     // [0..1] amax ping-pong, [2] scratch amax, [3] dummy
+    double* d_scal = nullptr;     // [0..1] amax ping-pong, [2] scratch amax, [3] dummy, [4] P2P global amax
     double* d_dt_hist = nullptr;  // [kDtHist]
     static constexpr uint64_t kDtHist = 4096;
     unsigned long long* d_stamps = nullptr;  // [cap][2]
-    unsigned long long* h_clock = nullptr;   // mapped pinned
+    unsigned long long* h_clock = nullptr;   // mapped pinned: [0] clock calibration, [1] cross-GPU wait timeout
+    unsigned long long wait_ns = 30ull * 1000000000ull;
     std::map<void*, uint64_t> dev_allocs;
     std::map<void*, uint64_t> host_allocs;
     ts_memory_state mem{};
@@ -224,8 +229,11 @@ struct ts_hydro_ctx {
     double** d_push_gather = nullptr; // [2][world] gather arrays (parity halves) of every rank
     unsigned int** d_push_flag = nullptr;  // [world] dt flag word of every peer (nullptr for self)
     uint32_t xseq = 0, aseq = 0;      // exchange / dt-gather sequence numbers (same on every rank)
-    bool dt_wait_device = true;       // P2P dt flags acquired by the stage-1 CTAs (else a stream wait)
-    bool dt_pending_device = false;   // the next stage 1 must acquire the flags of aseq
+    bool halo_fused = true;           // P2P: halo slabs pushed by the stage kernel (else copy engines)
+    bool halo_pushed = false;         // proxies of U^n were pushed by the last stage 3 (flags of xseq)
+    uint64_t halo_recv_mask = 0;      // ranks that push slabs to this one
+    double** d_push_out = nullptr;    // [3][world] every peer's state buffers (nullptr for self)
+    unsigned int** d_halo_flag = nullptr;  // [world] this rank's halo flag word on each receiving peer
     const double* amax_src = nullptr; // where this step's dt comes from
     int amax_n = 1;
 
@@ -339,12 +347,17 @@ void close_peers(ts_hydro_ctx* c) {
         if (q.recv) cudaIpcCloseMemHandle(q.recv);
         if (q.flags) cudaIpcCloseMemHandle(q.flags);
         if (q.gather) cudaIpcCloseMemHandle(q.gather);
+        for (double* u : q.U)
+            if (u) cudaIpcCloseMemHandle(u);
         q = PeerMap{};
     }
     c->pm.clear();
     c->p2p = false;
     dfree(c, &c->d_push_gather);
     dfree(c, &c->d_push_flag);
+    dfree(c, &c->d_push_out);
+    dfree(c, &c->d_halo_flag);
+    c->halo_pushed = false;
 }
 
 void free_mesh(ts_hydro_ctx* c) {
@@ -356,6 +369,9 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_nbr);
     dfree(c, &c->d_interior);
     dfree(c, &c->d_boundary);
+    dfree(c, &c->d_order);
+    dfree(c, &c->d_cta_bnd);
+    dfree(c, &c->d_push_tbl);
     dfree(c, &c->d_gid);
     dfree(c, &c->d_send_entries);
     dfree(c, &c->d_recv_entries);
@@ -397,6 +413,11 @@ int harvest(ts_hydro_ctx* c) {
 int sync_all(ts_hydro_ctx* c) {
     for (cudaStream_t s : c->streams)
         if (s != nullptr) TS_CUDA(c, cudaStreamSynchronize(s));
+    if (c->h_clock != nullptr && ((volatile unsigned long long*)c->h_clock)[1] != 0ull) {
+        ((volatile unsigned long long*)c->h_clock)[1] = 0ull;
+        return fail(c, TS_ECOMM, "a peer rank did not arrive at a cross-GPU wait within the deadline "
+                                 "(stepping calls must be collective: same sequence on every rank)");
+    }
     return TS_OK;
 }
 
@@ -497,6 +518,27 @@ int build_plans(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner) {
             peers[(size_t)owner[p]].recv_pairs.push_back(p);
             peers[(size_t)owner[p]].recv_pairs.push_back(f);
         }
+    // where each sent slab lands on the receiver: its local numbering is owned
+    // sub-grids (ascending id), then proxies (ascending id)
+    for (Peer& p : peers) {
+        if (p.rank == c->rank || p.send_pairs.empty()) continue;
+        std::vector<int64_t> their_owned, their_proxy;
+        std::vector<char> is_proxy((size_t)c->n_global, 0);
+        for (int64_t i = 0; i < c->n_global; ++i) {
+            if (owner[i] != p.rank) continue;
+            their_owned.push_back(i);
+            for (int f = 0; f < 6; ++f) {
+                const int64_t nb = nbr[6 * i + f];
+                if (nb >= 0 && owner[nb] != p.rank) is_proxy[(size_t)nb] = 1;
+            }
+        }
+        for (int64_t i = 0; i < c->n_global; ++i)
+            if (is_proxy[(size_t)i]) their_proxy.push_back(i);
+        for (size_t k = 0; k < p.send_pairs.size(); k += 2) {
+            const auto it = std::lower_bound(their_proxy.begin(), their_proxy.end(), p.send_pairs[k]);
+            p.send_dst.push_back((int32_t)((int64_t)their_owned.size() + (it - their_proxy.begin())));
+        }
+    }
     int64_t so = 0, ro = 0;
     for (Peer& p : peers) {
         p.n_send = (int64_t)p.send_pairs.size() / 2;
@@ -545,6 +587,8 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     a.cfl = c->cfg.cfl;
     a.dx = c->cfg.dx;
     a.p_floor = c->cfg.p_floor;
+    a.err = c->h_clock + 1;
+    a.wait_ns = c->wait_ns;
     return a;
 }
 
@@ -603,11 +647,8 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf, bool packed = false) {
             if (m.write32(cs, (CUdeviceptr)(q.flags + c->rank), seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
                 return fail(c, TS_ECUDA, "cuStreamWriteValue32 to a peer flag failed");
         }
-        for (const Peer& p : c->peers) {
-            if (p.rank == c->rank || p.n_recv == 0) continue;
-            if (m.wait32(cs, (CUdeviceptr)(c->d_flags + p.rank), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a halo flag failed");
-        }
+        TS_CUDA(c, tsh::launch_wait_flags(reinterpret_cast<const unsigned int*>(c->d_flags), c->halo_recv_mask, seq,
+                                          c->h_clock + 1, c->wait_ns, cs));
         recv = c->d_recv + (size_t)h * (size_t)c->n_recv_total * per;
     } else if (c->comm != nullptr) {
         Nccl& n = nccl();
@@ -639,7 +680,6 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf, bool packed = false) {
 int reduce_amax(ts_hydro_ctx* c, double* slot, cudaStream_t s) {
     c->amax_src = nullptr;
     c->amax_n = 1;
-    c->dt_pending_device = false;
     if (c->world <= 1) return TS_OK;
     if (c->p2p) {
         StreamMemOps& m = memops();
@@ -656,11 +696,11 @@ int reduce_amax(ts_hydro_ctx* c, double* slot, cudaStream_t s) {
                 CUDA_SUCCESS)
                 return fail(c, TS_ECUDA, "cuStreamWriteValue32 to a peer flag failed");
         }
-        for (int r = 0; r < c->world; ++r) {
-            if (r == c->rank) continue;
-            if (m.wait32(s, (CUdeviceptr)(c->d_flags + c->world + r), seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a dt flag failed");
-        }
+        uint64_t others = 0;
+        for (int r = 0; r < c->world; ++r)
+            if (r != c->rank) others |= 1ull << r;
+        TS_CUDA(c, tsh::launch_wait_flags(reinterpret_cast<const unsigned int*>(c->d_flags + c->world), others, seq,
+                                          c->h_clock + 1, c->wait_ns, s));
         c->amax_src = mine;
         c->amax_n = c->world;
         return TS_OK;
@@ -699,42 +739,75 @@ int do_step(ts_hydro_ctx* c) {
         if (!rc) rc = ensure_stream(c, 2, &bs);
         if (rc) return rc;
     }
-    const bool fused_push = multi && c->p2p;
+    const bool p2p = multi && c->p2p;
+    const bool fused_halo = p2p && c->halo_fused;
     const uint32_t push_seq = c->aseq + 1;
-    const bool wait_dt = c->dt_pending_device;
-    c->dt_pending_device = false;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
         if (stage == 1) {
             a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
         }
-        if (stage == 1 && wait_dt) {
-            a.wait_flags = reinterpret_cast<const unsigned int*>(c->d_flags + c->world);
-            a.wait_n = c->world;
-            a.wait_seq = c->aseq;
+        if (p2p && stage == 3) {
+            a.done_ctr = c->d_ctr;
+            a.total_ctas = (int)c->n_owned;
             a.rank = c->rank;
         }
-        if (stage == 3 && fused_push) {
+        if (p2p && stage == 3) {
+            // dt all-reduce fused into the stage-3 tail (see StageArgs)
             a.push_n = c->world;
-            a.rank = c->rank;
-            a.total_ctas = (int)c->n_owned;
-            a.done_ctr = c->d_ctr;
             a.push_gather = c->d_push_gather + (size_t)(push_seq & 1) * c->world;
             a.push_flag = c->d_push_flag;
             a.seq = push_seq;
+            a.dt_wait = reinterpret_cast<const unsigned int*>(c->d_flags + c->world);
+            a.gather_own = c->d_gather + (size_t)(push_seq & 1) * c->world;
+            a.amax_global = c->d_scal + 4;
         }
         if (!multi) {
             rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0);
             if (rc) return rc;
             continue;
         }
-        // U^(k-1) complete (interior + boundary of the previous stage).  The
-        // interior launch goes first (it needs no halo); the exchange is issued
-        // behind it on the high-priority halo stream (pack -> NCCL -> unpack)
-        // and the boundary sub-grids follow on the high-priority boundary
-        // stream, so they back-fill SMs as interior CTAs retire.
         double* in = const_cast<double*>(a.Uprev);
+        if (fused_halo) {
+            // One launch, boundary sub-grids first; they acquire the peers'
+            // slabs of U^(k-1) (pushed during the previous stage), push their
+            // own U^(k) slabs into the peers' proxies and release the peers'
+            // flags.  The first stage of a call refreshes the proxies of U^n
+            // by the copy-engine exchange instead (the state may have been
+            // replaced since the last push).
+            if (c->halo_pushed) {
+                a.halo_wait = reinterpret_cast<const unsigned int*>(c->d_flags);
+                a.halo_wait_mask = c->halo_recv_mask;
+                a.halo_wait_seq = c->xseq;
+            } else {
+                TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+                TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+                rc = exchange_on_comm(c, in);
+                if (rc) return rc;
+                TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
+                TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+            }
+            const int out_idx = stage == 1 ? 1 : (stage == 2 ? 2 : 0);
+            a.n_boundary = (int)c->boundary.size();
+            a.cta_bnd = c->d_cta_bnd;
+            a.push_tbl = c->d_push_tbl;
+            a.push_out = c->d_push_out + (size_t)out_idx * c->world;
+            a.halo_ctr = c->d_ctr + 1;
+            a.halo_flag = c->d_halo_flag;
+            a.halo_flag_n = c->world;
+            a.halo_seq = ++c->xseq;
+            rc = launch_stage_list(c, a, stage, c->d_order, c->n_owned, 0, 0, 0);
+            if (rc) return rc;
+            c->halo_pushed = true;
+            continue;
+        }
+        // Copy-engine / NCCL halos.  U^(k-1) complete (interior + boundary of
+        // the previous stage).  The interior launch goes first (it needs no
+        // halo); the exchange is issued behind it on the high-priority halo
+        // stream (pack -> transfer -> unpack) and the boundary sub-grids follow
+        // on the high-priority boundary stream, so they back-fill SMs as
+        // interior CTAs retire.
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
         TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
         TS_CUDA(c, cudaStreamWaitEvent(bs, c->ev_in, 0));
@@ -756,22 +829,11 @@ int do_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaEventRecord(c->ev_bnd, bs));
         TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_bnd, 0));
     }
-    if (fused_push) {
-        // the stage-3 kernels pushed this rank's max; wait (no SM) for the peers'
+    if (p2p) {
+        // the stage-3 tail gathered every rank's max: the next dt is local
         c->aseq = push_seq;
-        if (c->dt_wait_device) {
-            c->dt_pending_device = true;  // the next stage-1 CTAs acquire the peers' flags
-        } else {
-            StreamMemOps& m = memops();
-            for (int r = 0; r < c->world; ++r) {
-                if (r == c->rank) continue;
-                if (m.wait32(s, (CUdeviceptr)(c->d_flags + c->world + r), push_seq, CU_STREAM_WAIT_VALUE_GEQ) !=
-                    CUDA_SUCCESS)
-                    return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a dt flag failed");
-            }
-        }
-        c->amax_src = c->d_gather + (size_t)(push_seq & 1) * c->world;
-        c->amax_n = c->world;
+        c->amax_src = c->d_scal + 4;
+        c->amax_n = 1;
     } else if (multi) {
         double* slot = c->d_scal + ((c->steps_done & 1) ^ 1);
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
@@ -828,6 +890,7 @@ const char* ts_hydro_strerror(int code) {
         case TS_ENCCL: return "NCCL error";
         case TS_ENOMEM: return "out of device memory";
         case TS_ESTATE: return "call out of order";
+        case TS_ECOMM: return "peer rank did not arrive";
     }
     return "unknown error";
 }
@@ -875,7 +938,8 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->cfg = *cfg;
     c->nf = 6 + cfg->n_species;
     c->dev = cfg->device_id;
-    if (const char* w = std::getenv("TS_HYDRO_DT_WAIT")) c->dt_wait_device = std::strcmp(w, "stream") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_WAIT_TIMEOUT_MS")) c->wait_ns = 1000000ull * std::strtoull(w, nullptr, 10);
     if (cfg->device_id < 0) {
         c->host_only = true;
         *out = c;
@@ -903,9 +967,10 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
         rc = cuda_fail(c, e, "cudaMemset");
     if (!rc && (e = cudaMemset(c->d_scal, 0, 8 * sizeof(double))) != cudaSuccess) rc = cuda_fail(c, e, "cudaMemset");
     if (!rc && (e = cudaDeviceSynchronize()) != cudaSuccess) rc = cuda_fail(c, e, "cudaDeviceSynchronize");
-    if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, sizeof(unsigned long long), cudaHostAllocMapped)) !=
+    if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, 2 * sizeof(unsigned long long), cudaHostAllocMapped)) !=
                    cudaSuccess)
         rc = cuda_fail(c, e, "cudaHostAlloc");
+    if (!rc) c->h_clock[1] = 0ull;
     if (!rc) rc = calibrate_clock(c);
     if (rc) {
         std::fprintf(stderr, "ts_hydro_create: %s\n", c->err.c_str());
@@ -1097,6 +1162,8 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     rc = dalloc(c, &c->d_nbr, (size_t)nl * 6);
     if (!rc) rc = dalloc(c, &c->d_interior, c->interior.size());
     if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
+    if (!rc) rc = dalloc(c, &c->d_order, (size_t)c->n_owned);
+    if (!rc) rc = dalloc(c, &c->d_cta_bnd, (size_t)c->n_owned);
     if (!rc) rc = dalloc(c, &c->d_gid, (size_t)c->n_owned);
     if (rc) return rc;
     TS_CUDA(c, cudaMemcpy(c->d_nbr, c->nbr_local.data(), c->nbr_local.size() * sizeof(int32_t),
@@ -1107,6 +1174,28 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     if (!c->boundary.empty())
         TS_CUDA(c, cudaMemcpy(c->d_boundary, c->boundary.data(), c->boundary.size() * sizeof(int32_t),
                               cudaMemcpyHostToDevice));
+    {
+        // fused P2P launch order: boundary sub-grid b at position b * stride
+        // (while interior ones remain).  Measured on 4 B200s (Sedov 16^3 per
+        // GPU): stride 1 — every boundary sub-grid in the first wave — beats
+        // spreading them (stride 4: -7 %); TS_HYDRO_BSTRIDE overrides.
+        int stride = 1;
+        if (const char* e = std::getenv("TS_HYDRO_BSTRIDE")) stride = std::max(1, std::atoi(e));
+        std::vector<int32_t> order, bnd;
+        size_t bi = 0, ii = 0;
+        while (bi < c->boundary.size() || ii < c->interior.size()) {
+            const bool take_b = bi < c->boundary.size() && (ii >= c->interior.size() || order.size() % stride == 0);
+            if (take_b) {
+                bnd.push_back((int32_t)bi);
+                order.push_back(c->boundary[bi++]);
+            } else {
+                bnd.push_back(-1);
+                order.push_back(c->interior[ii++]);
+            }
+        }
+        TS_CUDA(c, cudaMemcpy(c->d_order, order.data(), order.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaMemcpy(c->d_cta_bnd, bnd.data(), bnd.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
     {
         std::vector<long long> gid(c->owned_gid.begin(), c->owned_gid.end());
         if (!gid.empty())
@@ -1129,9 +1218,27 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
         if (!rc) rc = dalloc(c, &c->d_recv, 2 * (size_t)c->n_recv_total * c->nf * kSlab);
         if (!rc) rc = dalloc(c, &c->d_flags, 2 * (size_t)world);
         if (!rc) rc = dalloc(c, &c->d_gather, 2 * (size_t)world);
-        if (!rc) rc = dalloc(c, &c->d_ctr, 1);
+        if (!rc) rc = dalloc(c, &c->d_ctr, 2);  // [0] dt push, [1] halo push
         if (rc) return rc;
-        TS_CUDA(c, cudaMemset(c->d_ctr, 0, sizeof(unsigned int)));
+        TS_CUDA(c, cudaMemset(c->d_ctr, 0, 2 * sizeof(unsigned int)));
+        // fused push targets by boundary position: {peer rank, local index on the peer}
+        std::vector<int2> tbl(c->boundary.size() * 6, make_int2(-1, -1));
+        std::vector<int32_t> bpos((size_t)c->n_owned, -1);
+        for (size_t b = 0; b < c->boundary.size(); ++b) bpos[(size_t)c->boundary[b]] = (int32_t)b;
+        c->halo_recv_mask = 0;
+        for (const Peer& p : c->peers) {
+            if (p.n_recv > 0) c->halo_recv_mask |= 1ull << p.rank;
+            for (int64_t k = 0; k < p.n_send; ++k) {
+                const int64_t l = local_of(c, p.send_pairs[(size_t)(2 * k)]);
+                const int f = (int)p.send_pairs[(size_t)(2 * k + 1)];
+                tbl[(size_t)bpos[(size_t)l] * 6 + f] = make_int2(p.rank, p.send_dst[(size_t)k]);
+            }
+        }
+        if (!tbl.empty()) {
+            rc = dalloc(c, &c->d_push_tbl, tbl.size());
+            if (rc) return rc;
+            TS_CUDA(c, cudaMemcpy(c->d_push_tbl, tbl.data(), tbl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        }
         TS_CUDA(c, cudaMemset(c->d_flags, 0, 2 * (size_t)world * sizeof(int32_t)));
         TS_CUDA(c, cudaMemset(c->d_gather, 0, 2 * (size_t)world * sizeof(double)));
         if (!se.empty())
@@ -1286,6 +1393,7 @@ int ts_hydro_step(ts_hydro_ctx* c, uint64_t nsteps) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
     cudaSetDevice(c->dev);
     if (c->world > 1 && c->comm == nullptr && !c->p2p)
         return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init or ts_hydro_p2p_import before stepping");
@@ -1305,6 +1413,7 @@ int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out,
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
+    c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
     cudaSetDevice(c->dev);
     cudaStream_t s;
     rc = ensure_stream(c, 0, &s);
@@ -1329,6 +1438,7 @@ int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
     if (ms == nullptr) return fail(c, TS_EINVAL, "null output");
     if (c->world > 1 && c->comm == nullptr && !c->p2p)
         return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init or ts_hydro_p2p_import before stepping");
+    c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
     cudaSetDevice(c->dev);
     cudaStream_t s;
     rc = ensure_stream(c, 0, &s);
@@ -1583,6 +1693,7 @@ int ts_hydro_p2p_export(ts_hydro_ctx* c, void* blob) {
     TS_CUDA(c, cudaIpcGetMemHandle(&b.recv, c->d_recv));
     TS_CUDA(c, cudaIpcGetMemHandle(&b.flags, c->d_flags));
     TS_CUDA(c, cudaIpcGetMemHandle(&b.gather, c->d_gather));
+    for (int k = 0; k < 3; ++k) TS_CUDA(c, cudaIpcGetMemHandle(&b.U[k], c->U[k]));
     b.n_recv_total = c->n_recv_total;
     for (const Peer& p : c->peers)
         if (p.rank >= 0 && p.rank < kMaxRanks) b.recv_off[p.rank] = p.recv_off;
@@ -1614,6 +1725,10 @@ int ts_hydro_p2p_import(ts_hydro_ctx* c, const void* blobs, int32_t world) {
         q.flags = static_cast<int32_t*>(p);
         TS_CUDA(c, cudaIpcOpenMemHandle(&p, b.gather, cudaIpcMemLazyEnablePeerAccess));
         q.gather = static_cast<double*>(p);
+        for (int k = 0; k < 3; ++k) {
+            TS_CUDA(c, cudaIpcOpenMemHandle(&p, b.U[k], cudaIpcMemLazyEnablePeerAccess));
+            q.U[k] = static_cast<double*>(p);
+        }
         q.n_recv_total = b.n_recv_total;
         q.recv_off_for_me = b.recv_off[c->rank];
     }
@@ -1626,14 +1741,27 @@ int ts_hydro_p2p_import(ts_hydro_ctx* c, const void* blobs, int32_t world) {
                     (r == c->rank ? c->d_gather : c->pm[(size_t)r].gather) + (size_t)h * world;
         for (int r = 0; r < world; ++r)
             if (r != c->rank) pf[(size_t)r] = reinterpret_cast<unsigned int*>(c->pm[(size_t)r].flags + world + c->rank);
+        std::vector<double*> po(3 * (size_t)world, nullptr);
+        std::vector<unsigned int*> hf((size_t)world, nullptr);
+        for (int r = 0; r < world; ++r) {
+            if (r == c->rank) continue;
+            for (int k = 0; k < 3; ++k) po[(size_t)k * world + r] = c->pm[(size_t)r].U[k];
+            if (c->peers[(size_t)r].n_send > 0)
+                hf[(size_t)r] = reinterpret_cast<unsigned int*>(c->pm[(size_t)r].flags + c->rank);
+        }
         rc = dalloc(c, &c->d_push_gather, pg.size());
         if (!rc) rc = dalloc(c, &c->d_push_flag, pf.size());
+        if (!rc) rc = dalloc(c, &c->d_push_out, po.size());
+        if (!rc) rc = dalloc(c, &c->d_halo_flag, hf.size());
         if (rc) return rc;
+        TS_CUDA(c, cudaMemcpy(c->d_push_out, po.data(), po.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaMemcpy(c->d_halo_flag, hf.data(), hf.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaMemcpy(c->d_push_gather, pg.data(), pg.size() * sizeof(double*), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaMemcpy(c->d_push_flag, pf.data(), pf.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaDeviceSynchronize());
     }
     c->p2p = true;
+    c->halo_pushed = false;
     return TS_OK;
 }
 

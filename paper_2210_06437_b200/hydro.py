@@ -34,7 +34,7 @@ HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "ts_hydro.h")
 N = 8
 NC = 512
 
-TS_OK, TS_EINVAL, TS_ESHUTDOWN, TS_ECUDA, TS_ENCCL, TS_ENOMEM, TS_ESTATE = range(7)
+TS_OK, TS_EINVAL, TS_ESHUTDOWN, TS_ECUDA, TS_ENCCL, TS_ENOMEM, TS_ESTATE, TS_ECOMM = range(8)
 RECON = {"ppm": 0, "minmod": 1}
 PROBLEMS = {"sod": 0, "sedov": 1, "random": 2, "polytrope": 3, "binary": 4}
 ACTIVITY_KINDS = ("kernel", "copy_host_to_device", "copy_device_to_host", "copy_device_to_device",

@@ -28,7 +28,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p-ce", "nccl"])
 @pytest.mark.parametrize("args", [["--dims", "4", "4", "8"], ["--dims", "2", "4", "4", "--periodic", "xyz", "--species", "5"],
                                   ["--dims", "4", "2", "6", "--recon", "minmod", "--steps", "2"]])
 def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args, transport):
@@ -41,3 +41,18 @@ def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args, transport):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
+def test_mismatched_collective_call_fails_instead_of_hanging(transport):
+    """Stepping is collective: a rank that makes one call too many must get
+    TS_ECOMM from the cross-GPU wait deadline, not spin the GPU forever."""
+    n = _gpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tools", "multigpu_check.py"), "--mismatch", "--transport", transport]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MISMATCH DETECTED" in r.stdout

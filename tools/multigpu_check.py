@@ -30,8 +30,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--species", type=int, default=0)
     ap.add_argument("--recon", default="ppm")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "p2p-ce", "nccl"])
+    ap.add_argument("--mismatch", action="store_true",
+                    help="rank 1 makes one stepping call too many: it must fail with TS_ECOMM, not hang")
     a = ap.parse_args()
+    if a.transport == "p2p-ce":  # P2P with copy-engine halos instead of the in-kernel push
+        os.environ["TS_HYDRO_HALO"] = "ce"
+    if a.mismatch:
+        os.environ["TS_HYDRO_WAIT_TIMEOUT_MS"] = "2000"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -50,7 +56,29 @@ def main():
     dev.init_random(2210)
     owned = dev.owned_ids()
     n_owned, n_proxy, n_interior = dev.local_counts()
-    dev.step(a.steps)
+    if a.mismatch:
+        dev.step(1)
+        dev.synchronize()
+        code = 0
+        if rank == 1:
+            try:
+                dev.step(1)
+                dev.synchronize()
+            except H.TsError as e:
+                code = e.code
+        dist.barrier()
+        res = torch.tensor([code if rank == 1 else H.TS_ECOMM])
+        dist.all_reduce(res, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print("MISMATCH DETECTED" if res.item() == H.TS_ECOMM else f"MISMATCH NOT DETECTED ({res.item()})",
+                  flush=True)
+        dist.destroy_process_group()
+        return 0 if res.item() == H.TS_ECOMM else 1
+    # two calls: the first stage of each call refreshes the halos by a copy, the
+    # other stages take the slabs the peers' stage kernels pushed
+    dev.step(1)
+    if a.steps > 1:
+        dev.step(a.steps - 1)
     got = dev.download()
     dt = dev.last_dt()
     recs = [r for r in dev.flush_activity() if r.kind == "kernel"]

@@ -22,15 +22,20 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--species", type=int, default=0)
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--quiet", action="store_true", help="totals and summary only")
+    ap.add_argument("--replicas", action="store_true", help="every rank steps its own single-GPU mesh")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
-    mesh = H.uniform_mesh(a.edge, a.edge, a.edge * world, world=world)
+    rep = a.replicas and world > 1
+    mesh = (H.uniform_mesh(a.edge, a.edge, a.edge) if rep else H.uniform_mesh(a.edge, a.edge, a.edge * world, world=world))
     dev = H.CudaDevice(H.HydroConfig(device_id=local, dx=1.0 / (8 * a.edge), n_species=a.species))
-    dev.set_mesh(mesh, rank)
-    if world > 1 and a.transport == "nccl":
+    dev.set_mesh(mesh, 0 if rep else rank)
+    if rep:
+        pass
+    elif world > 1 and a.transport == "nccl":
         uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dev.comm_init(uid[0], world, rank)
@@ -52,6 +57,22 @@ def main():
     for r in recs:
         lines.append(f"  {r.name:22s} s{r.stream_id} {(r.start_ns - t0) / 1e3:9.1f} -> {(r.end_ns - t0) / 1e3:9.1f} us"
                      f"  ({(r.end_ns - r.start_ns) / 1e3:7.1f})")
+    # per-kernel mean duration and the mean idle gap before each stage kernel
+    from collections import defaultdict
+    dur, gaps = defaultdict(list), []
+    prev_end = None
+    for r in recs:
+        dur[r.name].append((r.end_ns - r.start_ns) / 1e3)
+        if r.name.startswith("hydro_stage"):
+            if prev_end is not None:
+                gaps.append((r.start_ns - prev_end) / 1e3)
+            prev_end = r.end_ns
+    summ = "  summary: " + ", ".join(f"{k} {sum(v) / len(v):.1f} us x{len(v)}" for k, v in sorted(dur.items()))
+    if gaps:
+        summ += f", stage gap {sum(gaps) / len(gaps):.1f} us"
+    lines.insert(1, summ)
+    if a.quiet:
+        lines = lines[:2]
     text = "\n".join(lines)
     if world > 1:
         out = [None] * world
