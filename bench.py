@@ -11,7 +11,7 @@ total_cells * steps / seconds (workload.cpp:608-609).
 N=1 workload: BASELINE configs[1], Sedov–Taylor on 16^3 = 4096 sub-grids
 (128^3 cells, nf = 6, FP64).  N>1: weak scaling, 4096 sub-grids per GPU
 (domain 16 x 16 x 16N sub-grids, one contiguous Morton chunk = one z-slab per
-rank) with cross-GPU halos over NCCL.  `--workload polytrope` runs configs[2]
+rank) with cross-GPU halos pushed over NVLink by the stage kernel itself.  `--workload polytrope` runs configs[2]
 (32^3 sub-grids per GPU, 5 species, nf = 11).
 
 `--impl reference` times the CPU path of the reference's algorithm (the
