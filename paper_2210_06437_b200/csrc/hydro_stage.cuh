@@ -54,15 +54,23 @@ constexpr int kFaces = N + 1;
 #else
 #define TS_MINB_FOR(NF) (Lanes<NF>::min_blocks)
 #endif
-// Face-march unroll (measured on B200: 1 beats 3 — the larger body costs
-// more in scheduling / registers than the window moves it saves).
 #ifndef TS_KEEP_DL
 #define TS_KEEP_DL 0
 #endif
-#ifndef TS_FACE_UNROLL
-#define TS_FACE_UNROLL 1
+// Face-march unroll per reconstruction.  The rolled march pays ~90 register
+// moves per face rotating the window state; unrolling renames them away but
+// needs registers.  Measured on B200 (same-box A/B, Sedov 16^3): minmod
+// unrolled by 2 fits the 6-CTA register budget and gains 4 % (5.40 -> 5.62 G
+// cell-updates/s); PPM unrolled by 2 spills at 6 CTAs and loses 5 % even at 5
+// (3.37 -> 3.19), by 2 at 4 CTAs 11 %.  TS_FACE_UNROLL forces one value.
+template <int RECON>
+struct FaceUnroll {
+#ifdef TS_FACE_UNROLL
+    static constexpr int value = TS_FACE_UNROLL;
+#else
+    static constexpr int value = RECON == 1 ? 2 : 1;
 #endif
-constexpr int kFaceUnroll = TS_FACE_UNROLL;
+};
 
 template <int NF>
 struct StageSmem {
@@ -323,7 +331,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             c.cache[(0 * 3 + 2) * kPencils + t] = a;
         }
     }
-#pragma unroll kFaceUnroll
+#pragma unroll FaceUnroll<RECON>::value
     for (int j = 1; j < kFaces; ++j) {
         const double* next = next_addr<RECON>(p, j);
         double uL[kFA], uR[kFA], up[kFA];
