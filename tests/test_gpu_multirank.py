@@ -30,7 +30,10 @@ def _port():
 
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce", "nccl"])
 @pytest.mark.parametrize("args", [["--dims", "4", "4", "8"], ["--dims", "2", "4", "4", "--periodic", "xyz", "--species", "5"],
-                                  ["--dims", "4", "2", "6", "--recon", "minmod", "--steps", "2"]])
+                                  ["--dims", "4", "2", "6", "--recon", "minmod", "--steps", "2"],
+                                  # ragged Morton chunks: x- and y-face slabs, several foreign faces per sub-grid
+                                  ["--dims", "3", "3", "3"],
+                                  ["--dims", "5", "3", "2", "--periodic", "x", "--recon", "minmod", "--species", "2"]])
 def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args, transport):
     n = _gpus()
     if n < 2:
