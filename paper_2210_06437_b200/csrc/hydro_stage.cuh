@@ -45,6 +45,13 @@ struct Lanes {
     static constexpr int min_blocks = pair ? 4 : 6;
 };
 constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
+// PPM: reload the retiring cell's U^(k-1) from L1 (it was loaded two faces
+// earlier) instead of carrying it in the window state (12 registers and 12
+// moves per face).  PLM needs the value for its slope anyway.
+#ifndef TS_PPM_RELOAD_UP
+#define TS_PPM_RELOAD_UP 1
+#endif
+
 constexpr int kFA = 6;        // fields marched together: rho, s_n, s_t1, s_t2, E, tau
 constexpr int kFaces = N + 1;
 
@@ -114,6 +121,14 @@ struct Recon {
     double dl;
 #endif
 };
+
+// (Single-lane march only: measured +0.9 % at nf 6; the lane-pair march at
+// nf 11 loses 6 % with it.)
+template <int RECON>
+__device__ __forceinline__ double retiring_up(const Recon& r, const double* own_row, int j, int ss, int fo) {
+    if (RECON == 0 && TS_PPM_RELOAD_UP) return __ldg(own_row + (j - 1) * ss + fo);
+    return r.wp;
+}
 
 // q[j+1] - q[j]: recomputed (one DADD) rather than carried — a carried value
 // costs a register and two moves per face in the rolled march.
@@ -312,6 +327,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
     for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
     const double* un_row = c.Un + c.own + p.base;
+    const double* own_row = p.own + p.base;
     double un[kFA];
     if (kUn) {
 #pragma unroll
@@ -337,7 +353,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         double uL[kFA], uR[kFA], up[kFA];
 #pragma unroll
         for (int k = 0; k < kFA; ++k) {
-            up[k] = r[k].wp;  // U^(k-1) of cell j-1, the one retired at this face
+            up[k] = retiring_up<RECON>(r[k], own_row, j, p.ss, fo[k]);  // U^(k-1) of cell j-1, retired here
             recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
         }
         double F[kFA], vL, vR, a;
@@ -384,7 +400,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
-                const double upf = q.wp;
+                const double upf = retiring_up<RECON>(q, own_row, j, p.ss, fof);
                 recon_step<RECON>(next_addr<RECON>(p, j), fof, q, uL, uR);
                 const double vL = c.cache[(j * 3 + 0) * kPencils + t];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
