@@ -227,7 +227,7 @@ struct StageCtx {
     double* __restrict__ dU;     // shared accumulator
     double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
     size_t own;                  // element offset of the sub-grid's field 0
-    double dtdx;
+    double dtdx;                 // 0.5 dt/dx: fluxes are carried doubled (kt2)
     EosParams e;
 };
 
@@ -305,12 +305,12 @@ __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[k
     const double aL = fabs(vL) + eos_sqrt((e.gamma * pL) * invL);
     const double aR = fabs(vR) + eos_sqrt((e.gamma * pR) * invR);
     a = dmax(aL, aR);
-    F[0] = kt(a, uL[0], uR[0], uL[1], uR[1]);
-    F[1] = kt(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
-    F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
-    F[3] = kt(a, uL[3], uR[3], uL[3] * vL, uR[3] * vR);
-    F[4] = kt(a, uL[4], uR[4], (uL[4] + pL) * vL, (uR[4] + pR) * vR);
-    F[5] = kt(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
+    F[0] = kt2(a, uL[0], uR[0], uL[1], uR[1]);
+    F[1] = kt2(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
+    F[2] = kt2(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+    F[3] = kt2(a, uL[3], uR[3], uL[3] * vL, uR[3] * vR);
+    F[4] = kt2(a, uL[4], uR[4], (uL[4] + pL) * vL, (uR[4] + pR) * vR);
+    F[5] = kt2(a, uL[5], uR[5], uL[5] * vL, uR[5] * vR);
 }
 
 // Single-lane march, one instantiation per sweep mode (x: init, y:
@@ -395,7 +395,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             {
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
-                Fq = kt(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
+                Fq = kt2(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -405,7 +405,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 const double vL = c.cache[(j * 3 + 0) * kPencils + t];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
                 const double a = c.cache[(j * 3 + 2) * kPencils + t];
-                const double F = kt(a, uL, uR, uL * vL, uR * vR);
+                const double F = kt2(a, uL, uR, uL * vL, uR * vR);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -479,9 +479,9 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
         const double fL1 = role ? (uL[1] + pL) * vL : fma(uL[1], vL, pL);
         const double fR1 = role ? (uR[1] + pR) * vR : fma(uR[1], vR, pR);
         double F[3];
-        F[0] = kt(a, uL[0], uR[0], fL0, fR0);
-        F[1] = kt(a, uL[1], uR[1], fL1, fR1);
-        F[2] = kt(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+        F[0] = kt2(a, uL[0], uR[0], fL0, fR0);
+        F[1] = kt2(a, uL[1], uR[1], fL1, fR1);
+        F[2] = kt2(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
         if (NF > kFA && role == 0) {
             c.cache[(j * 3 + 0) * kPencils + pen] = vL;
             c.cache[(j * 3 + 1) * kPencils + pen] = vR;
@@ -526,7 +526,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
             {
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
-                Fq = kt(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
+                Fq = kt2(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -536,7 +536,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 const double vL = c.cache[(j * 3 + 0) * kPencils + pen];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
                 const double a = c.cache[(j * 3 + 2) * kPencils + pen];
-                const double F = kt(a, uL, uR, uL * vL, uR * vR);
+                const double F = kt2(a, uL, uR, uL * vL, uR * vR);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     c.cache = smem + StageSmem<NF>::dU;
     c.own = (size_t)g * NF * NC;
     c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
-    c.dtdx = dtdx;
+    c.dtdx = 0.5 * dtdx;  // the sweeps carry twice the KT flux (kt2)
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
     const double* own = A.Uprev + c.own;
     const int pen = Lanes<NF>::pair ? t >> 1 : t;
