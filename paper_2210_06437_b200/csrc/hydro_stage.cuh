@@ -111,7 +111,7 @@ __device__ __forceinline__ const double* paddr(const Pencil& p, int s) {
 }
 
 // Running reconstruction state of one field along the pencil.  On entry to
-// face j (between cells j-1 and j): w0 = q[j], w1 = q[j+1], D = slope(j),
+// face j (between cells j-1 and j): w0 = q[j], w1 = q[j+1], D = 2 slope(j),
 // fc = interface value at face j, hi = limited right edge of cell j-1,
 // qn = the next pencil value (prefetched), wp = q[j-1]
 // (the U^(k-1) value of the cell retired at face j).
@@ -148,11 +148,11 @@ __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
         const double q4 = __ldg(paddr(p, 1) + fo);
         r.qn = __ldg(paddr(p, 2) + fo);
         const double d0 = q1 - q0, d1 = q2 - q1, d2 = q3 - q2, d3 = q4 - q3;
-        const double D1 = mc_slope(d1, d0);
-        const double D2 = mc_slope(d2, d1);
-        const double D3 = mc_slope(d3, d2);
-        const double f2 = ppm_face(q1, q2, D1, D2);
-        const double f3 = ppm_face(q2, q3, D2, D3);
+        const double D1 = mc_slope2(d1, d0);  // slopes carried doubled
+        const double D2 = mc_slope2(d2, d1);
+        const double D3 = mc_slope2(d3, d2);
+        const double f2 = ppm_face2(q1, q2, D1, D2);
+        const double f3 = ppm_face2(q2, q3, D2, D3);
         double l = f2, h = f3;
         ppm_limit(l, q2, h);
         r.hi = h;
@@ -187,8 +187,8 @@ __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r,
     r.qn = __ldg(next + fo);  // `next` is always a valid address (the value is unused after the last face)
     if (RECON == 0) {
         const double dn = q - r.w1;
-        const double Dn = mc_slope(dn, recon_dl(r));
-        const double fn = ppm_face(r.w0, r.w1, r.D, Dn);
+        const double Dn = mc_slope2(dn, recon_dl(r));
+        const double fn = ppm_face2(r.w0, r.w1, r.D, Dn);
         double l = r.fc, h = fn;
         ppm_limit(l, r.w0, h);
         uL = r.hi;
