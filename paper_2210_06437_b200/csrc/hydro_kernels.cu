@@ -225,23 +225,23 @@ __global__ void selftest_math_kernel(unsigned long long n, unsigned long long se
 // Host-side launchers
 // ---------------------------------------------------------------------------
 template <int NF>
-cudaError_t launch_stage_n(const StageArgs& a, int recon, int stage, int n, cudaStream_t s);
-extern template cudaError_t launch_stage_n<6>(const StageArgs&, int, int, int, cudaStream_t);
-extern template cudaError_t launch_stage_n<7>(const StageArgs&, int, int, int, cudaStream_t);
-extern template cudaError_t launch_stage_n<8>(const StageArgs&, int, int, int, cudaStream_t);
-extern template cudaError_t launch_stage_n<9>(const StageArgs&, int, int, int, cudaStream_t);
-extern template cudaError_t launch_stage_n<10>(const StageArgs&, int, int, int, cudaStream_t);
-extern template cudaError_t launch_stage_n<11>(const StageArgs&, int, int, int, cudaStream_t);
+cudaError_t launch_stage_n(const StageArgs& a, int recon, int stage, int n, cudaStream_t s, bool pdl);
+extern template cudaError_t launch_stage_n<6>(const StageArgs&, int, int, int, cudaStream_t, bool);
+extern template cudaError_t launch_stage_n<7>(const StageArgs&, int, int, int, cudaStream_t, bool);
+extern template cudaError_t launch_stage_n<8>(const StageArgs&, int, int, int, cudaStream_t, bool);
+extern template cudaError_t launch_stage_n<9>(const StageArgs&, int, int, int, cudaStream_t, bool);
+extern template cudaError_t launch_stage_n<10>(const StageArgs&, int, int, int, cudaStream_t, bool);
+extern template cudaError_t launch_stage_n<11>(const StageArgs&, int, int, int, cudaStream_t, bool);
 
-cudaError_t launch_stage(const StageArgs& a, int nf, int recon, int stage, int n_ctas, cudaStream_t s) {
+cudaError_t launch_stage(const StageArgs& a, int nf, int recon, int stage, int n_ctas, cudaStream_t s, bool pdl) {
     if (n_ctas <= 0) return cudaSuccess;
     switch (nf) {
-        case 6: return launch_stage_n<6>(a, recon, stage, n_ctas, s);
-        case 7: return launch_stage_n<7>(a, recon, stage, n_ctas, s);
-        case 8: return launch_stage_n<8>(a, recon, stage, n_ctas, s);
-        case 9: return launch_stage_n<9>(a, recon, stage, n_ctas, s);
-        case 10: return launch_stage_n<10>(a, recon, stage, n_ctas, s);
-        case 11: return launch_stage_n<11>(a, recon, stage, n_ctas, s);
+        case 6: return launch_stage_n<6>(a, recon, stage, n_ctas, s, pdl);
+        case 7: return launch_stage_n<7>(a, recon, stage, n_ctas, s, pdl);
+        case 8: return launch_stage_n<8>(a, recon, stage, n_ctas, s, pdl);
+        case 9: return launch_stage_n<9>(a, recon, stage, n_ctas, s, pdl);
+        case 10: return launch_stage_n<10>(a, recon, stage, n_ctas, s, pdl);
+        case 11: return launch_stage_n<11>(a, recon, stage, n_ctas, s, pdl);
     }
     return cudaErrorInvalidValue;
 }

@@ -60,6 +60,19 @@ struct StageArgs {
     const unsigned int* halo_wait;       // own halo flags, by source rank
     unsigned long long halo_wait_mask;
     unsigned int halo_wait_seq;
+    // Single-rank dataflow between the stages of one step.  Stages 2 and 3
+    // are launched as programmatic dependents (PDL) of the previous stage, so
+    // their CTAs start in the previous stage's last wave instead of after it.
+    // A CTA then waits until its own sub-grid and its six face neighbours
+    // finished the previous stage (flow_wait[h] >= flow_seq, acquire) — the
+    // only data a stage reads — and publishes its own completion
+    // (flow_done[g] = flow_seq, release).  pdl_trigger: this launch lets its
+    // dependent start once every CTA is running (block 0 of stage 1 first
+    // zeroes amax_reset, which stage 3 accumulates into).
+    const unsigned int* flow_wait;       // nullptr: no wait (stream order)
+    unsigned int* flow_done;             // nullptr: no publish
+    unsigned int flow_seq;
+    int pdl_trigger;
     // Every cross-GPU spin gives up after wait_ns (globaltimer) and sets
     // *err (mapped host word) instead of hanging the GPU.
     unsigned long long* err;
@@ -67,7 +80,10 @@ struct StageArgs {
     double gamma, gm1, cfl, dx, p_floor;
 };
 
-cudaError_t launch_stage(const StageArgs& a, int nf, int recon, int stage, int n_ctas, cudaStream_t s);
+// pdl: launch as a programmatic dependent of the previous kernel on `s`
+// (cudaLaunchAttributeProgrammaticStreamSerialization; see StageArgs::flow_*).
+cudaError_t launch_stage(const StageArgs& a, int nf, int recon, int stage, int n_ctas, cudaStream_t s,
+                         bool pdl = false);
 cudaError_t launch_signal(const double* U, int nf, long long n_grids, double gamma, double p_floor,
                           double* amax, unsigned long long* stamp, int sms, cudaStream_t s);
 cudaError_t launch_init_random(double* U, int nf, const long long* gid, long long n_grids, uint64_t seed,

@@ -61,6 +61,9 @@ constexpr int kFaces = N + 1;
 #else
 #define TS_MINB_FOR(NF) (Lanes<NF>::min_blocks)
 #endif
+#ifndef TS_LAZY_DT
+#define TS_LAZY_DT 1
+#endif
 #ifndef TS_KEEP_DL
 #define TS_KEEP_DL 0
 #endif
@@ -569,6 +572,30 @@ __device__ __forceinline__ void wait_flag(const StageArgs& A, const unsigned int
     }
 }
 
+// Dataflow wait (single rank, see StageArgs::flow_*): acquire-spin until
+// *flag >= seq (wrapping compare), backing off with nanosleep so a waiting CTA
+// takes few issue slots from the previous stage's CTAs on the same SM.  The
+// producers are all resident (PDL starts this grid only once every CTA of the
+// previous one runs), so the wait is bounded; the deadline only guards bugs.
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void flow_wait_one(const StageArgs& A, const unsigned int* flag, unsigned int seq) {
+    if ((int)(ld_acquire_gpu(flag) - seq) >= 0) return;
+    const unsigned long long t0 = globaltimer();
+    unsigned int ns = 32;
+    while ((int)(ld_acquire_gpu(flag) - seq) < 0) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+        if (globaltimer() - t0 > A.wait_ns) {
+            if (A.err != nullptr) *reinterpret_cast<volatile unsigned long long*>(A.err) = 1ull;
+            return;
+        }
+    }
+}
+
 // Fused halo push of one boundary sub-grid (see StageArgs): copy the 3-deep
 // slab of every face with a foreign neighbour from this CTA's fresh U^(k)
 // into the peer's proxy slot (same in-sub-grid layout), then count the CTA
@@ -660,13 +687,38 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                     wait_flag(A, A.halo_wait + q, A.halo_wait_seq);
         __syncthreads();
     }
+    if (A.pdl_trigger) {
+        if (STAGE == 1 && blockIdx.x == 0) {
+            // the slot stage 3 accumulates into is zeroed before any dependent can start
+            if (t == 0 && A.amax_reset != nullptr) {
+                *A.amax_reset = 0.0;
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+    if (A.flow_wait != nullptr) {
+        // U^(k-1) of this sub-grid and of its face neighbours: the previous stage's output
+        if (t == 0) {
+            flow_wait_one(A, A.flow_wait + g, A.flow_seq);
+            for (int d = 0; d < 6; ++d) {
+                const int h = __ldg(A.nbr + 6 * g + d);
+                if (h >= 0) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
+            }
+        }
+        __syncthreads();
+    }
+    // TS_LAZY_DT: dt enters only the z sweep's update, so its two IEEE
+    // divisions can be done there, off the CTA's start-up path
     double amax_in = A.amax_in[0];
     for (int i = 1; i < A.amax_n; ++i) amax_in = fmax(amax_in, A.amax_in[i]);
-    const double dt = (A.cfl * A.dx) / amax_in;
-    const double dtdx = dt / A.dx;
+#if !TS_LAZY_DT
+    const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / A.dx);
+#endif
     if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
-        if (A.dt_out != nullptr) *A.dt_out = dt;
-        if (A.amax_reset != nullptr) *A.amax_reset = 0.0;
+        if (A.dt_out != nullptr) *A.dt_out = (A.cfl * A.dx) / amax_in;
+        if (A.amax_reset != nullptr && !A.pdl_trigger) *A.amax_reset = 0.0;
     }
     StageCtx c;
     c.Un = A.Un;
@@ -675,7 +727,6 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     c.cache = smem + StageSmem<NF>::dU;
     c.own = (size_t)g * NF * NC;
     c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
-    c.dtdx = 0.5 * dtdx;  // the sweeps carry twice the KT flux (kt2)
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
     const double* own = A.Uprev + c.own;
     const int pen = Lanes<NF>::pair ? t >> 1 : t;
@@ -694,6 +745,14 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         p.ss = axis == 0 ? 1 : (axis == 1 ? N : N * N);
         // fields in (rho, s_normal, s_t1, s_t2, E, tau) order, t1 < t2
         const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
+        if (axis == 2) {
+#if TS_LAZY_DT
+            const double dt = (A.cfl * A.dx) / amax_in;
+            c.dtdx = 0.5 * (dt / A.dx);  // the sweeps carry twice the KT flux (kt2)
+#else
+            c.dtdx = dtdx_early;
+#endif
+        }
         if (Lanes<NF>::pair) {
             if (axis == 0)
                 sweep_pair<NF, RECON, STAGE, 0>(c, p, fm, amax);
@@ -718,6 +777,14 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         if ((t & 31) == 0) atomic_max_nonneg(A.amax_out, amax);
+    }
+    if (A.flow_done != nullptr) {
+        // U^(k) of this sub-grid complete: CTA barrier, one gpu-scope fence, flag
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            atomicExch(A.flow_done + g, A.flow_seq);
+        }
     }
     if (A.done_ctr != nullptr) {
         // threadfence reduction to the last CTA of the stage (see StageArgs)
@@ -754,7 +821,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 }
 
 template <int NF, int RECON, int STAGE>
-inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s) {
+inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
     const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
     static bool configured = false;
     if (!configured) {
@@ -763,23 +830,36 @@ inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    stage_kernel<NF, RECON, STAGE><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);
-    return cudaGetLastError();
+    if (!pdl) {
+        stage_kernel<NF, RECON, STAGE><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)n_ctas);
+    cfg.blockDim = dim3((unsigned)Lanes<NF>::threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, stage_kernel<NF, RECON, STAGE>, a);
 }
 
 template <int NF, int RECON>
-inline cudaError_t launch_stage_r(const StageArgs& a, int stage, int n, cudaStream_t s) {
+inline cudaError_t launch_stage_r(const StageArgs& a, int stage, int n, cudaStream_t s, bool pdl) {
     switch (stage) {
-        case 1: return launch_stage_t<NF, RECON, 1>(a, n, s);
-        case 2: return launch_stage_t<NF, RECON, 2>(a, n, s);
-        case 3: return launch_stage_t<NF, RECON, 3>(a, n, s);
+        case 1: return launch_stage_t<NF, RECON, 1>(a, n, s, pdl);
+        case 2: return launch_stage_t<NF, RECON, 2>(a, n, s, pdl);
+        case 3: return launch_stage_t<NF, RECON, 3>(a, n, s, pdl);
     }
     return cudaErrorInvalidValue;
 }
 
 template <int NF>
-cudaError_t launch_stage_n(const StageArgs& a, int recon, int stage, int n, cudaStream_t s) {
-    return recon == 0 ? launch_stage_r<NF, 0>(a, stage, n, s) : launch_stage_r<NF, 1>(a, stage, n, s);
+cudaError_t launch_stage_n(const StageArgs& a, int recon, int stage, int n, cudaStream_t s, bool pdl) {
+    return recon == 0 ? launch_stage_r<NF, 0>(a, stage, n, s, pdl) : launch_stage_r<NF, 1>(a, stage, n, s, pdl);
 }
 
 }  // namespace tsh

@@ -2,5 +2,5 @@
 #include "hydro_stage.cuh"
 
 namespace tsh {
-template cudaError_t launch_stage_n<10>(const StageArgs&, int, int, int, cudaStream_t);
+template cudaError_t launch_stage_n<10>(const StageArgs&, int, int, int, cudaStream_t, bool);
 }  // namespace tsh
