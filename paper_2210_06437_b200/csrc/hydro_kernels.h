@@ -72,6 +72,7 @@ struct StageArgs {
     const unsigned int* flow_wait;       // nullptr: no wait (stream order)
     unsigned int* flow_done;             // nullptr: no publish
     unsigned int flow_seq;
+    int flow_n;                          // owned sub-grids (flag count); proxies are gated by the halo flags
     int pdl_trigger;
     // Every cross-GPU spin gives up after wait_ns (globaltimer) and sets
     // *err (mapped host word) instead of hanging the GPU.

@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             flow_wait_one(A, A.flow_wait + g, A.flow_seq);
             for (int d = 0; d < 6; ++d) {
                 const int h = __ldg(A.nbr + 6 * g + d);
-                if (h >= 0) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
+                if (h >= 0 && h < A.flow_n) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
             }
         }
         __syncthreads();

@@ -763,7 +763,10 @@ int do_step(ts_hydro_ctx* c) {
     // fills is at most one wave of a stage, so it pays only for a few waves
     // (measured on B200: +2.7 % at 4096 sub-grids = 4.6 waves of 6 CTAs/SM,
     // -0.7 % at 32768 = 37 waves): used up to 10 waves.
-    const bool flow = !multi && c->flow && c->d_flow != nullptr && c->n_owned <= 10 * 6 * (int64_t)c->sms;
+    // With N ranks the same holds for the fused P2P exchange: foreign
+    // neighbours stay gated by the halo flags, local ones by the stage flags.
+    const bool flow = (!multi || fused_halo) && c->flow && c->d_flow != nullptr &&
+                      c->n_owned <= 10 * 6 * (int64_t)c->sms;
     if (flow) ++c->flow_seq;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
@@ -786,14 +789,15 @@ int do_step(ts_hydro_ctx* c) {
             a.gather_own = c->d_gather + (size_t)(push_seq & 1) * c->world;
             a.amax_global = c->d_scal + 4;
         }
+        if (flow) {
+            const size_t n = (size_t)c->n_owned;
+            a.flow_seq = c->flow_seq;
+            a.flow_n = (int)c->n_owned;
+            a.pdl_trigger = stage < 3;
+            a.flow_wait = stage > 1 ? c->d_flow + (size_t)(stage - 2) * n : nullptr;
+            a.flow_done = stage < 3 ? c->d_flow + (size_t)(stage - 1) * n : nullptr;
+        }
         if (!multi) {
-            if (flow) {
-                const size_t n = (size_t)c->n_owned;
-                a.flow_seq = c->flow_seq;
-                a.pdl_trigger = stage < 3;
-                a.flow_wait = stage > 1 ? c->d_flow + (size_t)(stage - 2) * n : nullptr;
-                a.flow_done = stage < 3 ? c->d_flow + (size_t)(stage - 1) * n : nullptr;
-            }
             rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0, flow && stage > 1);
             if (rc) return rc;
             continue;
@@ -827,7 +831,10 @@ int do_step(ts_hydro_ctx* c) {
             a.halo_flag = c->d_halo_flag;
             a.halo_flag_n = c->world;
             a.halo_seq = ++c->xseq;
-            rc = launch_stage_list(c, a, stage, c->d_order, c->n_owned, 0, 0, 0);
+            // a stage that began with the copy-engine refresh waits on its
+            // event in stream order; the others start in the previous tail
+            rc = launch_stage_list(c, a, stage, c->d_order, c->n_owned, 0, 0, 0,
+                                   flow && stage > 1 && a.halo_wait != nullptr);
             if (rc) return rc;
             c->halo_pushed = true;
             continue;
