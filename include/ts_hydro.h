@@ -211,6 +211,69 @@ int ts_hydro_halo_exchange(ts_hydro_ctx* ctx);
 int ts_hydro_selftest_math(ts_hydro_ctx* ctx, uint64_t n, uint64_t seed, int32_t emax, uint64_t* bad_rcp,
                            uint64_t* bad_sqrt);
 
+/* ---- persisted state (checkpoint / restart) ------------------------------------ */
+/* FP64 field dump + mesh (the reference persists only
+ * profiles, codec.cpp:17-225, whose magic/version/length-checked layout this
+ * follows).  Layout: paper_2210_06437_b200/csrc/ts_hydro_ckpt.cpp.  Every
+ * reader validates magic, version, sizes and an FNV-1a 64 payload checksum
+ * (TS_EINVAL on any mismatch). */
+typedef struct ts_hydro_checkpoint_header {
+    uint32_t version;
+    int32_t nf, n_species, recon, cells_per_edge;
+    double gamma, cfl, dx, p_floor;
+    int64_t n_grids;   /* global mesh size                 */
+    int64_t n_records; /* sub-grids stored in this file    */
+    uint64_t steps_done;
+    int32_t world, rank; /* of the writer                  */
+    uint64_t checksum;
+} ts_hydro_checkpoint_header;
+
+/* Host-only (no GPU): write / inspect / read one checkpoint file.  state is
+ * [n_records][nf][512] in global_ids order. */
+int ts_hydro_checkpoint_write(const char* path, const ts_hydro_config* cfg, int64_t n_grids,
+                              const int64_t* neighbor_ids, const int32_t* owner, int32_t world, int32_t rank,
+                              int64_t n_records, const int64_t* global_ids, const double* state,
+                              uint64_t steps_done);
+int ts_hydro_checkpoint_info(const char* path, ts_hydro_checkpoint_header* out);
+/* Any output may be NULL (section skipped). */
+int ts_hydro_checkpoint_read(const char* path, int64_t* neighbor_ids, int32_t* owner, int64_t* global_ids,
+                             double* state);
+/* This context's U^n (its owned sub-grids) + the global mesh -> `path`. */
+int ts_hydro_save(ts_hydro_ctx* ctx, const char* path);
+/* U^n of this context's owned sub-grids from the files of a checkpoint (one
+ * per writing rank; any rank count): the bound mesh must equal the stored one
+ * (ownership may differ) and the numerics parameters must match. */
+int ts_hydro_restore(ts_hydro_ctx* ctx, const char* const* paths, int32_t n_paths);
+/* The bound global mesh (any output may be NULL) and the context's config. */
+int ts_hydro_get_mesh(const ts_hydro_ctx* ctx, int64_t* n_grids, int64_t* neighbor_ids, int32_t* owner,
+                      int32_t* world, int32_t* rank);
+int ts_hydro_get_config(const ts_hydro_ctx* ctx, ts_hydro_config* out);
+
+/* ---- the rest of the SimDevice contract on the real device ------------------- */
+/* SimDevice::launch_kernel (device.hpp:57-58, device.cpp:24-32): a named
+ * launch that occupies `stream_id` for duration_ns on the GPU (one timed
+ * thread), FIFO per stream, overlapping across streams; one kernel record
+ * named `name` (interned: the pointer stays valid for the context's life).
+ * TS_EINVAL: zero duration, bad stream, NULL/empty name.  `done` as for
+ * ts_hydro_launch_stage.  Usable on a context without a mesh. */
+int ts_hydro_launch_kernel(ts_hydro_ctx* ctx, const char* name, uint32_t stream_id, uint64_t duration_ns,
+                           uint64_t correlation_guid, ts_done_fn done, void* user);
+/* SimDevice::enqueue_copy (device.hpp:60-61, device.cpp:34-52): a real copy of
+ * `bytes` between context-owned staging buffers in direction `kind`
+ * (TS_ACTIVITY_COPY_H2D / _D2H / _D2D; pinned host <-> device), on the
+ * stream, with a device-stamped record carrying the bytes.  TS_EINVAL: not a
+ * copy kind, zero bytes, bad stream. */
+int ts_hydro_enqueue_copy(ts_hydro_ctx* ctx, int32_t kind, uint64_t bytes, uint32_t stream_id,
+                          uint64_t correlation_guid, ts_done_fn done, void* user);
+/* SimDevice::device_alloc / device_free (device.hpp:62-63, device.cpp:132-199):
+ * cudaMalloc / cudaFree with alloc / free records (stream -1, bytes) and
+ * memory counters; handles are opaque non-zero ids.  TS_EINVAL: zero bytes,
+ * unknown or already-freed handle. */
+int ts_hydro_device_alloc(ts_hydro_ctx* ctx, uint64_t bytes, uint64_t* handle);
+int ts_hydro_device_free(ts_hydro_ctx* ctx, uint64_t handle);
+/* Device address behind a handle (for callers that fill the buffer). */
+int ts_hydro_device_ptr(const ts_hydro_ctx* ctx, uint64_t handle, void** ptr);
+
 /* ---- timing hook -------------------------------------------------------------- */
 int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void* user);
 /* SimDevice::flush_activity: waits for in-flight work, returns completed

@@ -66,6 +66,41 @@ public:
         return token;
     }
 
+    // The rest of SimDevice's public surface (device.hpp:57-64) on the GPU, so
+    // a CudaHydroDevice stands in for the SimDevice a Locality owns: named
+    // launches occupy their stream for the requested time (the gravity
+    // kernels of workload.cpp:565-569), copies really move `bytes`.
+    CompletionToken launch_kernel(const std::string& name, std::uint32_t stream_id, std::uint64_t duration_ns,
+                                  Guid guid) {
+        auto* promise = new PromiseHandle();
+        CompletionToken token = promise->token();
+        const int rc = ts_hydro_launch_kernel(ctx_, name.c_str(), stream_id, duration_ns, guid, &fulfil, promise);
+        if (rc != TS_OK) {
+            delete promise;
+            check(rc, "launch_kernel");
+        }
+        return token;
+    }
+
+    CompletionToken enqueue_copy(ActivityKind kind, std::uint64_t bytes, std::uint32_t stream_id, Guid guid) {
+        auto* promise = new PromiseHandle();
+        CompletionToken token = promise->token();
+        const int rc = ts_hydro_enqueue_copy(ctx_, static_cast<std::int32_t>(kind), bytes, stream_id, guid, &fulfil,
+                                             promise);
+        if (rc != TS_OK) {
+            delete promise;
+            check(rc, "enqueue_copy");
+        }
+        return token;
+    }
+
+    std::uint64_t device_alloc(std::uint64_t bytes) {
+        std::uint64_t h = 0;
+        check(ts_hydro_device_alloc(ctx_, bytes, &h), "device_alloc");
+        return h;
+    }
+    void device_free(std::uint64_t handle) { check(ts_hydro_device_free(ctx_, handle), "device_free"); }
+
     // SimDevice::flush_activity(Profiler&): at-most-once, RunClock timestamps.
     std::uint64_t flush_activity(Profiler& sink) {
         std::uint64_t n = 0;

@@ -320,6 +320,38 @@ cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, 
     return cudaGetLastError();
 }
 
+// SimDevice::launch_kernel on a real GPU (reference device.cpp:24-32): one
+// thread occupies its stream for duration_ns of %globaltimer and stamps the
+// activity slot, so named simulated launches (e.g. the gravity kernels of
+// workload.cpp:565-569) become real device activity that serialises per
+// stream and overlaps across streams.
+__global__ void timed_kernel(unsigned long long duration_ns, unsigned long long* stamp) {
+    const unsigned long long t0 = globaltimer();
+    if (stamp != nullptr) stamp[0] = ~t0;
+    unsigned long long t = t0;
+    while (t - t0 < duration_ns) {
+        __nanosleep(duration_ns - (t - t0) > 2000ull ? 1000u : 64u);
+        t = globaltimer();
+    }
+    if (stamp != nullptr) stamp[1] = t;
+}
+
+// Activity stamp around a copy: which = 0 stores the start, 1 the end.
+__global__ void stamp_kernel(unsigned long long* stamp, int which) {
+    const unsigned long long t = globaltimer();
+    stamp[which] = which == 0 ? ~t : t;
+}
+
+cudaError_t launch_timed(unsigned long long duration_ns, unsigned long long* stamp, cudaStream_t s) {
+    timed_kernel<<<1, 1, 0, s>>>(duration_ns, stamp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(unsigned long long* stamp, int which, cudaStream_t s) {
+    stamp_kernel<<<1, 1, 0, s>>>(stamp, which);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_clock(unsigned long long* out, cudaStream_t s) {
     clock_kernel<<<1, 1, 0, s>>>(out);
     return cudaGetLastError();

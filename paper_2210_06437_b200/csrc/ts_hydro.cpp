@@ -29,6 +29,7 @@
 #include <map>
 #include <mutex>
 #include <new>
+#include <set>
 #include <string>
 #include <thread>
 #include <vector>
@@ -49,6 +50,7 @@ constexpr const char* kNamePack = "halo_pack_kernel";
 constexpr const char* kNameUnpack = "halo_unpack_kernel";
 constexpr const char* kNameH2D = "copy_host_to_device";
 constexpr const char* kNameD2H = "copy_device_to_host";
+constexpr const char* kNameD2D = "copy_device_to_device";
 constexpr const char* kNameAlloc = "device_alloc";
 constexpr const char* kNameFree = "device_free";
 
@@ -114,6 +116,7 @@ struct PendingLaunch {
     uint64_t guid;
     uint32_t slot;  // stamp slot
     bool overlap;   // PDL launch: may start before the previous kernel on its stream ended
+    uint64_t bytes = 0;  // copies (ts_hydro_enqueue_copy)
 };
 
 // Stream memory operation (driver API, resolved through the runtime so the
@@ -198,6 +201,8 @@ struct ts_hydro_ctx {
     // device memory
     double* U[3] = {nullptr, nullptr, nullptr};
     int32_t* d_nbr = nullptr;
+    std::vector<int64_t> mesh_nbr;    // the bound global mesh (checkpoints)
+    std::vector<int32_t> mesh_owner;
     int32_t* d_interior = nullptr;
     int32_t* d_boundary = nullptr;
     int32_t* d_order = nullptr;       // launch order of the fused P2P stage: boundary spread through the front
@@ -219,6 +224,14 @@ struct ts_hydro_ctx {
     std::map<void*, uint64_t> dev_allocs;
     std::map<void*, uint64_t> host_allocs;
     ts_memory_state mem{};
+    // SimDevice-contract entry points (ts_hydro_launch_kernel / _enqueue_copy / _device_alloc)
+    std::set<std::string> names;                          // interned launch names (stable c_str)
+    std::map<uint64_t, std::pair<void*, uint64_t>> handles;  // device_alloc handle -> (ptr, bytes)
+    uint64_t next_handle = 1;
+    void* stage_dev = nullptr;   // copy staging (context-internal, not counted)
+    uint64_t stage_dev_bytes = 0;
+    void* stage_host = nullptr;
+    uint64_t stage_host_bytes = 0;
 
     // comm
     ncclComm_t comm = nullptr;
@@ -403,6 +416,10 @@ int harvest(ts_hydro_ctx* c) {
         r.stream_id = p.stream_id;
         r.name = p.name;
         r.correlation_guid = p.guid;
+        if (p.bytes > 0) {
+            r.has_bytes = 1;
+            r.bytes = p.bytes;
+        }
         const unsigned long long enc_start = st[2 * (size_t)p.slot];
         const unsigned long long end = st[2 * (size_t)p.slot + 1];
         if (enc_start == 0 || end == 0) continue;  // launch had no CTA (empty)
@@ -1065,6 +1082,10 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         dfree(ctx, &ctx->d_stamps);
         for (auto& kv : ctx->host_allocs) cudaFreeHost(kv.first);
         ctx->host_allocs.clear();
+        for (auto& kv : ctx->handles) cudaFree(kv.second.first);
+        ctx->handles.clear();
+        if (ctx->stage_dev) cudaFree(ctx->stage_dev);
+        if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
         if (ctx->h_clock) cudaFreeHost(ctx->h_clock);
         if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
         if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
@@ -1156,6 +1177,8 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     c->world = world;
     c->rank = rank;
     c->n_global = n;
+    c->mesh_nbr.assign(nbr, nbr + 6 * n);
+    c->mesh_owner.assign(owner, owner + n);
     c->owned_gid.clear();
     c->proxy_gid.clear();
     for (int64_t i = 0; i < n; ++i)
@@ -1884,6 +1907,187 @@ int ts_hydro_host_free(ts_hydro_ctx* c, void* ptr) {
     c->mem.current_host_pinned_bytes -= it->second;
     c->host_allocs.erase(it);
     cudaFreeHost(ptr);
+    return TS_OK;
+}
+
+int ts_hydro_get_mesh(const ts_hydro_ctx* c, int64_t* n_grids, int64_t* nbr, int32_t* owner, int32_t* world,
+                      int32_t* rank) {
+    if (c == nullptr) return TS_EINVAL;
+    if (!c->have_mesh) return TS_ESTATE;
+    if (n_grids) *n_grids = c->n_global;
+    if (nbr) std::copy(c->mesh_nbr.begin(), c->mesh_nbr.end(), nbr);
+    if (owner) std::copy(c->mesh_owner.begin(), c->mesh_owner.end(), owner);
+    if (world) *world = c->world;
+    if (rank) *rank = c->rank;
+    return TS_OK;
+}
+
+int ts_hydro_get_config(const ts_hydro_ctx* c, ts_hydro_config* out) {
+    if (c == nullptr || out == nullptr) return TS_EINVAL;
+    *out = c->cfg;
+    return TS_OK;
+}
+
+int ts_hydro_save(ts_hydro_ctx* c, const char* path) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (path == nullptr) return fail(c, TS_EINVAL, "null checkpoint path");
+    std::vector<double> st((size_t)c->n_owned * c->nf * kNC);
+    rc = ts_hydro_download(c, 0, c->n_owned, st.data());
+    if (rc) return rc;
+    rc = ts_hydro_checkpoint_write(path, &c->cfg, c->n_global, c->mesh_nbr.data(), c->mesh_owner.data(), c->world,
+                                   c->rank, c->n_owned, c->owned_gid.data(), st.data(), c->steps_done);
+    if (rc) return fail(c, rc, std::string("cannot write checkpoint ") + path);
+    return TS_OK;
+}
+
+int ts_hydro_restore(ts_hydro_ctx* c, const char* const* paths, int32_t n_paths) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (paths == nullptr || n_paths < 1) return fail(c, TS_EINVAL, "no checkpoint files");
+    const size_t per = (size_t)c->nf * kNC;
+    std::vector<double> st((size_t)c->n_owned * per);
+    std::vector<char> have((size_t)c->n_owned, 0);
+    int64_t found = 0;
+    for (int32_t k = 0; k < n_paths; ++k) {
+        const std::string name = paths[k] != nullptr ? paths[k] : "(null)";
+        ts_hydro_checkpoint_header h{};
+        if (paths[k] == nullptr || ts_hydro_checkpoint_info(paths[k], &h) != TS_OK)
+            return fail(c, TS_EINVAL, "checkpoint " + name + ": unreadable, truncated or corrupt");
+        if (h.nf != c->nf || h.recon != c->cfg.recon || h.gamma != c->cfg.gamma || h.cfl != c->cfg.cfl ||
+            h.dx != c->cfg.dx || h.p_floor != c->cfg.p_floor)
+            return fail(c, TS_EINVAL, "checkpoint " + name + ": numerics parameters differ from this context");
+        if (h.n_grids != c->n_global) return fail(c, TS_EINVAL, "checkpoint " + name + ": mesh size differs");
+        std::vector<int64_t> nbr((size_t)h.n_grids * 6), gid((size_t)h.n_records);
+        std::vector<double> rec((size_t)h.n_records * per);
+        if (ts_hydro_checkpoint_read(paths[k], nbr.data(), nullptr, gid.data(), rec.data()) != TS_OK)
+            return fail(c, TS_EINVAL, "checkpoint " + name + ": read failed");
+        if (nbr != c->mesh_nbr) return fail(c, TS_EINVAL, "checkpoint " + name + ": mesh links differ");
+        for (int64_t r = 0; r < h.n_records; ++r) {
+            auto it = std::lower_bound(c->owned_gid.begin(), c->owned_gid.end(), gid[(size_t)r]);
+            if (it == c->owned_gid.end() || *it != gid[(size_t)r]) continue;  // another rank's sub-grid
+            const size_t i = (size_t)(it - c->owned_gid.begin());
+            if (!have[i]) ++found;
+            have[i] = 1;
+            std::copy(rec.begin() + (ptrdiff_t)((size_t)r * per), rec.begin() + (ptrdiff_t)((size_t)(r + 1) * per),
+                      st.begin() + (ptrdiff_t)(i * per));
+        }
+    }
+    if (found != c->n_owned)
+        return fail(c, TS_EINVAL, "checkpoint does not cover every owned sub-grid (" + std::to_string(found) + " of " +
+                                      std::to_string(c->n_owned) + ")");
+    return ts_hydro_upload(c, 0, c->n_owned, st.data());
+}
+
+// ---- the rest of the SimDevice contract on the real device -----------------
+int ts_hydro_launch_kernel(ts_hydro_ctx* c, const char* name, uint32_t stream_id, uint64_t duration_ns,
+                           uint64_t guid, ts_done_fn done, void* user) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    if (duration_ns == 0) return fail(c, TS_EINVAL, "kernel duration must be positive");
+    if (name == nullptr || *name == '\0') return fail(c, TS_EINVAL, "kernel name must be non-empty");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, stream_id, &s);
+    if (rc) return rc;
+    const char* interned = c->names.insert(name).first->c_str();
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, interned, (int32_t)stream_id, guid, &stamp);
+    if (rc) return rc;
+    TS_CUDA(c, tsh::launch_timed(duration_ns, stamp, s));
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    return TS_OK;
+}
+
+int ts_hydro_enqueue_copy(ts_hydro_ctx* c, int32_t kind, uint64_t bytes, uint32_t stream_id, uint64_t guid,
+                          ts_done_fn done, void* user) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    if (kind != TS_ACTIVITY_COPY_H2D && kind != TS_ACTIVITY_COPY_D2H && kind != TS_ACTIVITY_COPY_D2D)
+        return fail(c, TS_EINVAL, "not a copy kind");
+    if (bytes == 0) return fail(c, TS_EINVAL, "copy of zero bytes");
+    cudaSetDevice(c->dev);
+    cudaStream_t s;
+    rc = ensure_stream(c, stream_id, &s);
+    if (rc) return rc;
+    const uint64_t dev_need = kind == TS_ACTIVITY_COPY_D2D ? 2 * bytes : bytes;
+    const uint64_t host_need = kind == TS_ACTIVITY_COPY_D2D ? 0 : bytes;
+    if (dev_need > c->stage_dev_bytes || host_need > c->stage_host_bytes) {
+        // grow the staging buffers (in-flight copies may still use the old ones)
+        rc = sync_all(c);
+        if (rc) return rc;
+        if (dev_need > c->stage_dev_bytes) {
+            if (c->stage_dev) cudaFree(c->stage_dev);
+            c->stage_dev = nullptr;
+            c->stage_dev_bytes = 0;
+            TS_CUDA(c, cudaMalloc(&c->stage_dev, dev_need));
+            c->stage_dev_bytes = dev_need;
+        }
+        if (host_need > c->stage_host_bytes) {
+            if (c->stage_host) cudaFreeHost(c->stage_host);
+            c->stage_host = nullptr;
+            c->stage_host_bytes = 0;
+            TS_CUDA(c, cudaHostAlloc(&c->stage_host, host_need, cudaHostAllocDefault));
+            c->stage_host_bytes = host_need;
+        }
+    }
+    const char* name = kind == TS_ACTIVITY_COPY_H2D ? kNameH2D : (kind == TS_ACTIVITY_COPY_D2H ? kNameD2H : kNameD2D);
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, (uint8_t)kind, name, (int32_t)stream_id, guid, &stamp);
+    if (rc) return rc;
+    c->pending.back().bytes = bytes;
+    char* d = static_cast<char*>(c->stage_dev);
+    TS_CUDA(c, tsh::launch_stamp(stamp, 0, s));
+    if (kind == TS_ACTIVITY_COPY_H2D)
+        TS_CUDA(c, cudaMemcpyAsync(d, c->stage_host, bytes, cudaMemcpyHostToDevice, s));
+    else if (kind == TS_ACTIVITY_COPY_D2H)
+        TS_CUDA(c, cudaMemcpyAsync(c->stage_host, d, bytes, cudaMemcpyDeviceToHost, s));
+    else
+        TS_CUDA(c, cudaMemcpyAsync(d + bytes, d, bytes, cudaMemcpyDeviceToDevice, s));
+    TS_CUDA(c, tsh::launch_stamp(stamp, 1, s));
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    return TS_OK;
+}
+
+int ts_hydro_device_alloc(ts_hydro_ctx* c, uint64_t bytes, uint64_t* handle) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (bytes == 0 || handle == nullptr) return fail(c, TS_EINVAL, "zero-byte allocation");
+    if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
+    cudaSetDevice(c->dev);
+    char* p = nullptr;
+    rc = dalloc(c, &p, (size_t)bytes);  // counted + alloc record, like SimDevice::device_alloc
+    if (rc) return rc;
+    const uint64_t h = c->next_handle++;
+    c->handles[h] = {p, bytes};
+    *handle = h;
+    return TS_OK;
+}
+
+int ts_hydro_device_free(ts_hydro_ctx* c, uint64_t handle) {
+    if (c == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    auto it = c->handles.find(handle);
+    if (it == c->handles.end()) return fail(c, TS_EINVAL, "free of unknown or already-freed device handle");
+    cudaSetDevice(c->dev);
+    char* p = static_cast<char*>(it->second.first);
+    c->handles.erase(it);
+    dfree(c, &p);  // free record
+    return TS_OK;
+}
+
+int ts_hydro_device_ptr(const ts_hydro_ctx* c, uint64_t handle, void** ptr) {
+    if (c == nullptr || ptr == nullptr) return TS_EINVAL;
+    auto it = c->handles.find(handle);
+    if (it == c->handles.end()) return TS_EINVAL;
+    *ptr = it->second.first;
     return TS_OK;
 }
 

@@ -90,6 +90,15 @@ class _MemState(ctypes.Structure):
                                                "current_host_pinned_bytes", "peak_host_pinned_bytes")]
 
 
+class _CkptHeader(ctypes.Structure):
+    """ts_hydro_checkpoint_header (ts_hydro.h)."""
+    _fields_ = [("version", ctypes.c_uint32), ("nf", ctypes.c_int32), ("n_species", ctypes.c_int32),
+                ("recon", ctypes.c_int32), ("cells_per_edge", ctypes.c_int32), ("gamma", ctypes.c_double),
+                ("cfl", ctypes.c_double), ("dx", ctypes.c_double), ("p_floor", ctypes.c_double),
+                ("n_grids", ctypes.c_int64), ("n_records", ctypes.c_int64), ("steps_done", ctypes.c_uint64),
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("checksum", ctypes.c_uint64)]
+
+
 _lib = None
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -145,6 +154,22 @@ _SIGNATURES = {
     "ts_hydro_clock_ns": (ctypes.c_uint64, []),
     "ts_hydro_host_alloc": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.POINTER(_vp)]),
     "ts_hydro_host_free": (ctypes.c_int, [_vp, _vp]),
+    "ts_hydro_checkpoint_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_Config), ctypes.c_int64, _i64p,
+                                                 _i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _i64p,
+                                                 _f64p, ctypes.c_uint64]),
+    "ts_hydro_checkpoint_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_CkptHeader)]),
+    "ts_hydro_checkpoint_read": (ctypes.c_int, [ctypes.c_char_p, _i64p, _i32p, _i64p, _f64p]),
+    "ts_hydro_save": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "ts_hydro_restore": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int32]),
+    "ts_hydro_get_mesh": (ctypes.c_int, [_vp, _i64p, _i64p, _i32p, _i32p, _i32p]),
+    "ts_hydro_get_config": (ctypes.c_int, [_vp, ctypes.POINTER(_Config)]),
+    "ts_hydro_launch_kernel": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                              DONE_FN, _vp]),
+    "ts_hydro_enqueue_copy": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                             DONE_FN, _vp]),
+    "ts_hydro_device_alloc": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p]),
+    "ts_hydro_device_free": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "ts_hydro_device_ptr": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.POINTER(_vp)]),
 }
 
 
@@ -485,6 +510,27 @@ class CudaDevice:
     def init_random(self, seed: int = 2210) -> None:
         self._check(lib().ts_hydro_init_random(self._h, seed), "init_random")
 
+    # -- persisted state (ts_hydro_ckpt.cpp)
+    def save(self, path: str) -> None:
+        """U^n of the owned sub-grids + the global mesh -> one checkpoint file."""
+        self._check(lib().ts_hydro_save(self._h, os.fsencode(path)), "save")
+
+    def restore(self, paths) -> None:
+        """U^n of the owned sub-grids from a checkpoint's files (any writer rank count)."""
+        paths = [paths] if isinstance(paths, (str, os.PathLike)) else list(paths)
+        arr = (ctypes.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+        self._check(lib().ts_hydro_restore(self._h, arr, len(paths)), "restore")
+
+    def mesh(self) -> "Mesh":
+        """The bound global mesh (Mesh without positions)."""
+        n, w, r = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(lib().ts_hydro_get_mesh(self._h, ctypes.byref(n), None, None, ctypes.byref(w), ctypes.byref(r)),
+                    "get_mesh")
+        nbr = np.zeros((n.value, 6), np.int64)
+        own = np.zeros(n.value, np.int32)
+        self._check(lib().ts_hydro_get_mesh(self._h, None, _p(nbr, _i64p), _p(own, _i32p), None, None), "get_mesh")
+        return Mesh(nbr, np.zeros((n.value, 3), np.int32), own, w.value)
+
     # -- stepping
     def compute_dt(self) -> float:
         dt = ctypes.c_double()
@@ -613,6 +659,38 @@ class CudaDevice:
     def host_pinned_free(self, ptr: int) -> None:
         self._check(lib().ts_hydro_host_free(self._h, ptr), "host_pinned_free")
 
+    # -- the rest of the SimDevice contract (device.hpp:57-64) on the GPU
+    def _done(self, done):
+        cb = DONE_FN(lambda _u: done()) if done is not None else DONE_FN()
+        if done is not None:
+            self._callbacks.append(cb)
+        return cb
+
+    def launch_kernel(self, name: str, stream_id: int, duration_ns: int, guid: int = 0, done=None) -> None:
+        """SimDevice::launch_kernel: `name` occupies `stream_id` for duration_ns on the GPU."""
+        self._check(lib().ts_hydro_launch_kernel(self._h, name.encode(), stream_id, duration_ns, guid,
+                                                 self._done(done), None), "launch_kernel")
+
+    def enqueue_copy(self, kind: str, nbytes: int, stream_id: int, guid: int = 0, done=None) -> None:
+        """SimDevice::enqueue_copy: a real copy of nbytes ("copy_host_to_device", ...)."""
+        k = ACTIVITY_KINDS.index(kind) if kind in ACTIVITY_KINDS else -1
+        self._check(lib().ts_hydro_enqueue_copy(self._h, k, nbytes, stream_id, guid, self._done(done), None),
+                    "enqueue_copy")
+
+    def device_alloc(self, nbytes: int) -> int:
+        h = ctypes.c_uint64()
+        self._check(lib().ts_hydro_device_alloc(self._h, nbytes, ctypes.byref(h)), "device_alloc")
+        return h.value
+
+    def device_free(self, handle: int) -> None:
+        self._check(lib().ts_hydro_device_free(self._h, handle), "device_free")
+
+    def device_ptr(self, handle: int) -> int:
+        p = _vp()
+        if lib().ts_hydro_device_ptr(self._h, handle, ctypes.byref(p)) != TS_OK:
+            raise ValueError("unknown device handle")
+        return p.value
+
 
 def clock_ns() -> int:
     return lib().ts_hydro_clock_ns()
@@ -673,3 +751,49 @@ class WorkloadSession:
         seconds = time.perf_counter() - t0
         return ScalingPoint(n=self.mesh.world_size, total_time_s=seconds,
                             cells_per_second=self.mesh.total_cells() * self.config.num_steps / seconds)
+
+
+# ---------------------------------------------------------------------------
+# Checkpoint files (host side, no GPU): ts_hydro_checkpoint_{write,info,read}
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class Checkpoint:
+    """One checkpoint file: header fields, the global mesh, and the stored
+    sub-grids' U^n ([n_records][nf][512], in global_ids order)."""
+    header: dict
+    neighbor_ids: np.ndarray
+    owner: np.ndarray
+    global_ids: np.ndarray
+    state: np.ndarray
+
+
+def write_checkpoint(path: str, cfg: HydroConfig, mesh: Mesh, global_ids, state, steps_done: int = 0,
+                     rank: int = 0) -> None:
+    gids = np.ascontiguousarray(global_ids, np.int64)
+    st = np.ascontiguousarray(state, np.float64)
+    if st.shape != (gids.size, cfg.nf, NC):
+        raise ValueError(f"state shape {st.shape} != ({gids.size}, {cfg.nf}, {NC})")
+    nbr = np.ascontiguousarray(mesh.neighbor_ids, np.int64)
+    own = np.ascontiguousarray(mesh.owner, np.int32)
+    c = cfg.to_c()
+    rc = lib().ts_hydro_checkpoint_write(os.fsencode(path), ctypes.byref(c), mesh.n, _p(nbr, _i64p), _p(own, _i32p),
+                                         mesh.world_size, rank, gids.size, _p(gids, _i64p), _p(st, _f64p),
+                                         steps_done)
+    if rc != TS_OK:
+        raise ValueError(f"cannot write checkpoint {path}")
+
+
+def read_checkpoint(path: str) -> Checkpoint:
+    """Validated read (magic, version, sizes, payload checksum); ValueError otherwise."""
+    h = _CkptHeader()
+    if lib().ts_hydro_checkpoint_info(os.fsencode(path), ctypes.byref(h)) != TS_OK:
+        raise ValueError(f"checkpoint {path}: unreadable, truncated or corrupt")
+    nbr = np.zeros((h.n_grids, 6), np.int64)
+    own = np.zeros(h.n_grids, np.int32)
+    gid = np.zeros(h.n_records, np.int64)
+    st = np.zeros((h.n_records, h.nf, NC), np.float64)
+    if lib().ts_hydro_checkpoint_read(os.fsencode(path), _p(nbr, _i64p), _p(own, _i32p), _p(gid, _i64p),
+                                      _p(st, _f64p)) != TS_OK:
+        raise ValueError(f"checkpoint {path}: read failed")
+    hdr = {k: getattr(h, k) for k, _ in _CkptHeader._fields_}
+    return Checkpoint(hdr, nbr, own, gid, st)
