@@ -164,6 +164,14 @@ int ts_hydro_step(ts_hydro_ctx* ctx, uint64_t nsteps);
 /* Host-buffer step (e2e path): U^n from `host_in`, nsteps steps, U^{n+nsteps}
  * to `host_out` (pinned or pageable), synchronous. */
 int ts_hydro_step_host(ts_hydro_ctx* ctx, const double* host_in, double* host_out, uint64_t nsteps);
+/* Pipelined form of ts_hydro_step_host (asynchronous; `done` fires once
+ * host_out holds the result; ts_hydro_synchronize waits for all).  Copies move
+ * in sub-grid chunks on their own streams; when host_in is the previous
+ * call's host_out (a simulation chained through host memory) each H2D chunk
+ * starts as soon as the previous call's D2H of that chunk landed, so the two
+ * PCIe directions overlap.  Host buffers must stay valid until `done`. */
+int ts_hydro_step_host_async(ts_hydro_ctx* ctx, const double* host_in, double* host_out, uint64_t nsteps,
+                             ts_done_fn done, void* user);
 int ts_hydro_synchronize(ts_hydro_ctx* ctx);
 /* nsteps steps bracketed by CUDA events on the compute stream (the stream
  * every launch of a step is ordered on); blocks and returns device ms. */

@@ -188,6 +188,14 @@ struct ts_hydro_ctx {
 
     std::vector<cudaStream_t> streams;  // lazily created; [0] compute, [1] comm, [2] boundary
     cudaEvent_t ev_in = nullptr, ev_halo = nullptr, ev_red = nullptr, ev_bnd = nullptr;
+    // ts_hydro_step_host_async: chunked copies on their own streams; the
+    // previous call's host_out and its per-chunk D2H completion events
+    static constexpr int kXferChunksMax = 64;
+    int xfer_chunks = 8;  // TS_HYDRO_XFER_CHUNKS
+    cudaEvent_t ev_d2h[kXferChunksMax] = {};
+    cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr;
+    const void* prev_out = nullptr;
+    size_t prev_out_bytes = 0;
 
     // mesh
     bool have_mesh = false;
@@ -994,6 +1002,8 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->dev = cfg->device_id;
     if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
+        c->xfer_chunks = std::max(1, std::min(ts_hydro_ctx::kXferChunksMax, std::atoi(w)));
     if (const char* w = std::getenv("TS_HYDRO_WAIT_TIMEOUT_MS")) c->wait_ns = 1000000ull * std::strtoull(w, nullptr, 10);
     if (cfg->device_id < 0) {
         c->host_only = true;
@@ -1091,6 +1101,10 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
         if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
         if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
+        for (cudaEvent_t& e : ctx->ev_d2h)
+            if (e) cudaEventDestroy(e);
+        if (ctx->ev_h2d) cudaEventDestroy(ctx->ev_h2d);
+        if (ctx->ev_comp) cudaEventDestroy(ctx->ev_comp);
         for (cudaStream_t s : ctx->streams)
             if (s) cudaStreamDestroy(s);
     }
@@ -1497,6 +1511,108 @@ int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out,
     return TS_OK;
 }
 
+namespace {
+struct DoneThunk {
+    ts_done_fn fn;
+    void* user;
+    int32_t* list;
+};
+void CUDART_CB done_host(void* p) {
+    auto* t = static_cast<DoneThunk*>(p);
+    if (t->fn) t->fn(t->user);
+    delete t;
+}
+}  // namespace
+
+// Pipelined host-buffer steps.  Copies run in xfer_chunks sub-grid ranges on
+// their own streams (H2D 3, D2H 4), so that when a call's input is the
+// previous call's output (a chained simulation through host memory) the H2D of
+// chunk i starts as soon as the previous call's D2H of chunk i landed, and the
+// two PCIe directions run concurrently.  Ordering: H2D chunk i waits for the
+// previous call's D2H of chunk i (or of everything if the host ranges overlap
+// otherwise) and for the compute stream's earlier work; the steps wait for
+// the whole H2D (dt needs every sub-grid); the D2H waits for the steps.
+int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* host_out, uint64_t nsteps,
+                             ts_done_fn done, void* user) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
+    if (c->cfg.stream_count < 5) return fail(c, TS_EINVAL, "pipelined host steps need stream_count >= 5");
+    cudaSetDevice(c->dev);
+    cudaStream_t s, sh, sd;
+    rc = ensure_stream(c, 0, &s);
+    if (!rc) rc = ensure_stream(c, 3, &sh);
+    if (!rc) rc = ensure_stream(c, 4, &sd);
+    if (rc) return rc;
+    if (c->ev_h2d == nullptr) {
+        for (cudaEvent_t& e : c->ev_d2h) TS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming));
+        TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_comp, cudaEventDisableTiming));
+    }
+    c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
+    const int C = c->xfer_chunks;
+    const size_t per = (size_t)c->nf * kNC * sizeof(double);
+    const size_t bytes = (size_t)c->n_owned * per;
+    auto chunk = [&](int i, size_t* off, size_t* len) {
+        const int64_t g0 = c->n_owned * i / C, g1 = c->n_owned * (i + 1) / C;
+        *off = (size_t)g0 * per;
+        *len = (size_t)(g1 - g0) * per;
+    };
+    const char* in_b = reinterpret_cast<const char*>(host_in);
+    const char* prev_b = static_cast<const char*>(c->prev_out);
+    const bool chained = c->prev_out == host_in && c->prev_out_bytes == bytes;
+    const bool overlap = prev_b != nullptr && in_b < prev_b + c->prev_out_bytes && prev_b < in_b + bytes;
+    // H2D: U^n may still be read by earlier work on the compute stream
+    TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+    TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_in, 0));
+    if (overlap && !chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[C - 1], 0));
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, 0, &stamp);
+    if (rc) return rc;
+    c->pending.back().bytes = bytes;
+    TS_CUDA(c, tsh::launch_stamp(stamp, 0, sh));
+    for (int i = 0; i < C; ++i) {
+        size_t off, len;
+        chunk(i, &off, &len);
+        if (chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[i], 0));
+        if (len > 0)
+            TS_CUDA(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->U[0]) + off, in_b + off, len,
+                                       cudaMemcpyHostToDevice, sh));
+    }
+    TS_CUDA(c, tsh::launch_stamp(stamp, 1, sh));
+    TS_CUDA(c, cudaEventRecord(c->ev_h2d, sh));
+    // the steps
+    TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
+    rc = do_compute_dt(c);
+    if (rc) return rc;
+    for (uint64_t k = 0; k < nsteps; ++k) {
+        rc = do_step(c);
+        if (rc) return rc;
+    }
+    TS_CUDA(c, cudaEventRecord(c->ev_comp, s));
+    // D2H
+    TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));
+    rc = begin_launch(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, 0, &stamp);
+    if (rc) return rc;
+    c->pending.back().bytes = bytes;
+    TS_CUDA(c, tsh::launch_stamp(stamp, 0, sd));
+    char* out_b = reinterpret_cast<char*>(host_out);
+    for (int i = 0; i < C; ++i) {
+        size_t off, len;
+        chunk(i, &off, &len);
+        if (len > 0)
+            TS_CUDA(c, cudaMemcpyAsync(out_b + off, reinterpret_cast<const char*>(c->U[0]) + off, len,
+                                       cudaMemcpyDeviceToHost, sd));
+        TS_CUDA(c, cudaEventRecord(c->ev_d2h[i], sd));
+    }
+    TS_CUDA(c, tsh::launch_stamp(stamp, 1, sd));
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(sd, done_host, new DoneThunk{done, user, nullptr}));
+    c->prev_out = host_out;
+    c->prev_out_bytes = bytes;
+    return TS_OK;
+}
+
 int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
     int rc = check_state(c);
     if (rc) return rc;
@@ -1564,18 +1680,6 @@ int ts_hydro_launch_count(const ts_hydro_ctx* c, uint64_t* launches) {
     return TS_OK;
 }
 
-namespace {
-struct DoneThunk {
-    ts_done_fn fn;
-    void* user;
-    int32_t* list;
-};
-void CUDART_CB done_host(void* p) {
-    auto* t = static_cast<DoneThunk*>(p);
-    if (t->fn) t->fn(t->user);
-    delete t;
-}
-}  // namespace
 
 int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_index, int64_t count,
                           uint32_t stream_id, uint64_t guid, ts_done_fn done, void* user) {

@@ -131,6 +131,7 @@ _SIGNATURES = {
     "ts_hydro_compute_dt": (ctypes.c_int, [_vp, _f64p]),
     "ts_hydro_step": (ctypes.c_int, [_vp, ctypes.c_uint64]),
     "ts_hydro_step_host": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64]),
+    "ts_hydro_step_host_async": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, DONE_FN, _vp]),
     "ts_hydro_synchronize": (ctypes.c_int, [_vp]),
     "ts_hydro_time_steps": (ctypes.c_int, [_vp, ctypes.c_uint64, _f64p]),
     "ts_hydro_last_dt": (ctypes.c_int, [_vp, _f64p]),
@@ -542,6 +543,11 @@ class CudaDevice:
 
     def step_host(self, host_in: int, host_out: int, nsteps: int = 1) -> None:
         self._check(lib().ts_hydro_step_host(self._h, host_in, host_out, nsteps), "step_host")
+
+    def step_host_async(self, host_in: int, host_out: int, nsteps: int = 1, done=None) -> None:
+        """Pipelined step_host (ts_hydro_step_host_async); synchronize() or `done` before reading host_out."""
+        self._check(lib().ts_hydro_step_host_async(self._h, host_in, host_out, nsteps, self._done(done), None),
+                    "step_host_async")
 
     def time_steps(self, nsteps: int) -> float:
         """nsteps steps bracketed by CUDA events on the compute stream; device ms."""
