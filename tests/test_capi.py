@@ -123,7 +123,9 @@ def test_host_only_context_refuses_compute(hydro):
 
 
 @pytest.mark.parametrize("dims,periodic,world", [((4, 4, 8), "", 2), ((4, 4, 8), "z", 2), ((4, 4, 16), "xyz", 4),
-                                                 ((3, 5, 2), "y", 3)])
+                                                 ((3, 5, 2), "y", 3), ((4, 4, 32), "z", 8),
+                                                 # the bench's 8-GPU weak-scaling mesh (8 x Sedov 16^3)
+                                                 ((16, 16, 128), "", 8)])
 def test_halo_plans_pair_up_across_ranks(hydro, dims, periodic, world):
     """What rank r sends to s is exactly what s expects from r, in the same
     wire order; one aggregated message per directed rank pair."""

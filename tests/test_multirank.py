@@ -109,9 +109,9 @@ def _worker(rank, world, port, dims, periodic, steps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("dims,periodic", [((4, 4, 4), ""), ((2, 2, 4), "z"), ((3, 2, 2), "xy")])
-def test_partitioned_step_equals_single_domain_bitwise(hydro, oracle_lib, dims, periodic):
-    world = 2
+@pytest.mark.parametrize("dims,periodic,world", [((4, 4, 4), "", 2), ((2, 2, 4), "z", 2), ((3, 2, 2), "xy", 2),
+                                                 ((2, 2, 8), "z", 4)])
+def test_partitioned_step_equals_single_domain_bitwise(hydro, oracle_lib, dims, periodic, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
