@@ -74,6 +74,12 @@ struct StageArgs {
     unsigned int flow_seq;
     int flow_n;                          // owned sub-grids (flag count); proxies are gated by the halo flags
     int pdl_trigger;
+    // Stage 3 of a pipelined host step (ts_hydro_step_host_async): each CTA
+    // counts its sub-grid into chunk_ctr[g * chunk_n / chunk_owned] after a
+    // system-scope fence, so the D2H of a chunk can start (stream wait on the
+    // counter) while the rest of the stage still runs.
+    unsigned int* chunk_ctr;             // nullptr: no counting
+    int chunk_n, chunk_owned;
     // Every cross-GPU spin gives up after wait_ns (globaltimer) and sets
     // *err (mapped host word) instead of hanging the GPU.
     unsigned long long* err;

@@ -796,6 +796,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         if ((t & 31) == 0) atomic_max_nonneg(A.amax_out, amax);
     }
+    if (STAGE == 3 && A.chunk_ctr != nullptr) {
+        __syncthreads();
+        if (t == 0) {
+            __threadfence_system();  // U^(n+1) of this sub-grid visible to the copy engine
+            atomicAdd(A.chunk_ctr + (int)(((long long)g * A.chunk_n) / A.chunk_owned), 1u);
+        }
+    }
     if (A.flow_done != nullptr) {
         // U^(k) of this sub-grid complete: CTA barrier, one gpu-scope fence, flag
         __syncthreads();

@@ -127,6 +127,7 @@ struct PendingLaunch {
 struct StreamMemOps {
     bool ok = false;
     CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
 };
 
 StreamMemOps& memops() {
@@ -139,6 +140,9 @@ StreamMemOps& memops() {
             m.write32 = reinterpret_cast<decltype(m.write32)>(w);
             m.ok = true;
         }
+        void* v = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q) == cudaSuccess && v)
+            m.wait32 = reinterpret_cast<decltype(m.wait32)>(v);
     });
     return m;
 }
@@ -192,10 +196,14 @@ struct ts_hydro_ctx {
     // previous call's host_out and its per-chunk D2H completion events
     static constexpr int kXferChunksMax = 64;
     int xfer_chunks = 8;  // TS_HYDRO_XFER_CHUNKS
+    bool chunk_overlap = true;  // TS_HYDRO_CHUNK_OVERLAP=0: D2H waits for the whole last stage
     cudaEvent_t ev_d2h[kXferChunksMax] = {};
     cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr;
     const void* prev_out = nullptr;
     size_t prev_out_bytes = 0;
+    uint32_t* d_chunk_ctr = nullptr;          // [kXferChunksMax] stage-3 completions per D2H chunk
+    uint32_t chunk_expect[kXferChunksMax] = {};  // running totals (wrapping)
+    bool chunk_arm = false;                   // next stage-3 launch counts into d_chunk_ctr
 
     // mesh
     bool have_mesh = false;
@@ -396,6 +404,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_boundary);
     dfree(c, &c->d_order);
     dfree(c, &c->d_flow);
+    dfree(c, &c->d_chunk_ctr);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
     dfree(c, &c->d_gid);
@@ -799,6 +808,11 @@ int do_step(ts_hydro_ctx* c) {
             a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
         }
+        if (stage == 3 && c->chunk_arm) {
+            a.chunk_ctr = c->d_chunk_ctr;
+            a.chunk_n = c->xfer_chunks;
+            a.chunk_owned = (int)c->n_owned;
+        }
         if (p2p && stage == 3) {
             a.done_ctr = c->d_ctr;
             a.total_ctas = (int)c->n_owned;
@@ -1002,6 +1016,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->dev = cfg->device_id;
     if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
         c->xfer_chunks = std::max(1, std::min(ts_hydro_ctx::kXferChunksMax, std::atoi(w)));
     if (const char* w = std::getenv("TS_HYDRO_WAIT_TIMEOUT_MS")) c->wait_ns = 1000000ull * std::strtoull(w, nullptr, 10);
@@ -1567,8 +1582,8 @@ void CUDART_CB done_host(void* p) {
 // previous call's output (a chained simulation through host memory) the H2D of
 // chunk i starts as soon as the previous call's D2H of chunk i landed, and the
 // two PCIe directions run concurrently.  Ordering: H2D chunk i waits for the
-// previous call's D2H of chunk i (or of everything if the host ranges overlap
-// otherwise) and for the compute stream's earlier work; the steps wait for
+// previous call's D2H of chunk i (or of everything when the call is not
+// chained: that D2H still reads U^n) and for the compute stream's earlier work; the steps wait for
 // the whole H2D (dt needs every sub-grid); the D2H waits for the steps.
 int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* host_out, uint64_t nsteps,
                              ts_done_fn done, void* user) {
@@ -1593,18 +1608,19 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     const size_t per = (size_t)c->nf * kNC * sizeof(double);
     const size_t bytes = (size_t)c->n_owned * per;
     auto chunk = [&](int i, size_t* off, size_t* len) {
-        const int64_t g0 = c->n_owned * i / C, g1 = c->n_owned * (i + 1) / C;
+        // sub-grid g belongs to chunk floor(g C / n), the stage kernel's rule
+        const int64_t g0 = (c->n_owned * i + C - 1) / C, g1 = (c->n_owned * (i + 1) + C - 1) / C;
         *off = (size_t)g0 * per;
         *len = (size_t)(g1 - g0) * per;
     };
     const char* in_b = reinterpret_cast<const char*>(host_in);
-    const char* prev_b = static_cast<const char*>(c->prev_out);
     const bool chained = c->prev_out == host_in && c->prev_out_bytes == bytes;
-    const bool overlap = prev_b != nullptr && in_b < prev_b + c->prev_out_bytes && prev_b < in_b + bytes;
     // H2D: U^n may still be read by earlier work on the compute stream
     TS_CUDA(c, cudaEventRecord(c->ev_in, s));
     TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_in, 0));
-    if (overlap && !chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[C - 1], 0));
+    // the previous call's D2H reads U^n: chunk-wise behind it when chained,
+    // else behind all of it (an unrecorded event is a no-op wait)
+    if (!chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[C - 1], 0));
     unsigned long long* stamp = nullptr;
     rc = begin_launch(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, 0, &stamp);
     if (rc) return rc;
@@ -1622,15 +1638,28 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     TS_CUDA(c, cudaEventRecord(c->ev_h2d, sh));
     // the steps
     TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
+    // the last step's stage 3 counts finished sub-grids per chunk, and each
+    // D2H chunk waits (stream memory op) for its count instead of the stage
+    const bool fine = nsteps > 0 && memops().wait32 != nullptr && c->chunk_overlap;
+    if (fine && c->d_chunk_ctr == nullptr) {
+        rc = dalloc(c, &c->d_chunk_ctr, (size_t)ts_hydro_ctx::kXferChunksMax);
+        if (rc) return rc;
+        // zeroed before any D2H stream can test it
+        TS_CUDA(c, cudaMemsetAsync(c->d_chunk_ctr, 0, ts_hydro_ctx::kXferChunksMax * sizeof(uint32_t), s));
+        TS_CUDA(c, cudaStreamSynchronize(s));
+        std::fill(std::begin(c->chunk_expect), std::end(c->chunk_expect), 0u);
+    }
     rc = do_compute_dt(c);
     if (rc) return rc;
     for (uint64_t k = 0; k < nsteps; ++k) {
+        c->chunk_arm = fine && k + 1 == nsteps;
         rc = do_step(c);
+        c->chunk_arm = false;
         if (rc) return rc;
     }
     TS_CUDA(c, cudaEventRecord(c->ev_comp, s));
     // D2H
-    TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));
+    if (!fine) TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));
     rc = begin_launch(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, 0, &stamp);
     if (rc) return rc;
     c->pending.back().bytes = bytes;
@@ -1639,6 +1668,12 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     for (int i = 0; i < C; ++i) {
         size_t off, len;
         chunk(i, &off, &len);
+        if (fine) {
+            c->chunk_expect[i] += (uint32_t)(len / per);
+            if (memops().wait32(sd, (CUdeviceptr)(c->d_chunk_ctr + i), c->chunk_expect[i], CU_STREAM_WAIT_VALUE_GEQ) !=
+                CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWaitValue32 on a chunk counter failed");
+        }
         if (len > 0)
             TS_CUDA(c, cudaMemcpyAsync(out_b + off, reinterpret_cast<const char*>(c->U[0]) + off, len,
                                        cudaMemcpyDeviceToHost, sd));

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--sizes", type=int, nargs="+", default=sorted(SHAPES))
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--recon", default="ppm")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -49,10 +50,14 @@ def main():
             dev = H.CudaDevice(H.HydroConfig(device_id=local, n_species=species, dx=1.0 / (8 * nx),
                                              recon=a.recon))
             dev.set_mesh(mesh, rank)
-            if world > 1:
+            if world > 1 and a.transport == "nccl":
                 uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
                 dist.broadcast_object_list(uid, src=0)
                 dev.comm_init(uid[0], world, rank)
+            elif world > 1:  # the default fused P2P halo push (bench.py's transport)
+                blobs = [None] * world
+                dist.all_gather_object(blobs, dev.p2p_export())
+                dev.p2p_import(blobs)
             dev.init_random(2210)
             dev.step(3)
             dev.synchronize()
@@ -72,6 +77,7 @@ def main():
             value = cells * a.steps / (ms * 1e-3)
             per_gpu = value / world
             line = {"nf": nf, "subgrids_per_gpu": n, "gpus": world, "recon": a.recon,
+                    "transport": a.transport if world > 1 else None,
                     "cell_updates_per_s": value, "ms_per_step": ms / a.steps,
                     "hbm_frac": per_gpu * 64 * nf / (hbm * 1e9),
                     "stage_kernel_share": stage_ns * 1e-6 / ms, "halo_kernels_ms_per_step": halo_ns * 1e-6 / a.steps}
