@@ -76,7 +76,7 @@ struct StageArgs {
     int pdl_trigger;
     // Stage 3 of a pipelined host step (ts_hydro_step_host_async): each CTA
     // counts its sub-grid into chunk_ctr[g * chunk_n / chunk_owned] after a
-    // system-scope fence, so the D2H of a chunk can start (stream wait on the
+    // gpu-scope fence, so the D2H of a chunk can start (stream wait on the
     // counter) while the rest of the stage still runs.
     unsigned int* chunk_ctr;             // nullptr: no counting
     int chunk_n, chunk_owned;

@@ -799,7 +799,8 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     if (STAGE == 3 && A.chunk_ctr != nullptr) {
         __syncthreads();
         if (t == 0) {
-            __threadfence_system();  // U^(n+1) of this sub-grid visible to the copy engine
+            __threadfence();  // U^(n+1) of this sub-grid performed at gpu scope before the count (the
+                              // copy engine is a device agent; a system fence per CTA cost +170 us per stage)
             atomicAdd(A.chunk_ctr + (int)(((long long)g * A.chunk_n) / A.chunk_owned), 1u);
         }
     }
