@@ -382,6 +382,44 @@ __global__ void wait_flags_kernel(const unsigned int* flags, unsigned long long 
     }
 }
 
+// Multi-rank dt all-reduce as one tiny stream-ordered kernel between a step's
+// stage 3 and the next stage 1 (alternative to the stage-3 tail, StageArgs):
+// push this rank's max into slot `rank` of every rank's gather half, raise the
+// peers' dt flags, acquire theirs, write the global max.
+__global__ void dt_exchange_kernel(const double* local_amax, double* const* push_gather,
+                                   unsigned int* const* push_flag, int world, int rank, unsigned int seq,
+                                   const unsigned int* dt_wait, const double* gather_own, double* amax_global,
+                                   unsigned long long* err, unsigned long long wait_ns) {
+    const double am = *local_amax;
+    for (int q = 0; q < world; ++q) push_gather[q][rank] = am;
+    __threadfence_system();
+    for (int q = 0; q < world; ++q)
+        if (push_flag[q] != nullptr) atomicExch_system(push_flag[q], seq);
+    volatile unsigned long long* e = err;
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        const unsigned long long t0 = globaltimer();
+        while ((int)(ld_acquire_sys(dt_wait + q) - seq) < 0) {
+            if (globaltimer() - t0 > wait_ns) {
+                *e = 1ull;
+                return;
+            }
+        }
+    }
+    double g = gather_own[0];
+    for (int q = 1; q < world; ++q) g = fmax(g, gather_own[q]);
+    *amax_global = g;
+}
+
+cudaError_t launch_dt_exchange(const double* local_amax, double* const* push_gather, unsigned int* const* push_flag,
+                               int world, int rank, unsigned int seq, const unsigned int* dt_wait,
+                               const double* gather_own, double* amax_global, unsigned long long* err,
+                               unsigned long long wait_ns, cudaStream_t s) {
+    dt_exchange_kernel<<<1, 1, 0, s>>>(local_amax, push_gather, push_flag, world, rank, seq, dt_wait, gather_own,
+                                       amax_global, err, wait_ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
                               unsigned long long* err, unsigned long long wait_ns, cudaStream_t s) {
     if (mask == 0ull) return cudaSuccess;

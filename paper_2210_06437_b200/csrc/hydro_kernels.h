@@ -106,6 +106,10 @@ cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long 
 cudaError_t launch_clock(unsigned long long* out, cudaStream_t s);
 cudaError_t launch_timed(unsigned long long duration_ns, unsigned long long* stamp, cudaStream_t s);
 cudaError_t launch_stamp(unsigned long long* stamp, int which, cudaStream_t s);
+cudaError_t launch_dt_exchange(const double* local_amax, double* const* push_gather, unsigned int* const* push_flag,
+                               int world, int rank, unsigned int seq, const unsigned int* dt_wait,
+                               const double* gather_own, double* amax_global, unsigned long long* err,
+                               unsigned long long wait_ns, cudaStream_t s);
 cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
                               unsigned long long* err, unsigned long long wait_ns, cudaStream_t s);
 cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,

@@ -262,6 +262,11 @@ struct ts_hydro_ctx {
     uint32_t xseq = 0, aseq = 0;      // exchange / dt-gather sequence numbers (same on every rank)
     bool halo_fused = true;           // P2P: halo slabs pushed by the stage kernel (else copy engines)
     bool flow = true;                 // single rank: stages 2, 3 as PDL dependents gated by per-sub-grid flags
+    // P2P dt all-reduce: a one-thread kernel between stage 3 and the next
+    // stage 1 (default) or the stage-3 tail (TS_HYDRO_DT=tail: every CTA
+    // counts out after a fence, the last one pushes).  Same-box A/B, Sedov
+    // 4096/GPU: kernel +0.7 % at 2 B200s, +0.2 % at 4.
+    bool dt_kernel = true;
     uint32_t flow_seq = 0;
     bool halo_pushed = false;         // proxies of U^n were pushed by the last stage 3 (flags of xseq)
     uint64_t halo_recv_mask = 0;      // ranks that push slabs to this one
@@ -813,12 +818,12 @@ int do_step(ts_hydro_ctx* c) {
             a.chunk_n = c->xfer_chunks;
             a.chunk_owned = (int)c->n_owned;
         }
-        if (p2p && stage == 3) {
+        if (p2p && stage == 3 && !c->dt_kernel) {
             a.done_ctr = c->d_ctr;
             a.total_ctas = (int)c->n_owned;
             a.rank = c->rank;
         }
-        if (p2p && stage == 3) {
+        if (p2p && stage == 3 && !c->dt_kernel) {
             // dt all-reduce fused into the stage-3 tail (see StageArgs)
             a.push_n = c->world;
             a.push_gather = c->d_push_gather + (size_t)(push_seq & 1) * c->world;
@@ -906,7 +911,16 @@ int do_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_bnd, 0));
     }
     if (p2p) {
-        // the stage-3 tail gathered every rank's max: the next dt is local
+        if (c->dt_kernel) {
+            TS_CUDA(c, tsh::launch_dt_exchange(c->d_scal + ((c->steps_done & 1) ^ 1),
+                                               c->d_push_gather + (size_t)(push_seq & 1) * c->world, c->d_push_flag,
+                                               c->world, c->rank, push_seq,
+                                               reinterpret_cast<const unsigned int*>(c->d_flags + c->world),
+                                               c->d_gather + (size_t)(push_seq & 1) * c->world, c->d_scal + 4,
+                                               c->h_clock + 1, c->wait_ns, s));
+            c->launches++;
+        }
+        // the stage-3 tail (or the dt kernel) gathered every rank's max: the next dt is local
         c->aseq = push_seq;
         c->amax_src = c->d_scal + 4;
         c->amax_n = 1;
@@ -1016,6 +1030,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->dev = cfg->device_id;
     if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
         c->xfer_chunks = std::max(1, std::min(ts_hydro_ctx::kXferChunksMax, std::atoi(w)));
