@@ -6,6 +6,7 @@
 // compared bitwise in tests/); POLYTROPE and BINARY are product-only inputs
 // (parity tests feed the same array to both sides).
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <thread>
@@ -179,9 +180,14 @@ extern "C" int ts_hydro_ic_fill(const ts_hydro_config* cfg, int32_t problem, int
                                 const double r2 = std::sqrt((px - x2) * (px - x2) + (py - cy) * (py - cy) + (pz - cz) * (pz - cz));
                                 const double t1 = le15(le15.xi1 * r1 / R1), t2 = le15(le15.xi1 * r2 / R2);
                                 const double d1 = rc1 * std::pow(t1, 1.5), d2 = rc2 * std::pow(t2, 1.5);
-                                w.rho = std::max(d1 + d2, 1e-10);
+                                // pressure-matched atmosphere of 1e-5 rho_c: with the 1e-10 floor of
+                                // the single star, the vacuum gap between the stars emptied cells
+                                // faster than the cell-centred CFL step allows (negative densities,
+                                // NaN from step 1; tools/physics_check.py)
+                                constexpr double amb = 1e-5;
+                                w.rho = std::max(d1 + d2, amb);
                                 w.p = std::pow(w.rho, 5.0 / 3.0);
-                                if (d1 + d2 > 0.0) {
+                                if (d1 + d2 > amb) {
                                     w.vx = -0.1 * (py - cy);
                                     w.vy = 0.1 * (px - cxm);
                                 }
