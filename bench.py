@@ -253,6 +253,22 @@ def main(argv=None):
     total_cells = mesh.n * 512
     value = total_cells * a.steps / (ms * 1e-3)
 
+    # physical validity of the state the timed steps produced (outside the
+    # timed region): every value finite, densities and pressures positive
+    Us = dev.download()
+    rho = Us[:, 0]
+    pres = (cfg.gamma - 1.0) * (Us[:, 4] - 0.5 * (Us[:, 1] ** 2 + Us[:, 2] ** 2 + Us[:, 3] ** 2) / rho)
+    chk = [float(np.isfinite(Us).all()), float(rho.min()), float(pres.min())]
+    del Us, rho, pres
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(chk, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        chk = [float(x) for x in t.tolist()]
+    state_check = {"finite": bool(chk[0] == 1.0), "min_rho": chk[1], "min_p_before_floor": chk[2],
+                   "steps_taken": int(dev.steps_done())}
+
     # roofline of the dominant (stage) kernel: algorithmic bytes / kernel time
     peaks, peak_kind = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
@@ -351,6 +367,7 @@ def main(argv=None):
                          "fp64": fp64},
             "clocks": clk.summary(),
             "gpu_launches": launches,
+            "state_check": state_check,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
