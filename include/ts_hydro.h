@@ -282,6 +282,12 @@ int ts_hydro_device_free(ts_hydro_ctx* ctx, uint64_t handle);
 /* Device address behind a handle (for callers that fill the buffer). */
 int ts_hydro_device_ptr(const ts_hydro_ctx* ctx, uint64_t handle, void** ptr);
 
+/* Diagnostic: with TS_HYDRO_CTA_LOG set when the mesh is bound, every stage
+ * launch of ts_hydro_step logs per CTA {SM id, start, work start after the
+ * halo / dataflow waits, end} (globaltimer ns); this returns the last step's
+ * [3 stages][n_owned CTAs][4] (n = 0 when logging is off; out == NULL: count). */
+int ts_hydro_debug_cta_log(ts_hydro_ctx* ctx, uint64_t* out, uint64_t cap, uint64_t* n);
+
 /* ---- timing hook -------------------------------------------------------------- */
 int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void* user);
 /* SimDevice::flush_activity: waits for in-flight work, returns completed

@@ -21,6 +21,9 @@ struct StageArgs {
     double* amax_reset;         // stage 1: zeroed (the slot stage 3 accumulates into)
     double* dt_out;             // stage 1: dt of this step
     unsigned long long* stamp;  // [start, end] globaltimer ns of this launch (nullable)
+    // Diagnostic (TS_HYDRO_CTA_LOG): per CTA {SM id, start, work start (after
+    // the halo / dataflow waits), end} in globaltimer ns, indexed by blockIdx.
+    unsigned long long* cta_log;
     // Stage 3, multi-rank P2P transport: every CTA counts out in done_ctr
     // (across all launches of the stage, total_ctas); the last one pushes the
     // rank's final amax into slot `rank` of every rank's gather array

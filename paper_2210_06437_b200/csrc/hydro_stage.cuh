@@ -694,15 +694,19 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     extern __shared__ double smem[];
     if (A.stamp != nullptr && threadIdx.x == 0)
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
+    if (A.cta_log != nullptr && threadIdx.x == 0) {
+        unsigned int sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        A.cta_log[4 * blockIdx.x] = sm;
+        A.cta_log[4 * blockIdx.x + 1] = globaltimer();
+    }
     const int g = A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x;
     const int t = threadIdx.x;
     if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0) {
         // proxies of U^(k-1): pushed by the peers' previous-stage boundary CTAs
         // (released in their first wave, so this rarely spins)
-        if (t == 0)
-            for (int q = 0; q < 64; ++q)
-                if ((A.halo_wait_mask >> q) & 1ull)
-                    wait_flag(A, A.halo_wait + q, A.halo_wait_seq);
+        // one source rank per thread, in parallel
+        if (t < 64 && ((A.halo_wait_mask >> t) & 1ull)) wait_flag(A, A.halo_wait + t, A.halo_wait_seq);
         __syncthreads();
     }
     if (A.pdl_trigger) {
@@ -717,18 +721,20 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     if (A.flow_wait != nullptr) {
-        // U^(k-1) of this sub-grid and of its face neighbours: the previous stage's output
-        if (t == 0) {
-            flow_wait_one(A, A.flow_wait + g, A.flow_seq);
-            for (int d = 0; d < 6; ++d) {
-                const int h = __ldg(A.nbr + 6 * g + d);
-                if (h >= 0 && h < A.flow_n) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
-            }
+        // U^(k-1) of this sub-grid and of its face neighbours: the previous
+        // stage's output.  The seven flags are acquired in parallel, one per
+        // thread (one after the other they cost every CTA ~2-4 us of L2 round
+        // trips, measured with TS_HYDRO_CTA_LOG); the barrier extends each
+        // acquire to the whole CTA.
+        if (t < 7) {
+            const int h = t == 0 ? g : __ldg(A.nbr + 6 * g + (t - 1));
+            if (h >= 0 && h < A.flow_n) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
         }
         __syncthreads();
     }
     // TS_LAZY_DT: dt enters only the z sweep's update, so its two IEEE
     // divisions can be done there, off the CTA's start-up path
+    if (A.cta_log != nullptr && t == 0) A.cta_log[4 * blockIdx.x + 2] = globaltimer();
     double amax_in = A.amax_in[0];
     for (int i = 1; i < A.amax_n; ++i) amax_in = fmax(amax_in, A.amax_in[i]);
 #if !TS_LAZY_DT
@@ -843,6 +849,10 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     if (A.stamp != nullptr) {
         __syncthreads();
         if (t == 0) atomicMax(A.stamp + 1, globaltimer());
+    }
+    if (A.cta_log != nullptr) {
+        __syncthreads();
+        if (t == 0) A.cta_log[4 * blockIdx.x + 3] = globaltimer();
     }
 }
 

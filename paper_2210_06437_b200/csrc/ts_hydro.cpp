@@ -223,6 +223,7 @@ struct ts_hydro_ctx {
     int32_t* d_boundary = nullptr;
     int32_t* d_order = nullptr;       // launch order of the fused P2P stage: boundary spread through the front
     uint32_t* d_flow = nullptr;       // [2][n_owned] single-rank dataflow: last step seq that finished stage 1 / 2
+    unsigned long long* d_cta_log = nullptr;  // [3][n_owned][4] diagnostic per-CTA timeline of the last step
     int32_t* d_cta_bnd = nullptr;     // [n_owned] launch position -> boundary slot (-1: interior)
     int2* d_push_tbl = nullptr;       // [n_boundary][6] fused halo push targets
     long long* d_gid = nullptr;
@@ -409,6 +410,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_boundary);
     dfree(c, &c->d_order);
     dfree(c, &c->d_flow);
+    dfree(c, &c->d_cta_log);
     dfree(c, &c->d_chunk_ctr);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
@@ -809,6 +811,7 @@ int do_step(ts_hydro_ctx* c) {
     if (flow) ++c->flow_seq;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
+        if (c->d_cta_log != nullptr) a.cta_log = c->d_cta_log + 4 * (size_t)(stage - 1) * (size_t)c->n_owned;
         if (stage == 1) {
             a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
@@ -1269,6 +1272,7 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
     if (!rc) rc = dalloc(c, &c->d_order, (size_t)c->n_owned);
     if (!rc) rc = dalloc(c, &c->d_flow, 2 * (size_t)c->n_owned);
+    if (!rc && std::getenv("TS_HYDRO_CTA_LOG") != nullptr) rc = dalloc(c, &c->d_cta_log, 12 * (size_t)c->n_owned);
     if (!rc) {
         c->flow_seq = 0;
         TS_CUDA(c, cudaMemset(c->d_flow, 0, 2 * (size_t)c->n_owned * sizeof(uint32_t)));
@@ -2280,6 +2284,19 @@ int ts_hydro_device_ptr(const ts_hydro_ctx* c, uint64_t handle, void** ptr) {
     auto it = c->handles.find(handle);
     if (it == c->handles.end()) return TS_EINVAL;
     *ptr = it->second.first;
+    return TS_OK;
+}
+
+int ts_hydro_debug_cta_log(ts_hydro_ctx* c, uint64_t* out, uint64_t cap, uint64_t* n) {
+    if (c == nullptr || n == nullptr) return TS_EINVAL;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    *n = c->d_cta_log != nullptr ? 12 * (uint64_t)c->n_owned : 0;
+    if (out == nullptr || *n == 0) return TS_OK;
+    if (cap < *n) return fail(c, TS_EINVAL, "buffer too small");
+    cudaSetDevice(c->dev);
+    int rc = sync_all(c);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpy(out, c->d_cta_log, *n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return TS_OK;
 }
 

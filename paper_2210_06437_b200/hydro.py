@@ -171,6 +171,7 @@ _SIGNATURES = {
     "ts_hydro_device_alloc": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p]),
     "ts_hydro_device_free": (ctypes.c_int, [_vp, ctypes.c_uint64]),
     "ts_hydro_device_ptr": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.POINTER(_vp)]),
+    "ts_hydro_debug_cta_log": (ctypes.c_int, [_vp, _u64p, ctypes.c_uint64, _u64p]),
 }
 
 
@@ -690,6 +691,14 @@ class CudaDevice:
 
     def device_free(self, handle: int) -> None:
         self._check(lib().ts_hydro_device_free(self._h, handle), "device_free")
+
+    def debug_cta_log(self) -> np.ndarray:
+        """[3][n_owned][4] per-CTA {SM, start, work start, end} of the last step (TS_HYDRO_CTA_LOG)."""
+        n = ctypes.c_uint64()
+        self._check(lib().ts_hydro_debug_cta_log(self._h, None, 0, ctypes.byref(n)), "debug_cta_log")
+        out = np.zeros(max(n.value, 1), np.uint64)
+        self._check(lib().ts_hydro_debug_cta_log(self._h, _p(out, _u64p), out.size, ctypes.byref(n)), "debug_cta_log")
+        return out[:n.value].reshape(3, -1, 4) if n.value else out[:0].reshape(3, 0, 4)
 
     def device_ptr(self, handle: int) -> int:
         p = _vp()
