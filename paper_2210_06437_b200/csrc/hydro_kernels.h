@@ -74,7 +74,20 @@ struct StageArgs {
     // zeroes amax_reset, which stage 3 accumulates into).
     const unsigned int* flow_wait;       // nullptr: no wait (stream order)
     unsigned int* flow_done;             // nullptr: no publish
-    unsigned int flow_seq;
+    unsigned int flow_seq;               // published value
+    unsigned int flow_wait_seq;          // awaited value (the previous step's for stage 1)
+    // Single rank, across the step boundary: stage 1 is also a PDL dependent
+    // (of the previous step's stage 3).  Its x and y sweeps only need U^n of
+    // the sub-grid and its neighbours (flow flags of stage 3); dt needs every
+    // sub-grid's stage-3 max, so before its z sweep a CTA acquires the count of
+    // finished stage-3 CTAs (cnt_wait >= cnt_expect; stage 3 counts into
+    // cnt_done after its max atomics) and only then reads amax_in.  The max
+    // slots form a ring of three: block 0 of stage 1 zeroes the slot two steps
+    // ahead (amax_reset2) once the count is complete.
+    const unsigned int* cnt_wait;
+    unsigned int cnt_expect;
+    unsigned int* cnt_done;
+    double* amax_reset2;
     int flow_n;                          // owned sub-grids (flag count); proxies are gated by the halo flags
     int pdl_trigger;
     // Stage 3 of a pipelined host step (ts_hydro_step_host_async): each CTA

@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         // acquire to the whole CTA.
         if (t < 7) {
             const int h = t == 0 ? g : __ldg(A.nbr + 6 * g + (t - 1));
-            if (h >= 0 && h < A.flow_n) flow_wait_one(A, A.flow_wait + h, A.flow_seq);
+            if (h >= 0 && h < A.flow_n) flow_wait_one(A, A.flow_wait + h, A.flow_wait_seq);
         }
         __syncthreads();
     }
@@ -738,10 +738,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     double amax_in = A.amax_in[0];
     for (int i = 1; i < A.amax_n; ++i) amax_in = fmax(amax_in, A.amax_in[i]);
 #if !TS_LAZY_DT
+    if (A.cnt_wait != nullptr) {
+        if (t == 0) flow_wait_one(A, A.cnt_wait, A.cnt_expect);
+        __syncthreads();
+        amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
+    }
     const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / A.dx);
-#endif
     if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
         if (A.dt_out != nullptr) *A.dt_out = (A.cfl * A.dx) / amax_in;
+        if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
+    }
+#endif
+    if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
         if (A.amax_reset != nullptr && !A.pdl_trigger) *A.amax_reset = 0.0;
     }
     StageCtx c;
@@ -771,8 +779,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         const int fm[kFA] = {0, 1 + axis, axis == 0 ? 2 : 1, axis == 2 ? 2 : 3, 4, 5};
         if (axis == 2) {
 #if TS_LAZY_DT
+            if (A.cnt_wait != nullptr) {
+                // every sub-grid's stage-3 max of the previous step is in place
+                if (t == 0) flow_wait_one(A, A.cnt_wait, A.cnt_expect);
+                __syncthreads();
+                amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
+            }
             const double dt = (A.cfl * A.dx) / amax_in;
             c.dtdx = 0.5 * (dt / A.dx);  // the sweeps carry twice the KT flux (kt2)
+            if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
+                if (A.dt_out != nullptr) *A.dt_out = dt;
+                if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
+            }
 #else
             c.dtdx = dtdx_early;
 #endif
@@ -810,12 +828,14 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             atomicAdd(A.chunk_ctr + (int)(((long long)g * A.chunk_n) / A.chunk_owned), 1u);
         }
     }
-    if (A.flow_done != nullptr) {
-        // U^(k) of this sub-grid complete: CTA barrier, one gpu-scope fence, flag
+    if (A.flow_done != nullptr || A.cnt_done != nullptr) {
+        // U^(k) of this sub-grid (and, stage 3, its max) complete: CTA barrier,
+        // one gpu-scope fence, flag / count
         __syncthreads();
         if (t == 0) {
             __threadfence();
-            atomicExch(A.flow_done + g, A.flow_seq);
+            if (A.flow_done != nullptr) atomicExch(A.flow_done + g, A.flow_seq);
+            if (STAGE == 3 && A.cnt_done != nullptr) atomicAdd(A.cnt_done, 1u);
         }
     }
     if (A.done_ctr != nullptr) {

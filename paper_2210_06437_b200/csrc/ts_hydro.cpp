@@ -222,7 +222,7 @@ struct ts_hydro_ctx {
     int32_t* d_interior = nullptr;
     int32_t* d_boundary = nullptr;
     int32_t* d_order = nullptr;       // launch order of the fused P2P stage: boundary spread through the front
-    uint32_t* d_flow = nullptr;       // [2][n_owned] single-rank dataflow: last step seq that finished stage 1 / 2
+    uint32_t* d_flow = nullptr;       // [3][n_owned] dataflow: last step seq that finished stage 1 / 2 / 3
     unsigned long long* d_cta_log = nullptr;  // [3][n_owned][4] diagnostic per-CTA timeline of the last step
     int32_t* d_cta_bnd = nullptr;     // [n_owned] launch position -> boundary slot (-1: interior)
     int2* d_push_tbl = nullptr;       // [n_boundary][6] fused halo push targets
@@ -263,6 +263,10 @@ struct ts_hydro_ctx {
     uint32_t xseq = 0, aseq = 0;      // exchange / dt-gather sequence numbers (same on every rank)
     bool halo_fused = true;           // P2P: halo slabs pushed by the stage kernel (else copy engines)
     bool flow = true;                 // single rank: stages 2, 3 as PDL dependents gated by per-sub-grid flags
+    bool flow_chain = false;          // the last stream op was this call's stage 3: the next stage 1 may be a PDL dependent
+    bool flow_steps = true;           // TS_HYDRO_FLOW_STEPS=0: stage 1 stays stream-ordered
+    uint32_t* d_cnt3 = nullptr;       // finished stage-3 CTAs (monotonic)
+    uint32_t cnt3_expect = 0;
     // P2P dt all-reduce: a one-thread kernel between stage 3 and the next
     // stage 1 (default) or the stage-3 tail (TS_HYDRO_DT=tail: every CTA
     // counts out after a fence, the last one pushes).  Same-box A/B, Sedov
@@ -319,6 +323,9 @@ int cuda_fail(ts_hydro_ctx* c, cudaError_t e, const char* what) {
 int guard(ts_hydro_ctx* c) {
     if (c == nullptr) return TS_EINVAL;
     if (c->shut) return fail(c, TS_ESHUTDOWN, "device is shut down");
+    // every entry point may enqueue other work: only the steps of one call
+    // chain stage 3 -> next stage 1 as programmatic dependents
+    c->flow_chain = false;
     return TS_OK;
 }
 
@@ -410,6 +417,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_boundary);
     dfree(c, &c->d_order);
     dfree(c, &c->d_flow);
+    dfree(c, &c->d_cnt3);
     dfree(c, &c->d_cta_log);
     dfree(c, &c->d_chunk_ctr);
     dfree(c, &c->d_cta_bnd);
@@ -609,6 +617,15 @@ int build_plans(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner) {
     return TS_OK;
 }
 
+// Max-signal-speed slot of step s: with one rank a ring of three (stage 1 of
+// one step may run while the previous step's stage 3 still accumulates; see
+// StageArgs::cnt_wait), with N ranks the two-slot parity the exchanges use.
+double* amax_slot(const ts_hydro_ctx* c, uint64_t s) {
+    if (c->world > 1) return c->d_scal + (s & 1);
+    static constexpr int kRing[3] = {0, 1, 5};
+    return c->d_scal + kRing[s % 3];
+}
+
 int64_t local_of(const ts_hydro_ctx* c, int64_t gid) {
     auto it = std::lower_bound(c->owned_gid.begin(), c->owned_gid.end(), gid);
     if (it != c->owned_gid.end() && *it == gid) return it - c->owned_gid.begin();
@@ -631,10 +648,9 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     a.nbr = c->d_nbr;
     a.list = nullptr;
     a.first = 0;
-    const int par = (int)(c->steps_done & 1);
-    a.amax_in = c->amax_src != nullptr ? c->amax_src : c->d_scal + par;
+    a.amax_in = c->amax_src != nullptr ? c->amax_src : amax_slot(c, c->steps_done);
     a.amax_n = c->amax_src != nullptr ? c->amax_n : 1;
-    a.amax_out = c->d_scal + (par ^ 1);
+    a.amax_out = amax_slot(c, c->steps_done + 1);
     a.amax_reset = nullptr;
     a.dt_out = nullptr;
     a.gamma = c->cfg.gamma;
@@ -772,7 +788,7 @@ int do_compute_dt(ts_hydro_ctx* c) {
     cudaStream_t s;
     int rc = ensure_stream(c, 0, &s);
     if (rc) return rc;
-    double* slot = c->d_scal + (c->steps_done & 1);
+    double* slot = amax_slot(c, c->steps_done);
     TS_CUDA(c, cudaMemsetAsync(slot, 0, sizeof(double), s));
     unsigned long long* stamp = nullptr;
     rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameSignal, 0, 0, &stamp);
@@ -812,8 +828,10 @@ int do_step(ts_hydro_ctx* c) {
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
         if (c->d_cta_log != nullptr) a.cta_log = c->d_cta_log + 4 * (size_t)(stage - 1) * (size_t)c->n_owned;
+        const bool chain = flow && !multi && c->flow_steps && c->flow_chain;
         if (stage == 1) {
-            a.amax_reset = c->d_scal + ((c->steps_done & 1) ^ 1);
+            a.amax_reset = chain ? nullptr : amax_slot(c, c->steps_done + 1);
+            if (!multi) a.amax_reset2 = amax_slot(c, c->steps_done + 2);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
         }
         if (stage == 3 && c->chunk_arm) {
@@ -838,14 +856,26 @@ int do_step(ts_hydro_ctx* c) {
         }
         if (flow) {
             const size_t n = (size_t)c->n_owned;
+            const bool steps = !multi && c->flow_steps;  // stage 3 feeds the next stage 1 too
             a.flow_seq = c->flow_seq;
+            a.flow_wait_seq = c->flow_seq;
             a.flow_n = (int)c->n_owned;
-            a.pdl_trigger = stage < 3;
+            a.pdl_trigger = stage < 3 || steps;
             a.flow_wait = stage > 1 ? c->d_flow + (size_t)(stage - 2) * n : nullptr;
-            a.flow_done = stage < 3 ? c->d_flow + (size_t)(stage - 1) * n : nullptr;
+            a.flow_done = stage < 3 || steps ? c->d_flow + (size_t)(stage - 1) * n : nullptr;
+            if (stage == 1 && chain) {
+                a.flow_wait = c->d_flow + 2 * n;
+                a.flow_wait_seq = c->flow_seq - 1;
+                a.cnt_wait = c->d_cnt3;
+                a.cnt_expect = c->cnt3_expect;
+            }
+            if (stage == 3 && steps) {
+                a.cnt_done = c->d_cnt3;
+                c->cnt3_expect += (uint32_t)c->n_owned;
+            }
         }
         if (!multi) {
-            rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0, flow && stage > 1);
+            rc = launch_stage_list(c, a, stage, nullptr, c->n_owned, 0, 0, 0, flow && (stage > 1 || chain));
             if (rc) return rc;
             continue;
         }
@@ -938,6 +968,7 @@ int do_step(ts_hydro_ctx* c) {
     } else {
         c->amax_src = nullptr;
     }
+    c->flow_chain = flow && !multi;
     c->steps_done++;
     return TS_OK;
 }
@@ -1033,6 +1064,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     c->dev = cfg->device_id;
     if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_FLOW_STEPS")) c->flow_steps = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
@@ -1271,11 +1303,15 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     if (!rc) rc = dalloc(c, &c->d_interior, c->interior.size());
     if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
     if (!rc) rc = dalloc(c, &c->d_order, (size_t)c->n_owned);
-    if (!rc) rc = dalloc(c, &c->d_flow, 2 * (size_t)c->n_owned);
+    if (!rc) rc = dalloc(c, &c->d_flow, 3 * (size_t)c->n_owned);
+    if (!rc) rc = dalloc(c, &c->d_cnt3, 1);
     if (!rc && std::getenv("TS_HYDRO_CTA_LOG") != nullptr) rc = dalloc(c, &c->d_cta_log, 12 * (size_t)c->n_owned);
     if (!rc) {
         c->flow_seq = 0;
-        TS_CUDA(c, cudaMemset(c->d_flow, 0, 2 * (size_t)c->n_owned * sizeof(uint32_t)));
+        c->cnt3_expect = 0;
+        c->flow_chain = false;
+        TS_CUDA(c, cudaMemset(c->d_flow, 0, 3 * (size_t)c->n_owned * sizeof(uint32_t)));
+        TS_CUDA(c, cudaMemset(c->d_cnt3, 0, sizeof(uint32_t)));
     }
     if (!rc) rc = dalloc(c, &c->d_cta_bnd, (size_t)c->n_owned);
     if (!rc) rc = dalloc(c, &c->d_gid, (size_t)c->n_owned);
