@@ -33,6 +33,9 @@ namespace taskscope {
 class CudaHydroDevice {
 public:
     explicit CudaHydroDevice(const ts_hydro_config& cfg, Profiler* sink = nullptr) : sink_(sink) {
+        // RunClock is zeroed at its first read: fix the epoch before any device
+        // activity so no record predates it (clock.hpp:11-13)
+        (void)RunClock::instance().now_ns();
         check(ts_hydro_create(&cfg, &ctx_), "ts_hydro_create");
     }
     ~CudaHydroDevice() {

@@ -5,6 +5,9 @@
 #include <vector>
 
 #include "ts_hydro_taskscope.hpp"
+#ifdef TS_HAVE_EXPORT
+#include "taskscope/export.hpp"
+#endif
 
 int main(int argc, char** argv) {
     using namespace taskscope;
@@ -41,6 +44,16 @@ int main(int argc, char** argv) {
     const Snapshot s = profiler.snapshot();
     const auto it = s.profile.find("hydro_stage1_kernel");
     const auto grav = s.profile.find("multipole_kernel");
+#ifdef TS_HAVE_EXPORT
+    // the reference's own exporters over the real GPU activity: Google trace
+    // events (device lanes 10000 + device*1000 + stream) and the profile CSV
+    if (argc >= 4) {
+        const RunProfile run{s};
+        const auto events = write_trace_events(run, argv[2]);
+        const auto rows = write_profile_csv(run, argv[3]);
+        std::printf("trace events %llu, csv rows %llu\n", (unsigned long long)events, (unsigned long long)rows);
+    }
+#endif
     std::printf("records %llu, hydro_stage1_kernel calls %llu, multipole_kernel calls %llu\n", (unsigned long long)n,
                 (unsigned long long)(it == s.profile.end() ? 0 : it->second.calls),
                 (unsigned long long)(grav == s.profile.end() ? 0 : grav->second.calls));
