@@ -24,7 +24,8 @@ struct StageArgs {
     // Diagnostic (TS_HYDRO_CTA_LOG): per CTA {SM id, start, work start (after
     // the halo / dataflow waits), end} in globaltimer ns, indexed by blockIdx.
     unsigned long long* cta_log;
-    // Stage 3, multi-rank P2P transport: every CTA counts out in done_ctr
+    // Stage 3, multi-rank P2P transport, TS_HYDRO_DT=tail (the default is the
+    // one-thread dt_exchange_kernel after stage 3): every CTA counts out in done_ctr
     // (across all launches of the stage, total_ctas); the last one pushes the
     // rank's final amax into slot `rank` of every rank's gather array
     // (push_gather, this step's half), raises their dt flags (push_flag[q],
