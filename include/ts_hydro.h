@@ -133,6 +133,36 @@ int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_m
  * foreign neighbours become halo proxies filled by the exchange. */
 int ts_hydro_set_mesh(ts_hydro_ctx* ctx, int64_t n_grids, const int64_t* neighbor_ids,
                       const int32_t* owner, int32_t world_size, int32_t rank);
+/* ---- coarse-fine AMR mesh ----------
+ * The reference's multi-level octree (build_mesh, workload.cpp:264-327) links
+ * only same-level faces (Mesh::validate, workload.cpp:160-161), so a leaf
+ * next to another level has no ghost source there.  This binds a 2:1-balanced
+ * leaf set (single rank) whose cross-level face neighbours are proxy
+ * sub-grids: ids n_leaves .. n_leaves+n_proxy-1, refilled before every RK
+ * stage by prolongation (piecewise constant) from a coarse leaf or
+ * restriction (2x2x2 mean) from 8 fine leaves; after every stage the coarse
+ * cells on a coarse-fine face take the mean of the 4 fine face fluxes
+ * (reflux), so mass, momentum and energy stay conserved to round-off.
+ * Leaves are level-major: level[] non-decreasing, 0..max_level; cfg.dx is
+ * the finest level's dx (it sets the global dt), level L updates with
+ * dx * 2^(max_level - L).  neighbor_ids: [n_leaves][6] ids of leaves or
+ * proxies, -1 = outflow boundary.  Proxy and reflux ids are leaf ids.
+ * Layouts are those of oracle/hydro_oracle.h (orc_amr_proxy /
+ * orc_amr_reflux_rec).  Stepping: ts_hydro_step / ts_hydro_step_host;
+ * multi-rank, the pipelined host path and checkpoints refuse (TS_ESTATE). */
+typedef struct {
+    int32_t dst;       /* proxy id */
+    int32_t kind;      /* 0 = prolong from src[0], 1 = restrict from src[0..7] (octant order) */
+    int32_t octant;    /* kind 0: the proxy's octant of src[0] (bit d = upper half along axis d) */
+    int32_t src[8];
+} ts_amr_proxy;
+typedef struct {
+    int32_t coarse;    /* coarse leaf with at least one coarse-fine face */
+    int32_t fine[6][4];/* per face: the fine leaves behind it by transverse quadrant, -1 = none */
+} ts_amr_reflux;
+int ts_hydro_set_amr_mesh(ts_hydro_ctx* ctx, int64_t n_leaves, const int64_t* neighbor_ids, const int32_t* level,
+                          int32_t max_level, int64_t n_proxy, const ts_amr_proxy* proxies, int64_t n_reflux,
+                          const ts_amr_reflux* reflux);
 int ts_hydro_local_counts(const ts_hydro_ctx* ctx, int64_t* n_owned, int64_t* n_proxy,
                           int64_t* n_interior);
 int ts_hydro_owned_ids(const ts_hydro_ctx* ctx, int64_t* global_ids);

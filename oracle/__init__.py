@@ -42,7 +42,10 @@ class Params(ctypes.Structure):
 
 
 def build(force: bool = False) -> None:
-    if force or not os.path.exists(LIB_PATH):
+    src = os.path.join(HERE, "hydro_oracle.c")
+    stale = os.path.exists(LIB_PATH) and os.path.exists(src) and max(
+        os.path.getmtime(src), os.path.getmtime(os.path.join(HERE, "hydro_oracle.h"))) > os.path.getmtime(LIB_PATH)
+    if force or stale or not os.path.exists(LIB_PATH):
         subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
 
 
@@ -86,6 +89,12 @@ def lib():
                                    ctypes.c_int, ctypes.c_int, _f64p]
         L.orc_ic_random.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_uint64, _f64p]
+        L.orc_amr_fill.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _f64p]
+        L.orc_amr_reflux.argtypes = [ctypes.POINTER(Params), _i64p, _i32p, ctypes.c_int, ctypes.c_int64, _i32p,
+                                     _f64p, _f64p, ctypes.c_int, ctypes.c_double]
+        L.orc_run_amr.restype = ctypes.c_int
+        L.orc_run_amr.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i64p, _i32p, _i64p, ctypes.c_int,
+                                  ctypes.c_int64, _i32p, ctypes.c_int64, _i32p, _f64p, ctypes.c_int, _f64p]
         _lib = L
     return _lib
 
@@ -216,3 +225,30 @@ def to_global(U, pos, dims, field=0):
         x, y, z = pos[g]
         out[z * N:(z + 1) * N, y * N:(y + 1) * N, x * N:(x + 1) * N] = U[g, field].reshape(N, N, N)
     return out
+
+
+def amr_fill(nf, mesh, U):
+    """Proxy fill (prolongation / restriction) in place on U [n_total, nf, 512]."""
+    px = np.ascontiguousarray(mesh.proxies, np.int32)
+    lib().orc_amr_fill(nf, len(px), _p(px, _i32p), _p(U, _f64p))
+    return U
+
+
+def run_amr(p: Params, mesh, U, nsteps):
+    """nsteps SSP-RK3 steps on an AMR mesh (paper_2210_06437_b200.amr.AmrMesh);
+    U is [n_total, nf, 512] (proxy slots may hold anything).  Returns (U, dts)."""
+    U = np.array(U, np.float64, copy=True, order="C")
+    assert U.shape[0] == mesh.n_total
+    nbr = np.zeros((mesh.n_total, 6), np.int64) - 1
+    nbr[:mesh.n_leaves] = mesh.nbr
+    lev = np.ascontiguousarray(mesh.level, np.int32)
+    lf = np.ascontiguousarray(mesh.level_first, np.int64)
+    px = np.ascontiguousarray(mesh.proxies, np.int32)
+    rf = np.ascontiguousarray(mesh.reflux, np.int32)
+    dts = np.zeros(max(nsteps, 1), np.float64)
+    rc = lib().orc_run_amr(ctypes.byref(p), mesh.n_total, _p(nbr, _i64p), _p(lev, _i32p), _p(lf, _i64p),
+                           mesh.max_level, len(px), _p(px, _i32p), len(rf), _p(rf, _i32p), _p(U, _f64p), nsteps,
+                           _p(dts, _f64p))
+    if rc != 0:
+        raise MemoryError("oracle AMR run failed")
+    return U, dts[:nsteps]

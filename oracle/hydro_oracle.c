@@ -558,3 +558,126 @@ void orc_ic_random(const orc_params* p, int64_t g_begin, int64_t g_end, uint64_t
             for (int k = 6; k < nf; ++k) u[k * NC] = rho * r[k];
         }
 }
+
+/* ---------------------------------------------------------------------------
+ * Coarse-fine AMR.  The reference's octree
+ * (build_mesh, workload.cpp:264-327) refines by octants and links only
+ * same-level faces (validate, workload.cpp:160-161); Octo-Tiger fills
+ * coarse-fine ghosts by prolongation / restriction and corrects the coarse
+ * fluxes at the interface.  Restated here with one global dt,
+ * 2:1 balanced leaves, piecewise-constant prolongation, volume-mean
+ * restriction and a flux correction with the RK stage weight.
+ * ------------------------------------------------------------------------- */
+
+void orc_amr_fill(int nf, int64_t n_proxy, const orc_amr_proxy* px, double* U) {
+    for (int64_t k = 0; k < n_proxy; ++k) {
+        const orc_amr_proxy* r = &px[k];
+        for (int z = 0; z < N; ++z)
+            for (int y = 0; y < N; ++y)
+                for (int x = 0; x < N; ++x) {
+                    const int c = (int)cidx(x, y, z);
+                    for (int f = 0; f < nf; ++f) {
+                        double v;
+                        if (r->kind == 0) {
+                            const int cx = (r->octant & 1) * 4 + x / 2;
+                            const int cy = ((r->octant >> 1) & 1) * 4 + y / 2;
+                            const int cz = ((r->octant >> 2) & 1) * 4 + z / 2;
+                            v = U[((int64_t)r->src[0] * nf + f) * NC + cidx(cx, cy, cz)];
+                        } else {
+                            const int o = (x >> 2) | ((y >> 2) << 1) | ((z >> 2) << 2);
+                            const double* s = U + ((int64_t)r->src[o] * nf + f) * NC;
+                            const int bx = 2 * (x & 3), by = 2 * (y & 3), bz = 2 * (z & 3);
+                            double sum = s[cidx(bx, by, bz)];
+                            sum = sum + s[cidx(bx + 1, by, bz)];
+                            sum = sum + s[cidx(bx, by + 1, bz)];
+                            sum = sum + s[cidx(bx + 1, by + 1, bz)];
+                            sum = sum + s[cidx(bx, by, bz + 1)];
+                            sum = sum + s[cidx(bx + 1, by, bz + 1)];
+                            sum = sum + s[cidx(bx, by + 1, bz + 1)];
+                            sum = sum + s[cidx(bx + 1, by + 1, bz + 1)];
+                            v = 0.125 * sum;
+                        }
+                        U[((int64_t)r->dst * nf + f) * NC + c] = v;
+                    }
+                }
+    }
+}
+
+/* The KT flux of face j (0..N) of pencil (a, b) along `axis` of sub-grid g:
+ * the value orc_stage computes as F[j] for that pencil. */
+static void face_flux(const orc_params* p, const int64_t* nbr, const double* U, int64_t g, int axis, int a,
+                      int b, int j, double* F) {
+    double q[P], uL[N + 1], uR[N + 1], sL[16], sR[16];
+    for (int f = 0; f < p->nf; ++f) {
+        for (int s = 0; s < P; ++s) q[s] = pencil_value(p->nf, nbr, U, g, f, axis, a, b, s - 3);
+        reconstruct(p->recon, q, uL, uR);
+        sL[f] = uL[j];
+        sR[f] = uR[j];
+    }
+    kt_flux(p, axis, sL, sR, F);
+}
+
+void orc_amr_reflux(const orc_params* p, const int64_t* nbr, const int32_t* level, int max_level,
+                    int64_t n_rec, const orc_amr_reflux_rec* rf, const double* Uprev, double* Uout, int stage,
+                    double dt) {
+    const int nf = p->nf;
+    const double w = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : C23);
+    double Fc[16], F00[16], F10[16], F01[16], F11[16];
+    for (int64_t r = 0; r < n_rec; ++r) {
+        const int64_t g = rf[r].coarse;
+        const double dtdx = dt / ldexp(p->dx, max_level - level[g]);
+        for (int face = 0; face < 6; ++face) {
+            if (rf[r].fine[face][0] < 0) continue;
+            const int axis = face >> 1, side = face & 1;
+            const int jc = side ? N : 0, jf = side ? 0 : N, ic = side ? N - 1 : 0;
+            for (int b = 0; b < N; ++b)
+                for (int a = 0; a < N; ++a) {
+                    const int64_t leaf = rf[r].fine[face][(a >> 2) + 2 * (b >> 2)];
+                    const int fa = 2 * (a & 3), fb = 2 * (b & 3);
+                    face_flux(p, nbr, Uprev, g, axis, a, b, jc, Fc);
+                    face_flux(p, nbr, Uprev, leaf, axis, fa, fb, jf, F00);
+                    face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb, jf, F10);
+                    face_flux(p, nbr, Uprev, leaf, axis, fa, fb + 1, jf, F01);
+                    face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb + 1, jf, F11);
+                    const int64_t c = axis == 0 ? cidx(ic, a, b) : (axis == 1 ? cidx(a, ic, b) : cidx(a, b, ic));
+                    for (int f = 0; f < nf; ++f) {
+                        const double avg = 0.25 * ((F00[f] + F10[f]) + (F01[f] + F11[f]));
+                        const double corr = side ? Fc[f] - avg : avg - Fc[f];
+                        double* u = Uout + (g * nf + f) * NC + c;
+                        *u = *u + w * (dtdx * corr);
+                    }
+                }
+        }
+    }
+}
+
+int orc_run_amr(const orc_params* p, int64_t n_total, const int64_t* nbr, const int32_t* level,
+                const int64_t* level_first, int max_level, int64_t n_proxy, const orc_amr_proxy* px,
+                int64_t n_rec, const orc_amr_reflux_rec* rf, double* U, int nsteps, double* dt_hist) {
+    const size_t bytes = sizeof(double) * (size_t)n_total * (size_t)p->nf * NC;
+    double* U1 = (double*)calloc(1, bytes);
+    double* U2 = (double*)calloc(1, bytes);
+    if (!U1 || !U2) {
+        free(U1);
+        free(U2);
+        return -1;
+    }
+    const int64_t n_leaves = level_first[max_level + 1];
+    for (int s = 0; s < nsteps; ++s) {
+        const double amax = orc_max_signal_speed(p, 0, n_leaves, U);
+        const double dt = (p->cfl * p->dx) / amax;
+        if (dt_hist) dt_hist[s] = dt;
+        double* in[3] = {U, U1, U2};
+        double* out[3] = {U1, U2, U};
+        for (int k = 1; k <= 3; ++k) {
+            orc_amr_fill(p->nf, n_proxy, px, in[k - 1]);
+            for (int L = 0; L <= max_level; ++L)
+                orc_stage(p, n_total, nbr, in[k - 1], U, out[k - 1], k, dt / ldexp(p->dx, max_level - L),
+                          level_first[L], level_first[L + 1]);
+            orc_amr_reflux(p, nbr, level, max_level, n_rec, rf, in[k - 1], out[k - 1], k, dt);
+        }
+    }
+    free(U1);
+    free(U2);
+    return 0;
+}

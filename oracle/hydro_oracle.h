@@ -90,6 +90,35 @@ void orc_ic_sedov(const orc_params* p, int64_t ngrids, const int32_t* pos, int n
                   double* U);
 void orc_ic_random(const orc_params* p, int64_t g_begin, int64_t g_end, uint64_t seed, double* U);
 
+
+/* --- coarse-fine AMR ---
+ * Leaves numbered level-major (level_first[L] .. level_first[L+1]-1), then the
+ * proxies.  A leaf's face neighbour is a same-level leaf, a proxy or -1.
+ * Proxy kinds: 0 = prolongation (piecewise constant) from coarse leaf src[0],
+ * octant bit i = the proxy's half of that leaf along axis i; 1 = restriction
+ * (mean of 2x2x2 cells) from the 8 fine leaves src[octant o].  Reflux record:
+ * coarse leaf + for each face the 4 fine leaves behind it ((a>>2) + 2 (b>>2)
+ * over the face's transverse axes, -1 = not a coarse-fine face). */
+typedef struct {
+    int32_t dst, kind, octant, src[8];
+} orc_amr_proxy;
+typedef struct {
+    int32_t coarse;
+    int32_t fine[6][4];
+} orc_amr_reflux_rec;
+
+void orc_amr_fill(int nf, int64_t n_proxy, const orc_amr_proxy* px, double* U);
+/* Flux correction after stage `stage` (Uout already holds the stage result):
+ * coarse boundary cells take the mean of the fine face fluxes instead of
+ * their own.  dx of level L = ldexp(p->dx, max_level - L). */
+void orc_amr_reflux(const orc_params* p, const int64_t* nbr, const int32_t* level, int max_level,
+                    int64_t n_rec, const orc_amr_reflux_rec* rf, const double* Uprev, double* Uout, int stage,
+                    double dt);
+/* nsteps SSP-RK3 steps on an AMR mesh, one global dt = cfl dx / amax. */
+int orc_run_amr(const orc_params* p, int64_t n_total, const int64_t* nbr, const int32_t* level,
+                const int64_t* level_first, int max_level, int64_t n_proxy, const orc_amr_proxy* px,
+                int64_t n_rec, const orc_amr_reflux_rec* rf, double* U, int nsteps, double* dt_hist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,237 @@
+// amr_kernels.cu — coarse–fine AMR boundaries (SURVEY.md §8(f) rank 2,
+// DESIGN.md §11): the proxy fill (prolongation / restriction ghosts) before
+// each RK stage and the coarse flux correction after it.
+//
+// The reference's octree (build_mesh, workload.cpp:264-327) links only
+// same-level faces (Mesh::validate, workload.cpp:160-161); Octo-Tiger fills
+// coarse–fine ghosts from the other level and corrects the coarse fluxes
+// (PAPER.md:346).  Here a leaf whose face neighbour sits on another level
+// points at a proxy sub-grid slot (like the halo proxies of foreign
+// neighbours), so the fused stage kernel runs unchanged; these two kernels
+// are the only AMR-specific device code.  Both follow oracle/hydro_oracle.c
+// (orc_amr_fill, orc_amr_reflux) operation for operation (--fmad=false), so
+// the AMR path is bitwise equal to the oracle.
+//
+// Neither kernel is on the uniform-mesh hot path; they are latency-light
+// (proxy fill: 4 KB·nf copied or averaged per proxy; reflux: one CTA per
+// coarse sub-grid with a coarse–fine face, five face fluxes per face cell).
+#include "hydro_device.cuh"
+#include "hydro_kernels.h"
+
+namespace tsh {
+namespace {
+
+__device__ __forceinline__ int cidx(int x, int y, int z) { return (z * N + y) * N + x; }
+
+__global__ void __launch_bounds__(NC) amr_fill_kernel(double* __restrict__ U, int nf, const AmrProxy* px) {
+    const AmrProxy& r = px[blockIdx.x];
+    const int c = threadIdx.x;
+    const int x = c & 7, y = (c >> 3) & 7, z = c >> 6;
+    double* dst = U + (size_t)r.dst * nf * NC + c;
+    if (r.kind == 0) {
+        const int cc = cidx((r.octant & 1) * 4 + x / 2, ((r.octant >> 1) & 1) * 4 + y / 2,
+                            ((r.octant >> 2) & 1) * 4 + z / 2);
+        const double* s = U + (size_t)r.src[0] * nf * NC + cc;
+        for (int f = 0; f < nf; ++f) dst[(size_t)f * NC] = s[(size_t)f * NC];
+    } else {
+        const int o = (x >> 2) | ((y >> 2) << 1) | ((z >> 2) << 2);
+        const int bx = 2 * (x & 3), by = 2 * (y & 3), bz = 2 * (z & 3);
+        for (int f = 0; f < nf; ++f) {
+            const double* s = U + ((size_t)r.src[o] * nf + f) * NC;
+            double sum = s[cidx(bx, by, bz)];
+            sum = sum + s[cidx(bx + 1, by, bz)];
+            sum = sum + s[cidx(bx, by + 1, bz)];
+            sum = sum + s[cidx(bx + 1, by + 1, bz)];
+            sum = sum + s[cidx(bx, by, bz + 1)];
+            sum = sum + s[cidx(bx + 1, by, bz + 1)];
+            sum = sum + s[cidx(bx, by + 1, bz + 1)];
+            sum = sum + s[cidx(bx + 1, by + 1, bz + 1)];
+            dst[(size_t)f * NC] = 0.125 * sum;
+        }
+    }
+}
+
+// ---- scalar face flux, the oracle's reconstruct / side_flux / kt_flux -------
+constexpr int kMaxNf = 16;
+constexpr double kC16 = 1.0 / 6.0;
+
+__device__ double o_minmod(double a, double b) {
+    return (copysign(0.5, a) + copysign(0.5, b)) * fmin(fabs(a), fabs(b));
+}
+__device__ double o_minmod_theta(double a, double b, double theta) {
+    return o_minmod(theta * o_minmod(a, b), 0.5 * (a + b));
+}
+__device__ void o_limit_slope(double* ql, double q0, double* qr) {
+    if ((*qr < q0) != (q0 < *ql)) {
+        *ql = q0;
+        *qr = q0;
+        return;
+    }
+    const double t1 = *qr - *ql;
+    const double t2 = *qr + *ql;
+    const double t3 = (t1 * t1) * kC16;
+    const double t4 = t1 * (q0 - 0.5 * t2);
+    if (t4 > t3) {
+        *ql = fma(-2.0, *qr, 3.0 * q0);
+    } else if (-t3 > t4) {
+        *qr = fma(-2.0, *ql, 3.0 * q0);
+    }
+}
+
+// Face states of face j (0..N) of one pencil q[0..P-1] (cells -3..N+2).
+__device__ void o_face_states(int recon, const double* q, int j, double* uL, double* uR) {
+    double lo[P], hi[P];
+    if (recon == 0) {
+        double D[P], fc[P];
+        for (int i = 1; i <= P - 2; ++i) D[i] = o_minmod_theta(q[i + 1] - q[i], q[i] - q[i - 1], 2.0);
+        for (int i = 2; i <= P - 2; ++i) fc[i] = fma(kC16, D[i - 1] - D[i], 0.5 * (q[i - 1] + q[i]));
+        for (int i = 2; i <= P - 3; ++i) {
+            double ql = fc[i], qr = fc[i + 1];
+            o_limit_slope(&ql, q[i], &qr);
+            lo[i] = ql;
+            hi[i] = qr;
+        }
+    } else {
+        for (int i = 2; i <= P - 3; ++i) {
+            const double s = o_minmod(q[i + 1] - q[i], q[i] - q[i - 1]);
+            lo[i] = fma(-0.5, s, q[i]);
+            hi[i] = fma(0.5, s, q[i]);
+        }
+    }
+    *uL = hi[j + 2];
+    *uR = lo[j + 3];
+}
+
+struct FluxParams {
+    int nf, recon;
+    double gamma, p_floor;
+};
+
+__device__ void o_side_flux(const FluxParams& p, int axis, const double* u, double* f, double* a) {
+    const double rho = u[0], sx = u[1], sy = u[2], sz = u[3], E = u[4];
+    const double inv = 1.0 / rho;
+    const double vx = sx * inv, vy = sy * inv, vz = sz * inv;
+    const double s3[3] = {sx, sy, sz}, v3[3] = {vx, vy, vz};
+    const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
+    const double ke2 = fma(s3[axis], v3[axis], fma(s3[t1], v3[t1], s3[t2] * v3[t2]));
+    double pr = (p.gamma - 1.0) * fma(-0.5, ke2, E);
+    pr = fmax(pr, p.p_floor);
+    const double c = sqrt((p.gamma * pr) * inv);
+    const double v = v3[axis];
+    *a = fabs(v) + c;
+    f[0] = u[1 + axis];
+    f[1] = sx * v;
+    f[2] = sy * v;
+    f[3] = sz * v;
+    f[1 + axis] = fma(u[1 + axis], v, pr);
+    f[4] = (E + pr) * v;
+    for (int k = 5; k < p.nf; ++k) f[k] = u[k] * v;
+}
+
+// Pencil cell s (-3..N+2) along `axis` through (a, b) of local sub-grid g
+// (oracle pencil_value: face neighbour or clamp at an outflow boundary).
+__device__ double o_pencil_value(int nf, const int* nbr, const double* U, int g, int f, int axis, int a, int b,
+                                 int s) {
+    int h = g;
+    if (s < 0) {
+        const int nb = nbr[6 * g + 2 * axis];
+        if (nb >= 0) {
+            h = nb;
+            s += N;
+        } else {
+            s = 0;
+        }
+    } else if (s >= N) {
+        const int nb = nbr[6 * g + 2 * axis + 1];
+        if (nb >= 0) {
+            h = nb;
+            s -= N;
+        } else {
+            s = N - 1;
+        }
+    }
+    const int c = axis == 0 ? cidx(s, a, b) : (axis == 1 ? cidx(a, s, b) : cidx(a, b, s));
+    return U[((size_t)h * nf + f) * NC + c];
+}
+
+__device__ void o_face_flux(const FluxParams& p, const int* nbr, const double* U, int g, int axis, int a, int b,
+                            int j, double* F) {
+    double q[P], sL[kMaxNf], sR[kMaxNf], fL[kMaxNf], fR[kMaxNf], aL, aR;
+    for (int f = 0; f < p.nf; ++f) {
+        for (int s = 0; s < P; ++s) q[s] = o_pencil_value(p.nf, nbr, U, g, f, axis, a, b, s - 3);
+        o_face_states(p.recon, q, j, &sL[f], &sR[f]);
+    }
+    o_side_flux(p, axis, sL, fL, &aL);
+    o_side_flux(p, axis, sR, fR, &aR);
+    const double am = fmax(aL, aR);
+    for (int k = 0; k < p.nf; ++k) F[k] = 0.5 * fma(-am, sR[k] - sL[k], fL[k] + fR[k]);
+}
+
+// One CTA per coarse sub-grid with a coarse–fine face; thread (a, b) owns one
+// face cell of each face.  Faces in order 0..5 with a barrier between them,
+// so an edge cell corrected through two faces gets the oracle's order.
+__global__ void __launch_bounds__(N* N) amr_reflux_kernel(const double* __restrict__ Uprev, double* Uout,
+                                                          FluxParams p, const int* nbr, const int* level,
+                                                          int max_level, double dx, const AmrReflux* rf,
+                                                          int stage, const double* dt_ptr) {
+    const AmrReflux& r = rf[blockIdx.x];
+    const int g = r.coarse;
+    const double w = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
+    const double dtdx = *dt_ptr / ldexp(dx, max_level - level[g]);
+    const int a = threadIdx.x & 7, b = threadIdx.x >> 3;
+    double Fc[kMaxNf], F00[kMaxNf], F10[kMaxNf], F01[kMaxNf], F11[kMaxNf];
+    for (int face = 0; face < 6; ++face) {
+        if (r.fine[face][0] < 0) continue;
+        const int axis = face >> 1, side = face & 1;
+        const int jc = side ? N : 0, jf = side ? 0 : N, ic = side ? N - 1 : 0;
+        const int leaf = r.fine[face][(a >> 2) + 2 * (b >> 2)];
+        const int fa = 2 * (a & 3), fb = 2 * (b & 3);
+        o_face_flux(p, nbr, Uprev, g, axis, a, b, jc, Fc);
+        o_face_flux(p, nbr, Uprev, leaf, axis, fa, fb, jf, F00);
+        o_face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb, jf, F10);
+        o_face_flux(p, nbr, Uprev, leaf, axis, fa, fb + 1, jf, F01);
+        o_face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb + 1, jf, F11);
+        const int c = axis == 0 ? cidx(ic, a, b) : (axis == 1 ? cidx(a, ic, b) : cidx(a, b, ic));
+        for (int f = 0; f < p.nf; ++f) {
+            const double avg = 0.25 * ((F00[f] + F10[f]) + (F01[f] + F11[f]));
+            const double corr = side ? Fc[f] - avg : avg - Fc[f];
+            double* u = Uout + ((size_t)g * p.nf + f) * NC + c;
+            *u = *u + w * (dtdx * corr);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, long long n, unsigned long long* stamp,
+                            cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (stamp != nullptr) {
+        cudaError_t e = launch_stamp(stamp, 0, s);
+        if (e != cudaSuccess) return e;
+    }
+    amr_fill_kernel<<<(unsigned)n, NC, 0, s>>>(U, nf, px);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
+    return e;
+}
+
+cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int recon, double gamma, double p_floor,
+                              const int* nbr, const int* level, int max_level, double dx, const AmrReflux* rf,
+                              long long n, int stage, const double* dt, unsigned long long* stamp,
+                              cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (nf > kMaxNf) return cudaErrorInvalidValue;
+    if (stamp != nullptr) {
+        cudaError_t e = launch_stamp(stamp, 0, s);
+        if (e != cudaSuccess) return e;
+    }
+    FluxParams p{nf, recon, gamma, p_floor};
+    amr_reflux_kernel<<<(unsigned)n, N * N, 0, s>>>(Uprev, Uout, p, nbr, level, max_level, dx, rf, stage, dt);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
+    return e;
+}
+
+}  // namespace tsh

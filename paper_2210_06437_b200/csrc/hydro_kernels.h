@@ -102,6 +102,20 @@ struct StageArgs {
     unsigned long long* err;
     unsigned long long wait_ns;
     double gamma, gm1, cfl, dx, p_floor;
+    // dx of the sub-grids this launch updates: dx (the finest level's, which
+    // sets dt) on a uniform mesh, dx * 2^(max_level - level) for one level of
+    // an AMR mesh (launched per level, ts_hydro_set_amr_mesh)
+    double dx_upd;
+};
+
+// Coarse–fine AMR (amr_kernels.cu): proxy fill recipe and reflux record,
+// the layouts of ts_amr_proxy / ts_amr_reflux (include/ts_hydro.h).
+struct AmrProxy {
+    int dst, kind, octant, src[8];  // kind 0: prolong from src[0]; 1: restrict from src[0..7]
+};
+struct AmrReflux {
+    int coarse;
+    int fine[6][4];  // per face the 4 fine sub-grids behind it, -1: not coarse–fine
 };
 
 // pdl: launch as a programmatic dependent of the previous kernel on `s`
@@ -129,6 +143,12 @@ cudaError_t launch_dt_exchange(const double* local_amax, double* const* push_gat
                                unsigned long long wait_ns, cudaStream_t s);
 cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
                               unsigned long long* err, unsigned long long wait_ns, cudaStream_t s);
+cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, long long n, unsigned long long* stamp,
+                            cudaStream_t s);
+cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int recon, double gamma, double p_floor,
+                              const int* nbr, const int* level, int max_level, double dx, const AmrReflux* rf,
+                              long long n, int stage, const double* dt, unsigned long long* stamp,
+                              cudaStream_t s);
 cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
                                  int sms, cudaStream_t s);
 

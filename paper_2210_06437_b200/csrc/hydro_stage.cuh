@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         __syncthreads();
         amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
     }
-    const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / A.dx);
+    const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / A.dx_upd);
     if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
         if (A.dt_out != nullptr) *A.dt_out = (A.cfl * A.dx) / amax_in;
         if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                 amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
             }
             const double dt = (A.cfl * A.dx) / amax_in;
-            c.dtdx = 0.5 * (dt / A.dx);  // the sweeps carry twice the KT flux (kt2)
+            c.dtdx = 0.5 * (dt / A.dx_upd);  // the sweeps carry twice the KT flux (kt2)
             if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
                 if (A.dt_out != nullptr) *A.dt_out = dt;
                 if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;

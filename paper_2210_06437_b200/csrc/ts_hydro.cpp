@@ -48,6 +48,8 @@ constexpr const char* kNameStage[4] = {"", "hydro_stage1_kernel", "hydro_stage2_
 constexpr const char* kNameSignal = "signal_speed_kernel";
 constexpr const char* kNamePack = "halo_pack_kernel";
 constexpr const char* kNameUnpack = "halo_unpack_kernel";
+constexpr const char* kNameAmrFill = "amr_ghost_fill_kernel";
+constexpr const char* kNameAmrReflux = "amr_reflux_kernel";
 constexpr const char* kNameH2D = "copy_host_to_device";
 constexpr const char* kNameD2H = "copy_device_to_host";
 constexpr const char* kNameD2D = "copy_device_to_device";
@@ -280,6 +282,15 @@ struct ts_hydro_ctx {
     const double* amax_src = nullptr; // where this step's dt comes from
     int amax_n = 1;
 
+    // coarse-fine AMR mesh (ts_hydro_set_amr_mesh): leaves level-major, proxies after them
+    bool amr = false;
+    int amr_max_level = 0;
+    std::vector<int64_t> amr_level_first;  // [max_level + 2]
+    int64_t amr_n_proxy = 0, amr_n_rec = 0;
+    tsh::AmrProxy* d_amr_proxy = nullptr;
+    tsh::AmrReflux* d_amr_rec = nullptr;
+    int32_t* d_amr_level = nullptr;
+
     // stepping
     uint64_t steps_done = 0;
     uint64_t launches = 0;
@@ -427,6 +438,10 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_recv_entries);
     dfree(c, &c->d_send);
     dfree(c, &c->d_recv);
+    dfree(c, &c->d_amr_proxy);
+    dfree(c, &c->d_amr_rec);
+    dfree(c, &c->d_amr_level);
+    c->amr = false;
     c->have_mesh = false;
 }
 
@@ -657,6 +672,7 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     a.gm1 = c->cfg.gamma - 1.0;
     a.cfl = c->cfg.cfl;
     a.dx = c->cfg.dx;
+    a.dx_upd = c->cfg.dx;
     a.p_floor = c->cfg.p_floor;
     a.err = c->h_clock + 1;
     a.wait_ns = c->wait_ns;
@@ -801,7 +817,54 @@ int do_compute_dt(ts_hydro_ctx* c) {
     return TS_OK;
 }
 
+// One step on an AMR mesh (single rank, stream order): per stage, refill the
+// proxies of U^(k-1) (prolongation / restriction), one stage launch per
+// level (its own dx; the first launch of stage 1 writes dt and zeroes the
+// max slot stage 3 accumulates into), then the coarse flux correction.
+int do_step_amr(ts_hydro_ctx* c) {
+    cudaStream_t s;
+    int rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    const double* dt_ptr = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+    for (int stage = 1; stage <= 3; ++stage) {
+        tsh::StageArgs a = stage_args(c, stage);
+        unsigned long long* stamp = nullptr;
+        if (c->amr_n_proxy > 0) {
+            rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrFill, 0, 0, &stamp);
+            if (rc) return rc;
+            TS_CUDA(c, tsh::launch_amr_fill(const_cast<double*>(a.Uprev), c->nf, c->d_amr_proxy, c->amr_n_proxy,
+                                            stamp, s));
+        }
+        bool first = true;
+        for (int L = 0; L <= c->amr_max_level; ++L) {
+            const int64_t f0 = c->amr_level_first[(size_t)L], n = c->amr_level_first[(size_t)L + 1] - f0;
+            if (n <= 0) continue;
+            tsh::StageArgs b = a;
+            b.dx_upd = std::ldexp(c->cfg.dx, c->amr_max_level - L);
+            if (stage == 1 && first) {
+                b.amax_reset = amax_slot(c, c->steps_done + 1);
+                b.dt_out = const_cast<double*>(dt_ptr);
+            }
+            rc = launch_stage_list(c, b, stage, nullptr, n, (int)f0, 0, 0);
+            if (rc) return rc;
+            first = false;
+        }
+        if (c->amr_n_rec > 0) {
+            rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrReflux, 0, 0, &stamp);
+            if (rc) return rc;
+            TS_CUDA(c, tsh::launch_amr_reflux(a.Uprev, a.Uout, c->nf, c->cfg.recon, c->cfg.gamma, c->cfg.p_floor,
+                                              c->d_nbr, c->d_amr_level, c->amr_max_level, c->cfg.dx, c->d_amr_rec,
+                                              c->amr_n_rec, stage, dt_ptr, stamp, s));
+        }
+    }
+    c->amax_src = nullptr;
+    c->flow_chain = false;
+    c->steps_done++;
+    return TS_OK;
+}
+
 int do_step(ts_hydro_ctx* c) {
+    if (c->amr) return do_step_amr(c);
     cudaStream_t s, cs, bs;
     int rc = ensure_stream(c, 0, &s);
     if (rc) return rc;
@@ -1226,6 +1289,8 @@ int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_m
     return TS_OK;
 }
 
+static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, int32_t world);
+
 int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int32_t* owner, int32_t world,
                       int32_t rank) {
     int rc = guard(c);
@@ -1287,8 +1352,15 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
         }
         (foreign ? c->boundary : c->interior).push_back((int32_t)l);
     }
-    rc = build_plans(c, nbr, owner);
+    return bind_mesh(c, nbr, owner, world);
+}
+
+// Device side of a mesh whose owned / proxy lists, local neighbour table and
+// interior / boundary lists are in place (ts_hydro_set_mesh, _set_amr_mesh).
+static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, int32_t world) {
+    int rc = build_plans(c, nbr, owner);
     if (rc) return rc;
+    const int64_t nl = c->n_owned + c->n_proxy;
     if (c->host_only) {
         c->have_mesh = true;
         return TS_OK;
@@ -1441,6 +1513,98 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     c->amax_src = nullptr;
     c->xseq = c->aseq = 0;
     c->have_mesh = true;
+    return TS_OK;
+}
+
+int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const int32_t* level, int32_t max_level,
+                          int64_t np, const ts_amr_proxy* px, int64_t nr, const ts_amr_reflux* rf) {
+    static_assert(sizeof(ts_amr_proxy) == sizeof(tsh::AmrProxy), "proxy layout");
+    static_assert(sizeof(ts_amr_reflux) == sizeof(tsh::AmrReflux), "reflux layout");
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (nl < 1 || nbr == nullptr || level == nullptr) return fail(c, TS_EINVAL, "empty AMR mesh");
+    if (np < 0 || nr < 0 || (np > 0 && px == nullptr) || (nr > 0 && rf == nullptr))
+        return fail(c, TS_EINVAL, "AMR proxy / reflux tables missing");
+    if (max_level < 0 || max_level > 30) return fail(c, TS_EINVAL, "max_level outside 0..30");
+    if (nl + np > (int64_t)INT32_MAX / 2) return fail(c, TS_EINVAL, "too many sub-grids");
+    const int64_t nt = nl + np;
+    std::vector<int64_t> first((size_t)max_level + 2, 0);
+    for (int64_t i = 0; i < nl; ++i) {
+        const std::string where = "leaf " + std::to_string(i) + ": ";
+        if (level[i] < 0 || level[i] > max_level) return fail(c, TS_EINVAL, where + "level outside 0..max_level");
+        if (i > 0 && level[i] < level[i - 1]) return fail(c, TS_EINVAL, where + "leaves are not level-major");
+        for (int f = 0; f < 6; ++f) {
+            const int64_t nb = nbr[6 * i + f];
+            if (nb == -1) continue;
+            if (nb < 0 || nb >= nt) return fail(c, TS_EINVAL, where + "neighbor id out of range");
+            if (nb == i) return fail(c, TS_EINVAL, where + "sub-grid linked to itself");
+            // same-level leaf links are symmetric (Mesh::validate, workload.cpp:156-161)
+            if (nb < nl && nbr[6 * nb + (f ^ 1)] != i) return fail(c, TS_EINVAL, where + "leaf link is not symmetric");
+        }
+    }
+    for (int L = 0; L <= max_level + 1; ++L)
+        first[(size_t)L] = std::lower_bound(level, level + nl, L) - level;
+    for (int64_t k = 0; k < np; ++k) {
+        const ts_amr_proxy& r = px[k];
+        const std::string where = "proxy " + std::to_string(k) + ": ";
+        if (r.dst != nl + k) return fail(c, TS_EINVAL, where + "proxies must be numbered n_leaves + k");
+        if (r.kind != 0 && r.kind != 1) return fail(c, TS_EINVAL, where + "kind must be 0 (prolong) or 1 (restrict)");
+        if (r.octant < 0 || r.octant > 7) return fail(c, TS_EINVAL, where + "octant outside 0..7");
+        for (int o = 0; o < (r.kind == 0 ? 1 : 8); ++o)
+            if (r.src[o] < 0 || r.src[o] >= nl) return fail(c, TS_EINVAL, where + "source is not a leaf");
+    }
+    for (int64_t k = 0; k < nr; ++k) {
+        const ts_amr_reflux& r = rf[k];
+        const std::string where = "reflux record " + std::to_string(k) + ": ";
+        if (r.coarse < 0 || r.coarse >= nl) return fail(c, TS_EINVAL, where + "coarse id is not a leaf");
+        for (int f = 0; f < 6; ++f) {
+            if (r.fine[f][0] < 0) continue;
+            for (int q = 0; q < 4; ++q)
+                if (r.fine[f][q] < 0 || r.fine[f][q] >= nl || level[r.fine[f][q]] != level[r.coarse] + 1)
+                    return fail(c, TS_EINVAL, where + "fine ids must be leaves one level finer");
+        }
+    }
+    if (!c->host_only) {
+        cudaSetDevice(c->dev);
+        rc = sync_all(c);
+        if (rc) return rc;
+        free_mesh(c);
+    }
+    c->world = 1;
+    c->rank = 0;
+    c->n_global = nl;
+    c->mesh_nbr.assign(nbr, nbr + 6 * nl);
+    c->mesh_owner.assign((size_t)nl, 0);
+    c->owned_gid.resize((size_t)nl);
+    for (int64_t i = 0; i < nl; ++i) c->owned_gid[(size_t)i] = i;
+    c->proxy_gid.resize((size_t)np);
+    for (int64_t k = 0; k < np; ++k) c->proxy_gid[(size_t)k] = nl + k;
+    c->n_owned = nl;
+    c->n_proxy = np;
+    c->nbr_local.assign((size_t)nt * 6, -1);
+    for (int64_t i = 0; i < 6 * nl; ++i) c->nbr_local[(size_t)i] = (int32_t)nbr[i];
+    c->interior.resize((size_t)nl);
+    for (int64_t i = 0; i < nl; ++i) c->interior[(size_t)i] = (int32_t)i;
+    c->boundary.clear();
+    rc = bind_mesh(c, nullptr, nullptr, 1);
+    if (rc) return rc;
+    c->amr_max_level = max_level;
+    c->amr_level_first = first;
+    c->amr_n_proxy = np;
+    c->amr_n_rec = nr;
+    if (!c->host_only) {
+        rc = dalloc(c, &c->d_amr_proxy, (size_t)std::max<int64_t>(np, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_rec, (size_t)std::max<int64_t>(nr, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_level, (size_t)nl);
+        if (rc) return rc;
+        if (np > 0)
+            TS_CUDA(c, cudaMemcpy(c->d_amr_proxy, px, (size_t)np * sizeof(tsh::AmrProxy), cudaMemcpyHostToDevice));
+        if (nr > 0)
+            TS_CUDA(c, cudaMemcpy(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaMemcpy(c->d_amr_level, level, (size_t)nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    c->amr = true;
     return TS_OK;
 }
 
@@ -1647,6 +1811,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
     if (c->cfg.stream_count < 5) return fail(c, TS_EINVAL, "pipelined host steps need stream_count >= 5");
+    if (c->amr) return fail(c, TS_ESTATE, "pipelined host steps are not available on an AMR mesh (use ts_hydro_step_host)");
     cudaSetDevice(c->dev);
     cudaStream_t s, sh, sd;
     rc = ensure_stream(c, 0, &s);
@@ -1818,6 +1983,7 @@ int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_i
     if (count <= 0 || owned_index == nullptr) return fail(c, TS_EINVAL, "empty sub-grid list");
     if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
     if (c->world > 1) return fail(c, TS_ESTATE, "per-sub-grid launches are single-rank (use ts_hydro_step)");
+    if (c->amr) return fail(c, TS_ESTATE, "per-sub-grid launches are not available on an AMR mesh (use ts_hydro_step)");
     if (!c->dt_valid) return fail(c, TS_ESTATE, "no dt (call ts_hydro_compute_dt first)");
     std::vector<int32_t> list((size_t)count);
     for (int64_t k = 0; k < count; ++k) {
@@ -2164,6 +2330,7 @@ int ts_hydro_save(ts_hydro_ctx* c, const char* path) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->amr) return fail(c, TS_ESTATE, "checkpoints of AMR meshes are not supported");
     if (path == nullptr) return fail(c, TS_EINVAL, "null checkpoint path");
     std::vector<double> st((size_t)c->n_owned * c->nf * kNC);
     rc = ts_hydro_download(c, 0, c->n_owned, st.data());
@@ -2178,6 +2345,7 @@ int ts_hydro_restore(ts_hydro_ctx* c, const char* const* paths, int32_t n_paths)
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (c->amr) return fail(c, TS_ESTATE, "checkpoints of AMR meshes are not supported");
     if (paths == nullptr || n_paths < 1) return fail(c, TS_EINVAL, "no checkpoint files");
     const size_t per = (size_t)c->nf * kNC;
     std::vector<double> st((size_t)c->n_owned * per);

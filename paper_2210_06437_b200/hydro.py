@@ -119,6 +119,8 @@ _SIGNATURES = {
     "ts_hydro_num_fields": (ctypes.c_int, [_vp]),
     "ts_hydro_uniform_mesh": (ctypes.c_int, [ctypes.c_int32] * 5 + [_i64p, _i32p, _i32p]),
     "ts_hydro_set_mesh": (ctypes.c_int, [_vp, ctypes.c_int64, _i64p, _i32p, ctypes.c_int32, ctypes.c_int32]),
+    "ts_hydro_set_amr_mesh": (ctypes.c_int, [_vp, ctypes.c_int64, _i64p, _i32p, ctypes.c_int32, ctypes.c_int64,
+                                             _i32p, ctypes.c_int64, _i32p]),
     "ts_hydro_local_counts": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
     "ts_hydro_owned_ids": (ctypes.c_int, [_vp, _i64p]),
     "ts_hydro_halo_plan": (ctypes.c_int, [_vp, ctypes.c_int32, _i64p, _i64p, _i64p, _i64p]),
@@ -468,6 +470,19 @@ class CudaDevice:
                     "set_mesh")
         self.mesh = mesh
         self.rank = rank
+
+    def set_amr_mesh(self, mesh) -> None:
+        """Bind a coarse-fine AMR mesh (paper_2210_06437_b200.amr.AmrMesh), single rank."""
+        nbr = np.ascontiguousarray(mesh.nbr, np.int64)
+        lev = np.ascontiguousarray(mesh.level, np.int32)
+        px = np.ascontiguousarray(mesh.proxies, np.int32)
+        rf = np.ascontiguousarray(mesh.reflux, np.int32)
+        self._check(lib().ts_hydro_set_amr_mesh(self._h, mesh.n_leaves, _p(nbr, _i64p), _p(lev, _i32p),
+                                                mesh.max_level, mesh.n_proxy, _p(px, _i32p), len(rf),
+                                                _p(rf, _i32p)), "set_amr_mesh")
+        self.mesh = None
+        self.amr_mesh = mesh
+        self.rank = 0
 
     def local_counts(self):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -1,0 +1,195 @@
+"""Coarse-fine AMR: mesh builder, the
+oracle's prolongation / restriction / reflux, and the C-ABI validation of
+ts_hydro_set_amr_mesh on a host-only context.  CPU only; the GPU parity of the
+same runs is in test_gpu_amr.py."""
+import numpy as np
+import pytest
+
+from paper_2210_06437_b200 import amr
+
+DX = 1.0 / 64
+
+# a 2x2x2 block of level-0 positions refined in the middle of a 4^3 box
+CENTRE_BLOCK = {(0, x, y, z) for x in (1, 2) for y in (1, 2) for z in (1, 2)}
+# an L-shaped refined region off-centre: coarse leaves see fine ones on 1-3 faces
+L_SHAPE = {(0, 1, 1, 1), (0, 2, 1, 1), (0, 1, 2, 1), (0, 1, 1, 2), (0, 2, 2, 2)}
+
+
+def totals(mesh, U, nf):
+    vol = mesh.cell_volumes(DX)
+    return np.array([(U[:mesh.n_leaves, f].sum(axis=1) * vol).sum() for f in range(nf)])
+
+
+def test_builder_covers_the_domain_once():
+    for refine in (CENTRE_BLOCK, L_SHAPE, set()):
+        m = amr.amr_mesh(4, 4, 4, refine)
+        ext = 4 * 8 * DX * 2 ** m.max_level
+        assert np.isclose(m.cell_volumes(DX).sum() * 512, ext ** 3, rtol=1e-15, atol=0)
+        assert (np.diff(m.level) >= 0).all()
+        assert m.level_first[-1] == m.n_leaves
+        # same-level leaf links are symmetric; proxies only across levels
+        for i in range(m.n_leaves):
+            for f in range(6):
+                nb = m.nbr[i, f]
+                if 0 <= nb < m.n_leaves:
+                    assert m.nbr[nb, f ^ 1] == i and m.level[nb] == m.level[i]
+
+
+def test_builder_proxies_and_reflux_records():
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    assert m.n_proxy > 0 and len(m.reflux) > 0
+    kinds = m.proxies[:, 1]
+    assert set(kinds.tolist()) == {0, 1}
+    for r in m.proxies:
+        dst, kind, octant, src = r[0], r[1], r[2], r[3:]
+        assert m.n_leaves <= dst < m.n_total
+        if kind == 0:
+            assert m.level[src[0]] == 0 and 0 <= octant < 8
+        else:
+            assert (m.level[src] == 1).all()
+            # children in octant order: positions 2q + o
+            base = m.pos[src[0]]
+            for o in range(8):
+                assert tuple(m.pos[src[o]]) == (base[0] + (o & 1), base[1] + ((o >> 1) & 1), base[2] + (o >> 2))
+    for rec in m.reflux:
+        g, fine = rec[0], rec[1:].reshape(6, 4)
+        assert m.level[g] == 0
+        for f in range(6):
+            if fine[f, 0] < 0:
+                continue
+            axis, side = f >> 1, f & 1
+            for k in fine[f]:
+                assert m.level[k] == 1
+                # the fine leaf touches the coarse face
+                lo = m.pos[g] * 2
+                fp = m.pos[k]
+                assert fp[axis] == (lo[axis] + 2 if side else lo[axis] - 1)
+
+
+def test_unbalanced_mesh_is_rejected():
+    with pytest.raises(ValueError, match="2:1"):
+        amr.amr_mesh(4, 4, 4, lambda L, p: p == (1, 1, 1) or (L == 1 and p == (2, 2, 2)), max_level=2)
+
+
+def test_unrefined_amr_run_is_the_uniform_run(oracle_lib):
+    """No refinement: the AMR driver reduces to orc_run bitwise."""
+    m = amr.amr_mesh(4, 4, 4, set())
+    assert m.n_proxy == 0
+    nbr, pos, _ = oracle_lib.uniform_mesh(4, 4, 4)
+    assert (nbr == m.nbr).all() and (pos == m.pos).all()
+    p = oracle_lib.params(nf=6, dx=DX * 2)
+    U0 = amr.ic_blast(m, 6, DX * 2)
+    Ua, da = oracle_lib.run_amr(p, m, U0, 3)
+    Uu, du = oracle_lib.run(p, nbr, U0, 3)
+    assert np.array_equal(Ua, Uu) and np.array_equal(da, du)
+
+
+def test_fully_refined_amr_run_is_the_fine_uniform_run(oracle_lib):
+    """Every level-0 position refined: a uniform level-1 mesh, bitwise."""
+    m = amr.amr_mesh(2, 2, 2, lambda L, p: True)
+    assert m.n_proxy == 0 and (m.level == 1).all()
+    nbr, pos, _ = oracle_lib.uniform_mesh(4, 4, 4)
+    p = oracle_lib.params(nf=6, dx=DX)
+    U0 = amr.ic_blast(m, 6, DX, drift=(0.3, -0.2, 0.1))
+    at = {tuple(q): i for i, q in enumerate(pos)}
+    perm = np.array([at[tuple(q)] for q in m.pos])  # leaf -> uniform id
+    Uu0 = np.empty_like(U0)
+    Uu0[perm] = U0
+    Ua, da = oracle_lib.run_amr(p, m, U0, 2)
+    Uu, du = oracle_lib.run(p, nbr, Uu0, 2)
+    assert np.array_equal(Ua, Uu[perm]) and np.array_equal(da, du)
+
+
+# bump centred on a coarse-fine face, >= 0.375 (12 coarse cells) from the
+# outflow boundary: closer, the boundary itself leaks ~1e-12 in 5 steps on a
+# uniform mesh too
+CENTRE_BLOCK6 = {(0, x, y, z) for x in (2, 3) for y in (2, 3) for z in (2, 3)}
+CF_CASES = [((6, 6, 6), CENTRE_BLOCK6, (1.0, 0.75, 0.75)), ((4, 4, 4), L_SHAPE, (0.625, 0.625, 0.5))]
+
+
+@pytest.mark.parametrize("dims,refine,centre", CF_CASES, ids=["centre", "lshape"])
+@pytest.mark.parametrize("recon", [0, 1])
+def test_reflux_conserves_to_round_off(oracle_lib, dims, refine, centre, recon):
+    m = amr.amr_mesh(*dims, refine)
+    p = oracle_lib.params(nf=6, recon=recon, dx=DX)
+    U0 = amr.ic_blast(m, 6, DX, width=0.04, centre=centre)
+    # the bump sits on a coarse-fine face and its tail at the outflow
+    # boundary is ~1e-17, so mass, momentum and energy only move between cells
+    t0 = totals(m, U0, 6)
+    U, _ = oracle_lib.run_amr(p, m, U0, 5)
+    err = np.abs(totals(m, U, 6) - t0)[:5] / np.abs(t0).max()
+    assert err.max() < 1e-14, err
+    # without the flux correction the coarse-fine faces leak
+    m0 = amr.AmrMesh(m.dims, m.max_level, m.level, m.pos, m.nbr, m.level_first, m.proxies, m.reflux[:0])
+    U_nofix, _ = oracle_lib.run_amr(p, m0, U0, 5)
+    leak = np.abs(totals(m, U_nofix, 6) - t0)[[0, 4]] / np.abs(t0).max()
+    assert leak.min() > 1e-8, leak
+
+
+def test_uniform_flow_stays_uniform_across_levels(oracle_lib):
+    """Free-stream preservation: prolongation, restriction and reflux of a
+    uniform state are exact, so every cell keeps its bits."""
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    p = oracle_lib.params(nf=8, dx=DX)
+    U0 = amr.ic_blast(m, 8, DX, amp=0.0, drift=(0.5, -0.25, 0.125))
+    U0[:m.n_leaves, 6:] = 0.3
+    U, _ = oracle_lib.run_amr(p, m, U0, 4)
+    for f in range(8):
+        assert (U[:m.n_leaves, f] == U0[0, f, 0]).all(), f
+
+
+def test_fill_prolongs_and_restricts(oracle_lib):
+    m = amr.amr_mesh(2, 2, 2, {(0, 0, 0, 0)})
+    U = np.zeros((m.n_total, 6, 512))
+    rng = np.random.default_rng(5)
+    U[:m.n_leaves] = rng.random((m.n_leaves, 6, 512)) + 1
+    oracle_lib.amr_fill(6, m, U)
+    i = np.arange(512)
+    x, y, z = i & 7, (i >> 3) & 7, i >> 6
+    for r in m.proxies:
+        dst, kind, octant, src = r[0], r[1], r[2], r[3:]
+        if kind == 0:
+            cc = ((octant >> 2 & 1) * 4 + z // 2) * 64 + ((octant >> 1 & 1) * 4 + y // 2) * 8 + (octant & 1) * 4 + x // 2
+            assert np.array_equal(U[dst], U[src[0]][:, cc])
+        else:
+            o = (x >> 2) | ((y >> 2) << 1) | ((z >> 2) << 2)
+            fine = U[src[o]]  # [512(cell), 6, 512] per proxy cell
+            bx, by, bz = 2 * (x & 3), 2 * (y & 3), 2 * (z & 3)
+            mean = sum(fine[np.arange(512), :, (bz + k) * 64 + (by + j) * 8 + bx + ii]
+                       for k in (0, 1) for j in (0, 1) for ii in (0, 1)) / 8
+            assert np.allclose(U[dst].T, mean, rtol=1e-15, atol=0)
+
+
+def test_set_amr_mesh_validates(hydro):
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    d = hydro.CudaDevice(hydro.HydroConfig(device_id=-1))
+    d.set_amr_mesh(m)
+    assert d.local_counts()[:2] == (m.n_leaves, m.n_proxy)
+
+    def bad(**kw):
+        f = dict(nbr=m.nbr, level=m.level, proxies=m.proxies, reflux=m.reflux)
+        f.update(kw)
+        return amr.AmrMesh(m.dims, m.max_level, f["level"], m.pos, f["nbr"], m.level_first, f["proxies"],
+                           f["reflux"])
+
+    lev = m.level.copy()
+    lev[0] = 1
+    with pytest.raises(ValueError, match="level-major"):
+        d.set_amr_mesh(bad(level=lev))
+    nbr = m.nbr.copy()
+    nbr[0, 1] = m.n_total + 3
+    with pytest.raises(ValueError, match="out of range"):
+        d.set_amr_mesh(bad(nbr=nbr))
+    px = m.proxies.copy()
+    px[0, 1] = 7
+    with pytest.raises(ValueError, match="kind"):
+        d.set_amr_mesh(bad(proxies=px))
+    px = m.proxies.copy()
+    px[0, 3] = m.n_leaves + 1
+    with pytest.raises(ValueError, match="not a leaf"):
+        d.set_amr_mesh(bad(proxies=px))
+    rf = m.reflux.copy()
+    f = next(k for k in range(6) if rf[0, 1 + 4 * k] >= 0)
+    rf[0, 1 + 4 * f] = rf[0, 0]
+    with pytest.raises(ValueError, match="one level finer"):
+        d.set_amr_mesh(bad(reflux=rf))

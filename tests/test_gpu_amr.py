@@ -1,0 +1,132 @@
+"""GPU parity of the coarse-fine AMR path: ts_hydro_set_amr_mesh
++ ts_hydro_step through the C ABI against the oracle's orc_run_amr on the same
+inputs.  The proxy fill and reflux kernels follow the oracle operation for
+operation and the stage kernel is the uniform path's (bitwise to the oracle),
+so the contract is bitwise; RTOL (1e-12, north_star) is the stated tolerance."""
+import numpy as np
+import pytest
+
+from paper_2210_06437_b200 import amr
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+DX = 1.0 / 64
+L_SHAPE = {(0, 1, 1, 1), (0, 2, 1, 1), (0, 1, 2, 1), (0, 1, 1, 2), (0, 2, 2, 2)}
+CENTRE_BLOCK6 = {(0, x, y, z) for x in (2, 3) for y in (2, 3) for z in (2, 3)}
+
+
+def gpu_run(hydro, mesh, U0, steps, **kw):
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=DX, **kw))
+    d.set_amr_mesh(mesh)
+    d.upload(U0[:mesh.n_leaves])
+    d.step(steps)
+    d.synchronize()
+    U = d.download()
+    dt = d.last_dt()
+    recs = d.flush_activity()
+    d.close()
+    return U, dt, recs
+
+
+def check(U, ref, n_leaves):
+    ref = ref[:n_leaves]
+    for f in range(ref.shape[1]):
+        scale = np.abs(ref[:, f]).max() or 1.0
+        assert np.abs(U[:, f] - ref[:, f]).max() / scale <= RTOL, f
+    return np.array_equal(U, ref)
+
+
+@pytest.mark.parametrize("recon", [0, 1], ids=["ppm", "minmod"])
+@pytest.mark.parametrize("species", [0, 5])
+@pytest.mark.parametrize("case", ["lshape", "centre6"])
+def test_amr_steps_match_oracle_bitwise(hydro, oracle_lib, recon, species, case):
+    if case == "lshape":
+        m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+        centre = (0.625, 0.625, 0.5)
+    else:
+        m = amr.amr_mesh(6, 6, 6, CENTRE_BLOCK6)
+        centre = (1.0, 0.75, 0.75)
+    nf = 6 + species
+    U0 = amr.ic_blast(m, nf, DX, width=0.06, centre=centre, drift=(0.3, -0.1, 0.2))
+    p = oracle_lib.params(nf=nf, recon=recon, dx=DX)
+    ref, dts = oracle_lib.run_amr(p, m, U0, 4)
+    U, dt, _ = gpu_run(hydro, m, U0, 4, n_species=species, recon=("ppm", "minmod")[recon])
+    assert dt == dts[-1]
+    assert check(U, ref, m.n_leaves), "AMR path is not bitwise equal to the oracle"
+
+
+def test_amr_reflux_conserves_on_gpu(hydro, oracle_lib):
+    m = amr.amr_mesh(6, 6, 6, CENTRE_BLOCK6)
+    U0 = amr.ic_blast(m, 6, DX, width=0.04, centre=(1.0, 0.75, 0.75))
+    vol = m.cell_volumes(DX)
+    U, _, _ = gpu_run(hydro, m, U0, 5)
+    t0 = np.array([(U0[:m.n_leaves, f].sum(axis=1) * vol).sum() for f in range(5)])
+    t1 = np.array([(U[:, f].sum(axis=1) * vol).sum() for f in range(5)])
+    assert (np.abs(t1 - t0) / np.abs(t0).max()).max() < 1e-14
+
+
+def test_amr_free_stream_is_exact_on_gpu(hydro):
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    U0 = amr.ic_blast(m, 6, DX, amp=0.0, drift=(0.5, -0.25, 0.125))
+    U, _, _ = gpu_run(hydro, m, U0, 3)
+    for f in range(6):
+        assert (U[:, f] == U0[0, f, 0]).all(), f
+
+
+def test_amr_medium_mesh_matches_oracle(hydro, oracle_lib):
+    """16^3 level-0 box with a refined 4^3 centre: 4544 leaves, 3 steps."""
+    m = amr.amr_mesh(16, 16, 16, lambda L, p: all(6 <= v < 10 for v in p))
+    assert m.n_leaves == 4096 - 64 + 512
+    U0 = amr.ic_blast(m, 6, DX / 2, width=0.2, centre=(1.0, 1.0, 1.0))
+    p = oracle_lib.params(nf=6, dx=DX / 2)
+    ref, dts = oracle_lib.run_amr(p, m, U0, 3)
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=DX / 2))
+    d.set_amr_mesh(m)
+    d.upload(U0[:m.n_leaves])
+    d.step(3)
+    d.synchronize()
+    U = d.download()
+    assert d.last_dt() == dts[-1]
+    d.close()
+    assert check(U, ref, m.n_leaves)
+
+
+def test_amr_activity_records_and_refusals(hydro, tmp_path):
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    U0 = amr.ic_blast(m, 6, DX)
+    _, _, recs = gpu_run(hydro, m, U0, 2)
+    names = [r.name for r in recs]
+    # per step: 3 x (fill + one stage launch per level + reflux)
+    assert names.count("amr_ghost_fill_kernel") == 6
+    assert names.count("amr_reflux_kernel") == 6
+    assert sum(n.startswith("hydro_stage") for n in names) == 12
+    for r in recs:
+        assert r.start_ns <= r.end_ns
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=DX))
+    d.set_amr_mesh(m)
+    d.upload(U0[:m.n_leaves])
+    with pytest.raises(hydro.TsError, match="AMR"):
+        d.save(str(tmp_path / "x.ckpt"))
+    with pytest.raises(hydro.TsError, match="AMR"):
+        d.launch_stage(1, [0])
+    d.close()
+
+
+def test_amr_step_host_matches_resident_step(hydro):
+    import ctypes
+    m = amr.amr_mesh(4, 4, 4, L_SHAPE)
+    U0 = amr.ic_blast(m, 6, DX, drift=(0.1, 0.2, 0.3))
+    ref, _, _ = gpu_run(hydro, m, U0, 2)
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=DX))
+    d.set_amr_mesh(m)
+    nbytes = m.n_leaves * 6 * 512 * 8
+    hin, hout = d.host_pinned_alloc(nbytes), d.host_pinned_alloc(nbytes)
+    ctypes.memmove(hin, np.ascontiguousarray(U0[:m.n_leaves]).ctypes.data, nbytes)
+    d.step_host(hin, hout, 2)
+    out = np.empty((m.n_leaves, 6, 512))
+    ctypes.memmove(out.ctypes.data, hout, nbytes)
+    d.host_pinned_free(hin)
+    d.host_pinned_free(hout)
+    d.close()
+    assert np.array_equal(out, ref)
