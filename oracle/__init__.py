@@ -252,3 +252,31 @@ def run_amr(p: Params, mesh, U, nsteps):
     if rc != 0:
         raise MemoryError("oracle AMR run failed")
     return U, dts[:nsteps]
+
+
+def amr_reflux(p: Params, mesh, Uprev, Uout, stage_no, dt):
+    """orc_amr_reflux in place on Uout (both [n_total, nf, 512])."""
+    nbr = np.zeros((mesh.n_total, 6), np.int64) - 1
+    nbr[:mesh.n_leaves] = mesh.nbr
+    lev = np.ascontiguousarray(mesh.level, np.int32)
+    rf = np.ascontiguousarray(mesh.reflux, np.int32)
+    Uprev = np.ascontiguousarray(Uprev)
+    lib().orc_amr_reflux(ctypes.byref(p), _p(nbr, _i64p), _p(lev, _i32p), mesh.max_level, len(rf), _p(rf, _i32p),
+                         _p(Uprev, _f64p), _p(Uout, _f64p), stage_no, dt)
+    return Uout
+
+
+def amr_stage(p: Params, mesh, Uprev, Un, stage_no, dt, reflux=True):
+    """One AMR stage as orc_run_amr does it: fill proxies of Uprev (in place),
+    per-level orc_stage, then the flux correction."""
+    amr_fill(p.nf, mesh, Uprev)
+    nbr = np.zeros((mesh.n_total, 6), np.int64) - 1
+    nbr[:mesh.n_leaves] = mesh.nbr
+    out = np.zeros_like(Uprev)
+    for L in range(mesh.max_level + 1):
+        f0, f1 = int(mesh.level_first[L]), int(mesh.level_first[L + 1])
+        part = stage(p, nbr, Uprev, Un, stage_no, dt / np.ldexp(p.dx, mesh.max_level - L), f0, f1)
+        out[f0:f1] = part[f0:f1]
+    if reflux:
+        amr_reflux(p, mesh, Uprev, out, stage_no, dt)
+    return out

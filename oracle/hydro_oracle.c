@@ -681,3 +681,10 @@ int orc_run_amr(const orc_params* p, int64_t n_total, const int64_t* nbr, const 
     free(U2);
     return 0;
 }
+
+/* Diagnostics: the N+1 face fluxes F[j][f] of pencil (a, b) along `axis` of
+ * sub-grid g, exactly as orc_stage computes them. */
+void orc_debug_face_fluxes(const orc_params* p, const int64_t* nbr, const double* U, int64_t g, int axis, int a,
+                           int b, double* F) {
+    for (int j = 0; j <= N; ++j) face_flux(p, nbr, U, g, axis, a, b, j, F + (size_t)j * p->nf);
+}

@@ -114,6 +114,8 @@ void orc_amr_fill(int nf, int64_t n_proxy, const orc_amr_proxy* px, double* U);
 void orc_amr_reflux(const orc_params* p, const int64_t* nbr, const int32_t* level, int max_level,
                     int64_t n_rec, const orc_amr_reflux_rec* rf, const double* Uprev, double* Uout, int stage,
                     double dt);
+void orc_debug_face_fluxes(const orc_params* p, const int64_t* nbr, const double* U, int64_t g, int axis, int a,
+                           int b, double* F);
 /* nsteps SSP-RK3 steps on an AMR mesh, one global dt = cfl dx / amax. */
 int orc_run_amr(const orc_params* p, int64_t n_total, const int64_t* nbr, const int32_t* level,
                 const int64_t* level_first, int max_level, int64_t n_proxy, const orc_amr_proxy* px,

@@ -211,11 +211,17 @@ __global__ void selftest_math_kernel(unsigned long long n, unsigned long long se
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const uint64_t h = mix64(seed, i);
-        const int ex = (int)((h >> 52) % (2u * (unsigned)emax + 1u)) - emax;
-        const uint64_t bits = ((uint64_t)(ex + 1023) << 52) | (h & 0xFFFFFFFFFFFFFull);
+        // emax > 0: uniform mantissas, exponents in [-emax, emax]; emax < 0:
+        // mantissas within 2^-20 of 1 or 2 (the high word nearly constant,
+        // where the MUFU seeds are coarsest), exponents in [emax, -emax]
+        const int em = emax < 0 ? -emax : emax;
+        const int ex = (int)((h >> 52) % (2u * (unsigned)em + 1u)) - em;
+        uint64_t mant = h & 0xFFFFFFFFFFFFFull;
+        if (emax < 0) mant = (h >> 63) ? (mant & 0xFFFFFFFFull) : (0xFFFFFFFFFFFFFull - (mant & 0xFFFFFFFFull));
+        const uint64_t bits = ((uint64_t)(ex + 1023) << 52) | mant;
         const double x = __longlong_as_double((long long)bits);
-        if (__double_as_longlong(rcp_rn(x)) != __double_as_longlong(1.0 / x)) ++nb_rcp;
-        if (__double_as_longlong(sqrt_rn(x)) != __double_as_longlong(sqrt(x))) ++nb_sqrt;
+        if (__double_as_longlong(eos_rcp(x)) != __double_as_longlong(1.0 / x)) ++nb_rcp;
+        if (__double_as_longlong(eos_sqrt(x)) != __double_as_longlong(sqrt(x))) ++nb_sqrt;
     }
     if (nb_rcp) atomicAdd(bad, nb_rcp);
     if (nb_sqrt) atomicAdd(bad + 1, nb_sqrt);

@@ -2116,8 +2116,8 @@ int ts_hydro_selftest_math(ts_hydro_ctx* c, uint64_t n, uint64_t seed, int32_t e
     int rc = guard(c);
     if (rc) return rc;
     if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
-    if (bad_rcp == nullptr || bad_sqrt == nullptr || emax < 1 || emax > 1020)
-        return fail(c, TS_EINVAL, "emax must be in [1, 1020]");
+    if (bad_rcp == nullptr || bad_sqrt == nullptr || emax == 0 || emax > 1020 || emax < -1020)
+        return fail(c, TS_EINVAL, "emax must be in [1, 1020] (or [-1020, -1]: near-one mantissas)");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     cudaSetDevice(c->dev);
     cudaStream_t s;
