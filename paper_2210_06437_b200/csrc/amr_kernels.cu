@@ -78,28 +78,28 @@ __device__ void o_limit_slope(double* ql, double q0, double* qr) {
     }
 }
 
-// Face states of face j (0..N) of one pencil q[0..P-1] (cells -3..N+2).
-__device__ void o_face_states(int recon, const double* q, int j, double* uL, double* uR) {
-    double lo[P], hi[P];
+// Face states of face j (0..N) from the pencil window w[k] = q[j + k],
+// k = 0..5 (cells j-3 .. j+2): the oracle's reconstruct restricted to the two
+// cells either side of the face (the same per-element formulas, so the same
+// bits): uL = hi of cell j-1 (q index j+2), uR = lo of cell j (q index j+3).
+__device__ void o_face_states(int recon, const double* w, double* uL, double* uR) {
     if (recon == 0) {
-        double D[P], fc[P];
-        for (int i = 1; i <= P - 2; ++i) D[i] = o_minmod_theta(q[i + 1] - q[i], q[i] - q[i - 1], 2.0);
-        for (int i = 2; i <= P - 2; ++i) fc[i] = fma(kC16, D[i - 1] - D[i], 0.5 * (q[i - 1] + q[i]));
-        for (int i = 2; i <= P - 3; ++i) {
-            double ql = fc[i], qr = fc[i + 1];
-            o_limit_slope(&ql, q[i], &qr);
-            lo[i] = ql;
-            hi[i] = qr;
-        }
+        double D[5], fc[5];  // index k <-> oracle index j + k
+        for (int k = 1; k <= 4; ++k) D[k] = o_minmod_theta(w[k + 1] - w[k], w[k] - w[k - 1], 2.0);
+        for (int k = 2; k <= 4; ++k) fc[k] = fma(kC16, D[k - 1] - D[k], 0.5 * (w[k - 1] + w[k]));
+        double ql = fc[2], qr = fc[3];
+        o_limit_slope(&ql, w[2], &qr);
+        *uL = qr;
+        ql = fc[3];
+        qr = fc[4];
+        o_limit_slope(&ql, w[3], &qr);
+        *uR = ql;
     } else {
-        for (int i = 2; i <= P - 3; ++i) {
-            const double s = o_minmod(q[i + 1] - q[i], q[i] - q[i - 1]);
-            lo[i] = fma(-0.5, s, q[i]);
-            hi[i] = fma(0.5, s, q[i]);
-        }
+        const double sl = o_minmod(w[3] - w[2], w[2] - w[1]);
+        const double sr = o_minmod(w[4] - w[3], w[3] - w[2]);
+        *uL = fma(0.5, sl, w[2]);
+        *uR = fma(-0.5, sr, w[3]);
     }
-    *uL = hi[j + 2];
-    *uR = lo[j + 3];
 }
 
 struct FluxParams {
@@ -156,10 +156,10 @@ __device__ double o_pencil_value(int nf, const int* nbr, const double* U, int g,
 
 __device__ void o_face_flux(const FluxParams& p, const int* nbr, const double* U, int g, int axis, int a, int b,
                             int j, double* F) {
-    double q[P], sL[kMaxNf], sR[kMaxNf], fL[kMaxNf], fR[kMaxNf], aL, aR;
+    double w[6], sL[kMaxNf], sR[kMaxNf], fL[kMaxNf], fR[kMaxNf], aL, aR;
     for (int f = 0; f < p.nf; ++f) {
-        for (int s = 0; s < P; ++s) q[s] = o_pencil_value(p.nf, nbr, U, g, f, axis, a, b, s - 3);
-        o_face_states(p.recon, q, j, &sL[f], &sR[f]);
+        for (int k = 0; k < 6; ++k) w[k] = o_pencil_value(p.nf, nbr, U, g, f, axis, a, b, j + k - 3);
+        o_face_states(p.recon, w, &sL[f], &sR[f]);
     }
     o_side_flux(p, axis, sL, fL, &aL);
     o_side_flux(p, axis, sR, fR, &aR);
@@ -167,36 +167,49 @@ __device__ void o_face_flux(const FluxParams& p, const int* nbr, const double* U
     for (int k = 0; k < p.nf; ++k) F[k] = 0.5 * fma(-am, sR[k] - sL[k], fL[k] + fR[k]);
 }
 
-// One CTA per coarse sub-grid with a coarse–fine face; thread (a, b) owns one
-// face cell of each face.  Faces in order 0..5 with a barrier between them,
-// so an edge cell corrected through two faces gets the oracle's order.
-__global__ void __launch_bounds__(N* N) amr_reflux_kernel(const double* __restrict__ Uprev, double* Uout,
-                                                          FluxParams p, const int* nbr, const int* level,
-                                                          int max_level, double dx, const AmrReflux* rf,
-                                                          int stage, const double* dt_ptr) {
+// One CTA per coarse sub-grid with a coarse–fine face.  Per face (in order
+// 0..5, barrier-separated, so an edge cell corrected through two faces gets
+// the oracle's order) the 5 x 64 face fluxes — the coarse one and the 4 fine
+// ones behind each coarse face cell — are computed by 320 threads into shared
+// memory (one flux each: the work is latency-bound scalar code, so the
+// parallelism matters more than the redundancy), then the 64 face cells'
+// threads apply the correction.
+constexpr int kRefluxThreads = 5 * N * N;
+
+__global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double* __restrict__ Uprev, double* Uout,
+                                                                   FluxParams p, const int* nbr, const int* level,
+                                                                   int max_level, double dx, const AmrReflux* rf,
+                                                                   int stage, const double* dt_ptr) {
+    __shared__ double Fs[5][kMaxNf][N * N];
     const AmrReflux& r = rf[blockIdx.x];
     const int g = r.coarse;
     const double w = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
     const double dtdx = *dt_ptr / ldexp(dx, max_level - level[g]);
-    const int a = threadIdx.x & 7, b = threadIdx.x >> 3;
-    double Fc[kMaxNf], F00[kMaxNf], F10[kMaxNf], F01[kMaxNf], F11[kMaxNf];
+    const int cell = threadIdx.x & (N * N - 1), which = threadIdx.x / (N * N);  // which: 0 coarse, 1..4 fine
+    const int a = cell & 7, b = cell >> 3;
+    double F[kMaxNf];
     for (int face = 0; face < 6; ++face) {
         if (r.fine[face][0] < 0) continue;
         const int axis = face >> 1, side = face & 1;
-        const int jc = side ? N : 0, jf = side ? 0 : N, ic = side ? N - 1 : 0;
-        const int leaf = r.fine[face][(a >> 2) + 2 * (b >> 2)];
-        const int fa = 2 * (a & 3), fb = 2 * (b & 3);
-        o_face_flux(p, nbr, Uprev, g, axis, a, b, jc, Fc);
-        o_face_flux(p, nbr, Uprev, leaf, axis, fa, fb, jf, F00);
-        o_face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb, jf, F10);
-        o_face_flux(p, nbr, Uprev, leaf, axis, fa, fb + 1, jf, F01);
-        o_face_flux(p, nbr, Uprev, leaf, axis, fa + 1, fb + 1, jf, F11);
-        const int c = axis == 0 ? cidx(ic, a, b) : (axis == 1 ? cidx(a, ic, b) : cidx(a, b, ic));
-        for (int f = 0; f < p.nf; ++f) {
-            const double avg = 0.25 * ((F00[f] + F10[f]) + (F01[f] + F11[f]));
-            const double corr = side ? Fc[f] - avg : avg - Fc[f];
-            double* u = Uout + ((size_t)g * p.nf + f) * NC + c;
-            *u = *u + w * (dtdx * corr);
+        if (which == 0) {
+            o_face_flux(p, nbr, Uprev, g, axis, a, b, side ? N : 0, F);
+        } else {
+            const int q = which - 1;  // 00, 10, 01, 11
+            o_face_flux(p, nbr, Uprev, r.fine[face][(a >> 2) + 2 * (b >> 2)], axis, 2 * (a & 3) + (q & 1),
+                        2 * (b & 3) + (q >> 1), side ? 0 : N, F);
+        }
+        for (int f = 0; f < p.nf; ++f) Fs[which][f][cell] = F[f];
+        __syncthreads();
+        if (which == 0) {
+            const int ic = side ? N - 1 : 0;
+            const int c = axis == 0 ? cidx(ic, a, b) : (axis == 1 ? cidx(a, ic, b) : cidx(a, b, ic));
+            for (int f = 0; f < p.nf; ++f) {
+                const double avg = 0.25 * ((Fs[1][f][cell] + Fs[2][f][cell]) + (Fs[3][f][cell] + Fs[4][f][cell]));
+                const double Fc = Fs[0][f][cell];
+                const double corr = side ? Fc - avg : avg - Fc;
+                double* u = Uout + ((size_t)g * p.nf + f) * NC + c;
+                *u = *u + w * (dtdx * corr);
+            }
         }
         __syncthreads();
     }
@@ -228,7 +241,7 @@ cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int rec
         if (e != cudaSuccess) return e;
     }
     FluxParams p{nf, recon, gamma, p_floor};
-    amr_reflux_kernel<<<(unsigned)n, N * N, 0, s>>>(Uprev, Uout, p, nbr, level, max_level, dx, rf, stage, dt);
+    amr_reflux_kernel<<<(unsigned)n, kRefluxThreads, 0, s>>>(Uprev, Uout, p, nbr, level, max_level, dx, rf, stage, dt);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
     return e;
