@@ -246,8 +246,8 @@ int ts_hydro_halo_exchange(ts_hydro_ctx* ctx);
 /* Diagnostic: bitwise check of the kernels' branch-free reciprocal and square
  * root against IEEE 1.0/x and sqrt(x) on n random positive doubles with
  * binary exponents in [-emax, emax]; emax < 0 draws mantissas within 2^-20
- * of 1 or 2 instead (exponents in [emax, -emax]).  Returns the mismatch
- * counts. */
+ * of 1 or 2 instead, 1 in 64 exactly all-ones (exponents in [emax, -emax]).
+ * Returns the mismatch counts. */
 int ts_hydro_selftest_math(ts_hydro_ctx* ctx, uint64_t n, uint64_t seed, int32_t emax, uint64_t* bad_rcp,
                            uint64_t* bad_sqrt);
 
