@@ -16,7 +16,9 @@ into what ``ts_hydro_set_amr_mesh`` (include/ts_hydro.h) binds:
 * the reflux records: per coarse leaf with a refined face neighbour, the 4
   fine leaves behind each such face, by transverse quadrant.
 
-The mesh must be 2:1 balanced across faces (a ``ValueError`` otherwise).
+The mesh must be 2:1 balanced across faces (a ``ValueError`` otherwise);
+children of a refined neighbour position that do not touch the face may be
+refined further.
 """
 from __future__ import annotations
 
@@ -136,13 +138,20 @@ def amr_mesh(nx: int, ny: int, nz: int,
                 nbr[i, f] = proxy_of[key]
                 continue
             kids = children(L, q)
-            if all(k in index for k in kids):
+            axis, side = f >> 1, f & 1
+            near = [k for o, k in enumerate(kids) if ((o >> axis) & 1) == (0 if side == 1 else 1)]
+            if all(k in index for k in near):
                 key = (1, L, q)
                 if key not in proxy_of:
+                    # children away from this face may be refined further (2:1
+                    # holds across faces); the stage kernel reads only the 3
+                    # coarse layers next to the face, i.e. the near children,
+                    # so a non-leaf child's octant is filled from any leaf child
+                    # (never read)
+                    first_leaf = next(index[k] for k in kids if k in index)
                     proxy_of[key] = n + len(proxies)
-                    proxies.append([proxy_of[key], 1, 0] + [index[k] for k in kids])
+                    proxies.append([proxy_of[key], 1, 0] + [index.get(k, first_leaf) for k in kids])
                 nbr[i, f] = proxy_of[key]
-                axis, side = f >> 1, f & 1
                 ta, tb = transverse_axes(axis)
                 rec = reflux.setdefault(i, [[-1] * 4 for _ in range(6)])
                 for qa in range(2):

@@ -126,6 +126,28 @@ def test_reflux_conserves_to_round_off(oracle_lib, dims, refine, centre, recon):
     assert leak.min() > 1e-8, leak
 
 
+# three levels: a refined 2^3 level-0 block with its central 2^3 level-1
+# positions refined again (restrictions with further-refined far children)
+def THREE_LEVELS(L, p):
+    return (L == 0 and all(1 <= v <= 2 for v in p)) or (L == 1 and all(3 <= v <= 4 for v in p))
+
+
+def test_three_level_mesh_conserves_and_keeps_free_stream(oracle_lib):
+    m = amr.amr_mesh(4, 4, 4, THREE_LEVELS, max_level=2)
+    assert m.max_level == 2 and list(np.diff(m.level_first)) == [56, 56, 64]
+    dx = DX / 2
+    vol = m.cell_volumes(dx)
+    p = oracle_lib.params(nf=6, dx=dx)
+    U0 = amr.ic_blast(m, 6, dx, width=0.05, centre=(0.5, 0.5, 0.5))
+    t = lambda U: np.array([(U[:m.n_leaves, f].sum(axis=1) * vol).sum() for f in range(5)])  # noqa: E731
+    U, _ = oracle_lib.run_amr(p, m, U0, 3)
+    assert (np.abs(t(U) - t(U0)) / np.abs(t(U0)).max()).max() < 1e-14
+    U0 = amr.ic_blast(m, 6, dx, amp=0.0, drift=(0.5, -0.25, 0.125))
+    U, _ = oracle_lib.run_amr(p, m, U0, 2)
+    for f in range(6):
+        assert (U[:m.n_leaves, f] == U0[0, f, 0]).all(), f
+
+
 def test_uniform_flow_stays_uniform_across_levels(oracle_lib):
     """Free-stream preservation: prolongation, restriction and reflux of a
     uniform state are exact, so every cell keeps its bits."""

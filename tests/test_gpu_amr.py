@@ -56,6 +56,27 @@ def test_amr_steps_match_oracle_bitwise(hydro, oracle_lib, recon, species, case)
     assert check(U, ref, m.n_leaves), "AMR path is not bitwise equal to the oracle"
 
 
+@pytest.mark.parametrize("recon", [0, 1], ids=["ppm", "minmod"])
+def test_three_level_amr_matches_oracle_bitwise(hydro, oracle_lib, recon):
+    """Levels 0-2 (three stage launches per stage, restrictions whose far
+    children are refined further), 3 steps."""
+    ref = lambda L, p: (L == 0 and all(1 <= v <= 2 for v in p)) or (L == 1 and all(3 <= v <= 4 for v in p))  # noqa
+    m = amr.amr_mesh(4, 4, 4, ref, max_level=2)
+    dx = DX / 2
+    U0 = amr.ic_blast(m, 6, dx, width=0.06, centre=(0.45, 0.5, 0.55), drift=(0.2, 0.1, -0.3))
+    p = oracle_lib.params(nf=6, recon=recon, dx=dx)
+    ref_U, dts = oracle_lib.run_amr(p, m, U0, 3)
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=dx, recon=("ppm", "minmod")[recon]))
+    d.set_amr_mesh(m)
+    d.upload(U0[:m.n_leaves])
+    d.step(3)
+    d.synchronize()
+    U = d.download()
+    assert d.last_dt() == dts[-1]
+    d.close()
+    assert check(U, ref_U, m.n_leaves)
+
+
 def test_amr_reflux_conserves_on_gpu(hydro, oracle_lib):
     m = amr.amr_mesh(6, 6, 6, CENTRE_BLOCK6)
     U0 = amr.ic_blast(m, 6, DX, width=0.04, centre=(1.0, 0.75, 0.75))
