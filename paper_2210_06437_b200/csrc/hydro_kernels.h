@@ -106,6 +106,13 @@ struct StageArgs {
     // sets dt) on a uniform mesh, dx * 2^(max_level - level) for one level of
     // an AMR mesh (launched per level, ts_hydro_set_amr_mesh)
     double dx_upd;
+    // AMR, all levels in one launch: sub-grid g (level-major) is updated
+    // with lvl_dx[L] for the last L < lvl_n with g >= lvl_first[L]
+    // (lvl_n = 0: dx_upd for every CTA)
+    static constexpr int kMaxLevels = 8;
+    int lvl_n;
+    int lvl_first[kMaxLevels];
+    double lvl_dx[kMaxLevels];
 };
 
 // Coarse–fine AMR (amr_kernels.cu): proxy fill recipe and reflux record,

@@ -689,6 +689,15 @@ __device__ __forceinline__ void halo_push(const StageArgs& A, size_t own, int b)
     }
 }
 
+// dx of sub-grid g's level (StageArgs::lvl_*); uniform launches: dx_upd
+__device__ __forceinline__ double level_dx(const StageArgs& A, int g) {
+    double dx = A.dx_upd;
+#pragma unroll
+    for (int L = 1; L < StageArgs::kMaxLevels; ++L)
+        if (L < A.lvl_n && g >= A.lvl_first[L]) dx = A.lvl_dx[L];
+    return dx;
+}
+
 template <int NF, int RECON, int STAGE>
 __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(StageArgs A) {
     extern __shared__ double smem[];
@@ -743,7 +752,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         __syncthreads();
         amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
     }
-    const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / A.dx_upd);
+    const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / level_dx(A, g));
     if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
         if (A.dt_out != nullptr) *A.dt_out = (A.cfl * A.dx) / amax_in;
         if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
@@ -786,7 +795,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                 amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
             }
             const double dt = (A.cfl * A.dx) / amax_in;
-            c.dtdx = 0.5 * (dt / A.dx_upd);  // the sweeps carry twice the KT flux (kt2)
+            c.dtdx = 0.5 * (dt / level_dx(A, g));  // the sweeps carry twice the KT flux (kt2)
             if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
                 if (A.dt_out != nullptr) *A.dt_out = dt;
                 if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;

@@ -199,6 +199,7 @@ struct ts_hydro_ctx {
     static constexpr int kXferChunksMax = 64;
     int xfer_chunks = 8;  // TS_HYDRO_XFER_CHUNKS
     bool chunk_overlap = true;  // TS_HYDRO_CHUNK_OVERLAP=0: D2H waits for the whole last stage
+    bool amr_fused = true;      // TS_HYDRO_AMR_SPLIT=1: one stage launch per AMR level
     cudaEvent_t ev_d2h[kXferChunksMax] = {};
     cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr;
     const void* prev_out = nullptr;
@@ -818,9 +819,12 @@ int do_compute_dt(ts_hydro_ctx* c) {
 }
 
 // One step on an AMR mesh (single rank, stream order): per stage, refill the
-// proxies of U^(k-1) (prolongation / restriction), one stage launch per
-// level (its own dx; the first launch of stage 1 writes dt and zeroes the
-// max slot stage 3 accumulates into), then the coarse flux correction.
+// proxies of U^(k-1) (prolongation / restriction), the stage over all leaves
+// (one launch; each CTA takes its level's dx from StageArgs::lvl_*, so the
+// level-0 launch's tail no longer idles the GPU before the level-1 launch;
+// TS_HYDRO_AMR_SPLIT=1 or > kMaxLevels levels: one launch per level, the
+// first of stage 1 writing dt and zeroing the max slot stage 3 accumulates
+// into), then the coarse flux correction.
 int do_step_amr(ts_hydro_ctx* c) {
     cudaStream_t s;
     int rc = ensure_stream(c, 0, &s);
@@ -835,8 +839,24 @@ int do_step_amr(ts_hydro_ctx* c) {
             TS_CUDA(c, tsh::launch_amr_fill(const_cast<double*>(a.Uprev), c->nf, c->d_amr_proxy, c->amr_n_proxy,
                                             stamp, s));
         }
+        if (c->amr_fused && c->amr_max_level < tsh::StageArgs::kMaxLevels) {
+            tsh::StageArgs b = a;
+            b.lvl_n = c->amr_max_level + 1;
+            for (int L = 0; L <= c->amr_max_level; ++L) {
+                b.lvl_first[L] = (int)c->amr_level_first[(size_t)L];
+                b.lvl_dx[L] = std::ldexp(c->cfg.dx, c->amr_max_level - L);
+            }
+            b.dx_upd = b.lvl_dx[0];
+            if (stage == 1) {
+                b.amax_reset = amax_slot(c, c->steps_done + 1);
+                b.dt_out = const_cast<double*>(dt_ptr);
+            }
+            rc = launch_stage_list(c, b, stage, nullptr, c->n_owned, 0, 0, 0);
+            if (rc) return rc;
+        }
         bool first = true;
-        for (int L = 0; L <= c->amr_max_level; ++L) {
+        for (int L = 0; L <= c->amr_max_level && !(c->amr_fused && c->amr_max_level < tsh::StageArgs::kMaxLevels);
+             ++L) {
             const int64_t f0 = c->amr_level_first[(size_t)L], n = c->amr_level_first[(size_t)L + 1] - f0;
             if (n <= 0) continue;
             tsh::StageArgs b = a;
@@ -1130,6 +1150,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_FLOW_STEPS")) c->flow_steps = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
         c->xfer_chunks = std::max(1, std::min(ts_hydro_ctx::kXferChunksMax, std::atoi(w)));
     if (const char* w = std::getenv("TS_HYDRO_WAIT_TIMEOUT_MS")) c->wait_ns = 1000000ull * std::strtoull(w, nullptr, 10);

@@ -56,10 +56,14 @@ def test_amr_steps_match_oracle_bitwise(hydro, oracle_lib, recon, species, case)
     assert check(U, ref, m.n_leaves), "AMR path is not bitwise equal to the oracle"
 
 
+@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
 @pytest.mark.parametrize("recon", [0, 1], ids=["ppm", "minmod"])
-def test_three_level_amr_matches_oracle_bitwise(hydro, oracle_lib, recon):
-    """Levels 0-2 (three stage launches per stage, restrictions whose far
-    children are refined further), 3 steps."""
+def test_three_level_amr_matches_oracle_bitwise(hydro, oracle_lib, recon, split, monkeypatch):
+    """Levels 0-2 (restrictions whose far children are refined further), 3
+    steps; one stage launch over all levels (default) and one per level
+    (TS_HYDRO_AMR_SPLIT=1)."""
+    if split:
+        monkeypatch.setenv("TS_HYDRO_AMR_SPLIT", "1")
     ref = lambda L, p: (L == 0 and all(1 <= v <= 2 for v in p)) or (L == 1 and all(3 <= v <= 4 for v in p))  # noqa
     m = amr.amr_mesh(4, 4, 4, ref, max_level=2)
     dx = DX / 2
@@ -113,15 +117,20 @@ def test_amr_medium_mesh_matches_oracle(hydro, oracle_lib):
     assert check(U, ref, m.n_leaves)
 
 
-def test_amr_activity_records_and_refusals(hydro, tmp_path):
+def test_amr_activity_records_and_refusals(hydro, tmp_path, monkeypatch):
     m = amr.amr_mesh(4, 4, 4, L_SHAPE)
     U0 = amr.ic_blast(m, 6, DX)
     _, _, recs = gpu_run(hydro, m, U0, 2)
     names = [r.name for r in recs]
-    # per step: 3 x (fill + one stage launch per level + reflux)
+    # per step: 3 x (fill + one stage launch over both levels + reflux)
     assert names.count("amr_ghost_fill_kernel") == 6
     assert names.count("amr_reflux_kernel") == 6
-    assert sum(n.startswith("hydro_stage") for n in names) == 12
+    assert sum(n.startswith("hydro_stage") for n in names) == 6
+    monkeypatch.setenv("TS_HYDRO_AMR_SPLIT", "1")
+    _, _, recs = gpu_run(hydro, m, U0, 2)
+    # split: one stage launch per level
+    assert sum(r.name.startswith("hydro_stage") for r in recs) == 12
+    monkeypatch.delenv("TS_HYDRO_AMR_SPLIT")
     for r in recs:
         assert r.start_ns <= r.end_ns
     d = hydro.CudaDevice(hydro.HydroConfig(dx=DX))
