@@ -23,10 +23,19 @@ namespace {
 
 __device__ __forceinline__ int cidx(int x, int y, int z) { return (z * N + y) * N + x; }
 
-__global__ void __launch_bounds__(NC) amr_fill_kernel(double* __restrict__ U, int nf, const AmrProxy* px) {
+__global__ void __launch_bounds__(NC) amr_fill_kernel(double* __restrict__ U, int nf, const AmrProxy* px,
+                                                       const unsigned char* __restrict__ face_mask) {
     const AmrProxy& r = px[blockIdx.x];
     const int c = threadIdx.x;
     const int x = c & 7, y = (c >> 3) & 7, z = c >> 6;
+    if (face_mask != nullptr) {
+        // only the H = 3 layers next to a face some sub-grid reads through
+        constexpr int H = 3;
+        const unsigned m = face_mask[blockIdx.x];
+        const bool read = ((m & 1u) && x < H) || ((m & 2u) && x >= N - H) || ((m & 4u) && y < H) ||
+                          ((m & 8u) && y >= N - H) || ((m & 16u) && z < H) || ((m & 32u) && z >= N - H);
+        if (!read) return;
+    }
     double* dst = U + (size_t)r.dst * nf * NC + c;
     if (r.kind == 0) {
         const int cc = cidx((r.octant & 1) * 4 + x / 2, ((r.octant >> 1) & 1) * 4 + y / 2,
@@ -217,14 +226,14 @@ __global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double
 
 }  // namespace
 
-cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, long long n, unsigned long long* stamp,
-                            cudaStream_t s) {
+cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, const unsigned char* face_mask, long long n,
+                            unsigned long long* stamp, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     if (stamp != nullptr) {
         cudaError_t e = launch_stamp(stamp, 0, s);
         if (e != cudaSuccess) return e;
     }
-    amr_fill_kernel<<<(unsigned)n, NC, 0, s>>>(U, nf, px);
+    amr_fill_kernel<<<(unsigned)n, NC, 0, s>>>(U, nf, px, face_mask);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
     return e;

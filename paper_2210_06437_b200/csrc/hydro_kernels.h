@@ -150,8 +150,11 @@ cudaError_t launch_dt_exchange(const double* local_amax, double* const* push_gat
                                unsigned long long wait_ns, cudaStream_t s);
 cudaError_t launch_wait_flags(const unsigned int* flags, unsigned long long mask, unsigned int seq,
                               unsigned long long* err, unsigned long long wait_ns, cudaStream_t s);
-cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, long long n, unsigned long long* stamp,
-                            cudaStream_t s);
+// face_mask[p] (nullable: whole proxies): bit f set when some sub-grid reads
+// proxy p through p's face f; only the 3 cell layers next to those faces are
+// filled (the stage and reflux kernels read nothing else of a proxy)
+cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, const unsigned char* face_mask, long long n,
+                            unsigned long long* stamp, cudaStream_t s);
 cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int recon, double gamma, double p_floor,
                               const int* nbr, const int* level, int max_level, double dx, const AmrReflux* rf,
                               long long n, int stage, const double* dt, unsigned long long* stamp,

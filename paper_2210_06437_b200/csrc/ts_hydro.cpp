@@ -289,6 +289,8 @@ struct ts_hydro_ctx {
     std::vector<int64_t> amr_level_first;  // [max_level + 2]
     int64_t amr_n_proxy = 0, amr_n_rec = 0;
     tsh::AmrProxy* d_amr_proxy = nullptr;
+    unsigned char* d_amr_pmask = nullptr;  // per proxy: faces read (launch_amr_fill)
+    bool amr_slab_fill = true;             // TS_HYDRO_AMR_FULLFILL=1: fill whole proxies
     tsh::AmrReflux* d_amr_rec = nullptr;
     int32_t* d_amr_level = nullptr;
 
@@ -440,6 +442,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_send);
     dfree(c, &c->d_recv);
     dfree(c, &c->d_amr_proxy);
+    dfree(c, &c->d_amr_pmask);
     dfree(c, &c->d_amr_rec);
     dfree(c, &c->d_amr_level);
     c->amr = false;
@@ -836,7 +839,8 @@ int do_step_amr(ts_hydro_ctx* c) {
         if (c->amr_n_proxy > 0) {
             rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrFill, 0, 0, &stamp);
             if (rc) return rc;
-            TS_CUDA(c, tsh::launch_amr_fill(const_cast<double*>(a.Uprev), c->nf, c->d_amr_proxy, c->amr_n_proxy,
+            TS_CUDA(c, tsh::launch_amr_fill(const_cast<double*>(a.Uprev), c->nf, c->d_amr_proxy,
+                                            c->amr_slab_fill ? c->d_amr_pmask : nullptr, c->amr_n_proxy,
                                             stamp, s));
         }
         if (c->amr_fused && c->amr_max_level < tsh::StageArgs::kMaxLevels) {
@@ -1151,6 +1155,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_AMR_FULLFILL")) c->amr_slab_fill = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
         c->xfer_chunks = std::max(1, std::min(ts_hydro_ctx::kXferChunksMax, std::atoi(w)));
     if (const char* w = std::getenv("TS_HYDRO_WAIT_TIMEOUT_MS")) c->wait_ns = 1000000ull * std::strtoull(w, nullptr, 10);
@@ -1616,11 +1621,21 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
     c->amr_n_rec = nr;
     if (!c->host_only) {
         rc = dalloc(c, &c->d_amr_proxy, (size_t)std::max<int64_t>(np, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_pmask, (size_t)std::max<int64_t>(np, 1));
         if (!rc) rc = dalloc(c, &c->d_amr_rec, (size_t)std::max<int64_t>(nr, 1));
         if (!rc) rc = dalloc(c, &c->d_amr_level, (size_t)nl);
         if (rc) return rc;
-        if (np > 0)
+        if (np > 0) {
             TS_CUDA(c, cudaMemcpy(c->d_amr_proxy, px, (size_t)np * sizeof(tsh::AmrProxy), cudaMemcpyHostToDevice));
+            // leaf g reads proxy p = nbr[g][f] through p's face f ^ 1
+            std::vector<unsigned char> pm((size_t)np, 0);
+            for (int64_t g = 0; g < nl; ++g)
+                for (int f = 0; f < 6; ++f) {
+                    const int64_t h = nbr[6 * g + f];
+                    if (h >= nl) pm[(size_t)(h - nl)] |= (unsigned char)(1u << (f ^ 1));
+                }
+            TS_CUDA(c, cudaMemcpy(c->d_amr_pmask, pm.data(), (size_t)np, cudaMemcpyHostToDevice));
+        }
         if (nr > 0)
             TS_CUDA(c, cudaMemcpy(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaMemcpy(c->d_amr_level, level, (size_t)nl * sizeof(int32_t), cudaMemcpyHostToDevice));

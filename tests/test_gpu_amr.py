@@ -56,14 +56,17 @@ def test_amr_steps_match_oracle_bitwise(hydro, oracle_lib, recon, species, case)
     assert check(U, ref, m.n_leaves), "AMR path is not bitwise equal to the oracle"
 
 
-@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+@pytest.mark.parametrize("mode", ["default", "split", "fullfill"])
 @pytest.mark.parametrize("recon", [0, 1], ids=["ppm", "minmod"])
-def test_three_level_amr_matches_oracle_bitwise(hydro, oracle_lib, recon, split, monkeypatch):
+def test_three_level_amr_matches_oracle_bitwise(hydro, oracle_lib, recon, mode, monkeypatch):
     """Levels 0-2 (restrictions whose far children are refined further), 3
-    steps; one stage launch over all levels (default) and one per level
-    (TS_HYDRO_AMR_SPLIT=1)."""
-    if split:
+    steps; one stage launch over all levels and proxies filled only in the
+    face layers read (default), one stage launch per level
+    (TS_HYDRO_AMR_SPLIT=1), whole proxies filled (TS_HYDRO_AMR_FULLFILL=1)."""
+    if mode == "split":
         monkeypatch.setenv("TS_HYDRO_AMR_SPLIT", "1")
+    if mode == "fullfill":
+        monkeypatch.setenv("TS_HYDRO_AMR_FULLFILL", "1")
     ref = lambda L, p: (L == 0 and all(1 <= v <= 2 for v in p)) or (L == 1 and all(3 <= v <= 4 for v in p))  # noqa
     m = amr.amr_mesh(4, 4, 4, ref, max_level=2)
     dx = DX / 2
