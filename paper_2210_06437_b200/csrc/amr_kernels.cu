@@ -23,19 +23,41 @@ namespace {
 
 __device__ __forceinline__ int cidx(int x, int y, int z) { return (z * N + y) * N + x; }
 
+// Activity stamps in the kernel itself (as the stage kernel does): start
+// stored inverted, both ends by atomicMax into the zeroed ring slot — no
+// stamp launches around the kernel.
+__device__ __forceinline__ void stamp_begin(unsigned long long* stamp) {
+    if (stamp != nullptr && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
+}
+__device__ __forceinline__ void stamp_end(unsigned long long* stamp) {
+    if (stamp != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(stamp + 1, globaltimer());
+    }
+}
+
+__device__ __forceinline__ void fill_cells(double* __restrict__ U, int nf, const AmrProxy& r, int c);
+
 __global__ void __launch_bounds__(NC) amr_fill_kernel(double* __restrict__ U, int nf, const AmrProxy* px,
-                                                       const unsigned char* __restrict__ face_mask) {
-    const AmrProxy& r = px[blockIdx.x];
+                                                       const unsigned char* __restrict__ face_mask,
+                                                       unsigned long long* stamp) {
+    stamp_begin(stamp);
     const int c = threadIdx.x;
     const int x = c & 7, y = (c >> 3) & 7, z = c >> 6;
+    bool read = true;
     if (face_mask != nullptr) {
         // only the H = 3 layers next to a face some sub-grid reads through
         constexpr int H = 3;
         const unsigned m = face_mask[blockIdx.x];
-        const bool read = ((m & 1u) && x < H) || ((m & 2u) && x >= N - H) || ((m & 4u) && y < H) ||
-                          ((m & 8u) && y >= N - H) || ((m & 16u) && z < H) || ((m & 32u) && z >= N - H);
-        if (!read) return;
+        read = ((m & 1u) && x < H) || ((m & 2u) && x >= N - H) || ((m & 4u) && y < H) ||
+               ((m & 8u) && y >= N - H) || ((m & 16u) && z < H) || ((m & 32u) && z >= N - H);
     }
+    if (read) fill_cells(U, nf, px[blockIdx.x], c);
+    stamp_end(stamp);
+}
+
+__device__ __forceinline__ void fill_cells(double* __restrict__ U, int nf, const AmrProxy& r, int c) {
+    const int x = c & 7, y = (c >> 3) & 7, z = c >> 6;
     double* dst = U + (size_t)r.dst * nf * NC + c;
     if (r.kind == 0) {
         const int cc = cidx((r.octant & 1) * 4 + x / 2, ((r.octant >> 1) & 1) * 4 + y / 2,
@@ -188,7 +210,9 @@ constexpr int kRefluxThreads = 5 * N * N;
 __global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double* __restrict__ Uprev, double* Uout,
                                                                    FluxParams p, const int* nbr, const int* level,
                                                                    int max_level, double dx, const AmrReflux* rf,
-                                                                   int stage, const double* dt_ptr) {
+                                                                   int stage, const double* dt_ptr,
+                                                                   unsigned long long* stamp) {
+    stamp_begin(stamp);
     __shared__ double Fs[5][kMaxNf][N * N];
     const AmrReflux& r = rf[blockIdx.x];
     const int g = r.coarse;
@@ -222,6 +246,7 @@ __global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double
         }
         __syncthreads();
     }
+    stamp_end(stamp);
 }
 
 }  // namespace
@@ -229,14 +254,8 @@ __global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double
 cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, const unsigned char* face_mask, long long n,
                             unsigned long long* stamp, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    if (stamp != nullptr) {
-        cudaError_t e = launch_stamp(stamp, 0, s);
-        if (e != cudaSuccess) return e;
-    }
-    amr_fill_kernel<<<(unsigned)n, NC, 0, s>>>(U, nf, px, face_mask);
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
-    return e;
+    amr_fill_kernel<<<(unsigned)n, NC, 0, s>>>(U, nf, px, face_mask, stamp);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int recon, double gamma, double p_floor,
@@ -245,15 +264,10 @@ cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int rec
                               cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     if (nf > kMaxNf) return cudaErrorInvalidValue;
-    if (stamp != nullptr) {
-        cudaError_t e = launch_stamp(stamp, 0, s);
-        if (e != cudaSuccess) return e;
-    }
     FluxParams p{nf, recon, gamma, p_floor};
-    amr_reflux_kernel<<<(unsigned)n, kRefluxThreads, 0, s>>>(Uprev, Uout, p, nbr, level, max_level, dx, rf, stage, dt);
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && stamp != nullptr) e = launch_stamp(stamp, 1, s);
-    return e;
+    amr_reflux_kernel<<<(unsigned)n, kRefluxThreads, 0, s>>>(Uprev, Uout, p, nbr, level, max_level, dx, rf, stage, dt,
+                                                            stamp);
+    return cudaGetLastError();
 }
 
 }  // namespace tsh
