@@ -140,7 +140,9 @@ int ts_hydro_set_mesh(ts_hydro_ctx* ctx, int64_t n_grids, const int64_t* neighbo
  * leaf set (single rank) whose cross-level face neighbours are proxy
  * sub-grids: ids n_leaves .. n_leaves+n_proxy-1, refilled before every RK
  * stage by prolongation (piecewise constant) from a coarse leaf or
- * restriction (2x2x2 mean) from 8 fine leaves; after every stage the coarse
+ * restriction (2x2x2 mean) from 8 fine leaves — only the 3 cell layers next
+ * to the faces leaves read them through (the rest of a proxy is unspecified;
+ * env TS_HYDRO_AMR_FULLFILL=1 fills whole proxies); after every stage the coarse
  * cells on a coarse-fine face take the mean of the 4 fine face fluxes
  * (reflux), so mass, momentum and energy stay conserved to round-off.
  * Leaves are level-major: level[] non-decreasing, 0..max_level; cfg.dx is
