@@ -16,7 +16,8 @@ rank) with cross-GPU halos pushed over NVLink by the stage kernel itself.  `--wo
 
 `--impl reference` times the CPU path of the reference's algorithm (the
 oracle port in oracle/, all host threads; the reference itself ships no hydro
-arithmetic) on a bounded sample of the same workload.
+arithmetic) on the same mesh and initial state, a bounded number of steps; it
+imports nothing of the product (mesh and initial models from the oracle).
 """
 from __future__ import annotations
 
@@ -115,35 +116,45 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(workload: str, steps: int, warmup: int, target_s: float = 0.0, recon: str = "ppm"):
-    """The oracle (CPU restatement of the path) on a bounded sample: an 8^3
-    sub-grid piece of the same workload, all host threads."""
+def cpu_reference(workload: str, steps: int, warmup: int, world: int = 1, budget_s: float = 120.0,
+                  recon: str = "ppm"):
+    """The oracle (plain-C restatement of the path, oracle/hydro_oracle.c) on
+    the SAME mesh and initial state as the GPU arm, all host threads.  Imports
+    nothing of the product: mesh and initial models come from the oracle.
+    Timing scope as run_benchmark (workload.cpp:595-612): the stepping only,
+    one orc_run call over the timed steps.  Bounded: one untimed warm-up step,
+    then min(steps, what fits in budget_s) timed steps."""
     import oracle
     oracle.build()
     edge, species, problem = WORKLOADS[workload]
     nf = 6 + species
-    dx = 1.0 / ((edge or BINARY_DIMS[0]) * 8)
-    n = 8
+    dims = BINARY_DIMS if edge is None else (edge, edge, edge * world)
+    dx = 1.0 / (dims[0] * 8)
     p = oracle.params(nf=nf, dx=dx, recon={"ppm": 0, "minmod": 1}[recon])
-    nbr, pos, _ = oracle.uniform_mesh(n, n, n)
-    from paper_2210_06437_b200 import hydro as H
-    mesh = H.Mesh(nbr, pos, np.zeros(len(pos), np.int32), 1, (n, n, n))
-    prob = "random" if problem == "random_device" else problem
-    U = H.ic_fill(H.HydroConfig(dx=dx, n_species=species), prob, mesh, np.arange(mesh.n))
+    nbr, pos, _ = oracle.uniform_mesh(*dims)
+    n = len(pos)
+    if problem == "sedov":
+        U = oracle.ic_sedov(p, pos, dims)
+    elif problem == "polytrope":
+        U = oracle.ic_polytrope(p, pos, dims)
+    elif problem == "binary":
+        U = oracle.ic_binary(p, pos, dims)
+    else:  # random_device: the reference generator cell_value
+        U = oracle.ic_random(p, 0, n, 2210)
     threads = os.cpu_count() or 1
-    for _ in range(warmup):
-        U, _ = oracle.run(p, nbr, U, 1, nthreads=threads)
-    done, t0 = 0, time.perf_counter()
-    while done < steps or (time.perf_counter() - t0) < target_s:
-        U, _ = oracle.run(p, nbr, U, 1, nthreads=threads)
-        done += 1
-        if done >= 200:
-            break
+    t0 = time.perf_counter()
+    U, _ = oracle.run(p, nbr, U, max(1, min(warmup, 1)), nthreads=threads)
+    t_step = time.perf_counter() - t0
+    k = int(max(1, min(steps, budget_s // max(t_step, 1e-9))))
+    t0 = time.perf_counter()
+    U, _ = oracle.run(p, nbr, U, k, nthreads=threads)
     sec = time.perf_counter() - t0
-    cells = mesh.n * 512
-    return {"value": cells * done / sec, "unit": "cell-updates/s", "cores": threads, "kind": "port",
-            "sample": f"{n}^3 = {mesh.n} sub-grids of the {workload} workload ({cells} cells), {done} SSP-RK3 steps, "
-                      f"{threads} threads, oracle/hydro_oracle.c", "seconds": sec, "steps": done}
+    cells = n * 512
+    return {"value": cells * k / sec, "unit": "cell-updates/s", "cores": threads, "kind": "port",
+            "sample": f"the full {workload} mesh of the GPU arm ({dims[0]}x{dims[1]}x{dims[2]} = {n} sub-grids, "
+                      f"{cells} cells, nf {nf}), {k} timed SSP-RK3 steps after 1 warm-up step, {threads} threads, "
+                      f"oracle/hydro_oracle.c (orc_run)",
+            "seconds": sec, "steps": k, "dims": list(dims)}
 
 
 def main(argv=None):
@@ -172,11 +183,18 @@ def main(argv=None):
     if a.impl == "reference":
         if rank != 0:
             return 0
-        cb = cpu_reference(a.workload, a.steps, a.warmup, recon=a.recon)
-        line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": a.gpus, "steps": cb["steps"],
-                "warmup": a.warmup, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": {"workload": f"{a.workload} (bounded CPU sample)", "recon": a.recon, "nf": nf},
+        cb = cpu_reference(a.workload, a.steps, a.warmup, world=world, recon=a.recon)
+        d = cb["dims"]
+        line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": world, "steps": cb["steps"],
+                "warmup": 1, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
+                "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference",
+                "config": {"workload": f"{a.workload}: {sub_per_gpu} sub-grids (8^3 + 3-deep halo) per GPU, "
+                                       f"domain {d[0]}x{d[1]}x{d[2]} sub-grids",
+                           "problem": problem, "nf": nf, "recon": a.recon, "total_cells": d[0] * d[1] * d[2] * 512,
+                           "same_config": True,
+                           "timed": "CPU oracle on the host cores, rank 0 only (the reference ships no hydro "
+                                    "arithmetic: its kernels are timed sleeps, workload.cpp:544-552)"},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -343,7 +361,7 @@ def main(argv=None):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cb = cpu_reference(a.workload, 2, 1, target_s=10.0, recon=a.recon)
+        cb = cpu_reference(a.workload, 20, 1, world=1, budget_s=15.0, recon=a.recon)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:

@@ -18,6 +18,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -104,6 +106,34 @@ public:
     }
     void device_free(std::uint64_t handle) { check(ts_hydro_device_free(ctx_, handle), "device_free"); }
 
+    // SimDevice::host_pinned_alloc/free (device.hpp:64-65): handle-based like
+    // the reference (handles from 1, device.cpp:171-212); the pinned memory
+    // itself is reachable through host_pinned_ptr.
+    std::uint64_t host_pinned_alloc(std::uint64_t bytes) {
+        void* p = nullptr;
+        check(ts_hydro_host_alloc(ctx_, bytes, &p), "host_pinned_alloc");
+        std::lock_guard<std::mutex> lk(pinned_mu_);
+        const std::uint64_t h = next_pinned_++;
+        pinned_[h] = p;
+        return h;
+    }
+    void host_pinned_free(std::uint64_t handle) {
+        void* p = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(pinned_mu_);
+            auto it = pinned_.find(handle);
+            if (it == pinned_.end()) throw std::invalid_argument("host_pinned_free: unknown host pinned handle");
+            p = it->second;
+            pinned_.erase(it);
+        }
+        check(ts_hydro_host_free(ctx_, p), "host_pinned_free");
+    }
+    void* host_pinned_ptr(std::uint64_t handle) const {
+        std::lock_guard<std::mutex> lk(pinned_mu_);
+        auto it = pinned_.find(handle);
+        return it == pinned_.end() ? nullptr : it->second;
+    }
+
     // SimDevice::flush_activity(Profiler&): at-most-once, RunClock timestamps.
     std::uint64_t flush_activity(Profiler& sink) {
         std::uint64_t n = 0;
@@ -128,6 +158,10 @@ public:
         }
         return n;
     }
+
+    // SimDevice::flush_activity() (device.hpp:76-77): to the default sink given
+    // at construction; without one the records stay buffered (returns 0).
+    std::uint64_t flush_activity() { return sink_ != nullptr ? flush_activity(*sink_) : 0; }
 
     DeviceMemoryState memory_state() const {
         ts_memory_state m{};
@@ -155,6 +189,9 @@ private:
 
     ts_hydro_ctx* ctx_ = nullptr;
     Profiler* sink_ = nullptr;
+    mutable std::mutex pinned_mu_;
+    std::map<std::uint64_t, void*> pinned_;
+    std::uint64_t next_pinned_ = 1;
 };
 
 }  // namespace taskscope

@@ -89,6 +89,11 @@ def lib():
                                    ctypes.c_int, ctypes.c_int, _f64p]
         L.orc_ic_random.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_uint64, _f64p]
+        L.orc_ic_polytrope.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i32p, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, _f64p]
+        L.orc_ic_binary.restype = ctypes.c_int
+        L.orc_ic_binary.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i32p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, _f64p]
         L.orc_amr_fill.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _f64p]
         L.orc_amr_reflux.argtypes = [ctypes.POINTER(Params), _i64p, _i32p, ctypes.c_int, ctypes.c_int64, _i32p,
                                      _f64p, _f64p, ctypes.c_int, ctypes.c_double]
@@ -161,6 +166,21 @@ def ic_sedov(p: Params, pos, dims):
 def ic_random(p: Params, g_begin, g_end, seed=2210):
     U = np.zeros((g_end - g_begin, p.nf, NC), np.float64)
     lib().orc_ic_random(ctypes.byref(p), g_begin, g_end, seed, _p(U, _f64p))
+    return U
+
+
+def ic_polytrope(p: Params, pos, dims):
+    U = np.zeros((len(pos), p.nf, NC), np.float64)
+    lib().orc_ic_polytrope(ctypes.byref(p), len(pos), _p(np.ascontiguousarray(pos), _i32p), dims[0], dims[1],
+                           dims[2], _p(U, _f64p))
+    return U
+
+
+def ic_binary(p: Params, pos, dims):
+    U = np.zeros((len(pos), p.nf, NC), np.float64)
+    if lib().orc_ic_binary(ctypes.byref(p), len(pos), _p(np.ascontiguousarray(pos), _i32p), dims[0], dims[1],
+                           dims[2], _p(U, _f64p)) != 0:
+        raise MemoryError("oracle binary initial model")
     return U
 
 

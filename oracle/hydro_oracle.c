@@ -559,6 +559,143 @@ void orc_ic_random(const orc_params* p, int64_t g_begin, int64_t g_end, uint64_t
         }
 }
 
+/* BASELINE configs 3 and 4: the rotating n = 1 polytrope (one star per cubic
+ * block of T = min(dims) sub-grids: the weak-scaling tile) with 5 radial-shell
+ * species, and the V1309-like contact binary (two n = 1.5 polytropes,
+ * q ~ 0.1, co-rotating, 1e-5 rho_c pressure-matched atmosphere, species =
+ * the two stars' densities).  Same formulas and operation order as the
+ * product's initial-model generator (so the bench's CPU arm needs nothing of
+ * the product); tests/test_oracle.py checks the two agree bitwise. */
+typedef struct {
+    double* theta;
+    int64_t n;
+    double h, xi1;
+} lane_emden;
+
+static double le_rhs(double nidx, double x, double t, double dt) {
+    const double tp = t > 0.0 ? pow(t, nidx) : 0.0;
+    return -tp - 2.0 / x * dt;
+}
+
+/* theta(xi) of index n by RK4 (step 1e-4) to the first zero */
+static int le_init(lane_emden* le, double nidx) {
+    const double h = 1e-4;
+    int64_t cap = 1 << 16, n = 0;
+    double* th_tab = (double*)malloc((size_t)cap * sizeof(double));
+    if (th_tab == NULL) return -1;
+    double xi = 1e-6, th = 1.0 - xi * xi / 6.0, dth = -xi / 3.0;
+    th_tab[n++] = 1.0;
+    while (th > 0.0 && xi < 20.0) {
+        const double a1 = le_rhs(nidx, xi, th, dth);
+        const double t1 = th + 0.5 * h * dth, d1 = dth + 0.5 * h * a1;
+        const double a2 = le_rhs(nidx, xi + 0.5 * h, t1, d1);
+        const double t2 = th + 0.5 * h * d1, d2 = dth + 0.5 * h * a2;
+        const double a3 = le_rhs(nidx, xi + 0.5 * h, t2, d2);
+        const double t3 = th + h * d2, d3 = dth + h * a3;
+        const double a4 = le_rhs(nidx, xi + h, t3, d3);
+        th += h / 6.0 * (dth + 2 * d1 + 2 * d2 + d3);
+        dth += h / 6.0 * (a1 + 2 * a2 + 2 * a3 + a4);
+        xi += h;
+        if (n == cap) {
+            cap *= 2;
+            double* nt = (double*)realloc(th_tab, (size_t)cap * sizeof(double));
+            if (nt == NULL) {
+                free(th_tab);
+                return -1;
+            }
+            th_tab = nt;
+        }
+        th_tab[n++] = th > 0.0 ? th : 0.0;
+    }
+    le->theta = th_tab;
+    le->n = n;
+    le->h = h;
+    le->xi1 = xi;
+    return 0;
+}
+
+static double le_eval(const lane_emden* le, double xi) {
+    if (xi >= le->xi1) return 0.0;
+    const double k = xi / le->h;
+    const size_t i = (size_t)k;
+    if ((int64_t)i + 1 >= le->n) return 0.0;
+    const double fr = k - (double)i;
+    return le->theta[i] * (1.0 - fr) + le->theta[i + 1] * fr;
+}
+
+static void set_cell_species(const orc_params* p, double* U, int64_t g, int c, double rho, double vx, double vy,
+                             double pr, const double* species) {
+    set_cell(p, U, g, c, rho, vx, vy, 0.0, pr, 0.0);
+    for (int k = 6; k < p->nf; ++k) U[g * p->nf * NC + (int64_t)k * NC + c] = (k - 6) < 5 ? species[k - 6] : 0.0;
+}
+
+void orc_ic_polytrope(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz, double* U) {
+    const double kPi = 3.14159265358979323846;
+    const int T = nx < ny ? (nx < nz ? nx : nz) : (ny < nz ? ny : nz);
+    const double Lb = T * N * p->dx;
+    const double R = 0.4 * 0.5 * Lb;
+    for (int64_t g = 0; g < ngrids; ++g)
+        for (int z = 0; z < N; ++z)
+            for (int y = 0; y < N; ++y)
+                for (int x = 0; x < N; ++x) {
+                    const int lc[3] = {x, y, z};
+                    double rr[3];
+                    for (int d = 0; d < 3; ++d) {
+                        const double xc = ((double)((int64_t)pos[3 * g + d] * N + lc[d]) + 0.5) * p->dx;
+                        const double b = floor(xc / Lb);
+                        rr[d] = xc - (b + 0.5) * Lb;
+                    }
+                    const double r = sqrt(rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2]);
+                    const double xi = kPi * r / R;
+                    const double th = r < R ? (xi > 1e-12 ? sin(xi) / xi : 1.0) : 0.0;
+                    const double rho = th > 1e-10 ? th : 1e-10;
+                    double sp[5] = {0, 0, 0, 0, 0}, vx = 0.0, vy = 0.0;
+                    if (r < R) {
+                        vx = -0.1 * rr[1];
+                        vy = 0.1 * rr[0];
+                        int shell = (int)(5.0 * r / R);
+                        if (shell > 4) shell = 4;
+                        sp[shell] = rho;
+                    }
+                    set_cell_species(p, U, g, (int)cidx(x, y, z), rho, vx, vy, rho * rho, sp);
+                }
+}
+
+int orc_ic_binary(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz, double* U) {
+    lane_emden le;
+    if (le_init(&le, 1.5) != 0) return -1;
+    const double L[3] = {(double)nx * N * p->dx, (double)ny * N * p->dx, (double)nz * N * p->dx};
+    const double R1 = 0.22 * L[0], R2 = 0.5 * R1;
+    const double sep = R1 + R2;
+    const double rc1 = 1.0, rc2 = 0.8;
+    const double m1 = rc1 * R1 * R1 * R1, m2 = rc2 * R2 * R2 * R2;
+    const double cxm = 0.5 * L[0], cy = 0.5 * L[1], cz = 0.5 * L[2];
+    const double x1 = cxm - sep * m2 / (m1 + m2), x2 = cxm + sep * m1 / (m1 + m2);
+    const double amb = 1e-5;
+    for (int64_t g = 0; g < ngrids; ++g)
+        for (int z = 0; z < N; ++z)
+            for (int y = 0; y < N; ++y)
+                for (int x = 0; x < N; ++x) {
+                    const double px = ((double)((int64_t)pos[3 * g] * N + x) + 0.5) * p->dx;
+                    const double py = ((double)((int64_t)pos[3 * g + 1] * N + y) + 0.5) * p->dx;
+                    const double pz = ((double)((int64_t)pos[3 * g + 2] * N + z) + 0.5) * p->dx;
+                    const double r1 = sqrt((px - x1) * (px - x1) + (py - cy) * (py - cy) + (pz - cz) * (pz - cz));
+                    const double r2 = sqrt((px - x2) * (px - x2) + (py - cy) * (py - cy) + (pz - cz) * (pz - cz));
+                    const double t1 = le_eval(&le, le.xi1 * r1 / R1), t2 = le_eval(&le, le.xi1 * r2 / R2);
+                    const double d1 = rc1 * pow(t1, 1.5), d2 = rc2 * pow(t2, 1.5);
+                    const double rho = d1 + d2 > amb ? d1 + d2 : amb;
+                    double vx = 0.0, vy = 0.0;
+                    if (d1 + d2 > amb) {
+                        vx = -0.1 * (py - cy);
+                        vy = 0.1 * (px - cxm);
+                    }
+                    const double sp[5] = {d1, d2, 0.0, 0.0, 0.0};
+                    set_cell_species(p, U, g, (int)cidx(x, y, z), rho, vx, vy, pow(rho, 5.0 / 3.0), sp);
+                }
+    free(le.theta);
+    return 0;
+}
+
 /* ---------------------------------------------------------------------------
  * Coarse-fine AMR.  The reference's octree
  * (build_mesh, workload.cpp:264-327) refines by octants and links only

@@ -89,6 +89,9 @@ void orc_ic_sod(const orc_params* p, int64_t ngrids, const int32_t* pos, int axi
 void orc_ic_sedov(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz,
                   double* U);
 void orc_ic_random(const orc_params* p, int64_t g_begin, int64_t g_end, uint64_t seed, double* U);
+/* configs 3 / 4 initial models (domain nx x ny x nz sub-grids) */
+void orc_ic_polytrope(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz, double* U);
+int orc_ic_binary(const orc_params* p, int64_t ngrids, const int32_t* pos, int nx, int ny, int nz, double* U);
 
 
 /* --- coarse-fine AMR ---

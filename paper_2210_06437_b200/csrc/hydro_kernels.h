@@ -15,6 +15,16 @@ struct StageArgs {
     const int* nbr;             // [local][6] local neighbour index, -1 = outflow
     const int* list;            // CTA -> local sub-grid (nullable: first + blockIdx.x)
     int first;
+    // Per-sub-grid drop-in (ts_hydro_launch_stage): up to kInlineList sub-grids
+    // passed by value in the launch parameters (no device list per launch);
+    // list_inline_n > 0 takes precedence over list / first.
+    static constexpr int kInlineList = 32;
+    int list_inline_n;
+    int list_inline[kInlineList];
+    // The CTA that does stage 1's once-per-step duties (dt_out, amax_reset,
+    // amax_reset2): 0 = block 0 of the launch (batched steps); g + 1 = the CTA
+    // of sub-grid g (drop-in launches: exactly one launch per step holds it).
+    int lead_g1;
     const double* amax_in;      // signal speed(s) behind this step's dt (max over amax_n values:
     int amax_n;                 //   one per rank when the P2P transport gathered them)
     double* amax_out;           // stage 3: max signal speed of U^{n+1}
@@ -33,8 +43,8 @@ struct StageArgs {
     // seq) and writes the max over its own gather half (gather_own) to
     // amax_global, the next stage 1's amax_in.  The dt all-reduce is thereby
     // one CTA's tail: stage 1 starts with the global dt in place.
-    unsigned int* done_ctr;              // nullptr: single rank (no tail)
-    int total_ctas;
+    unsigned int* done_ctr;              // nullptr: single rank (no tail); monotonic
+    unsigned int done_target;            // done_ctr after this stage's last CTA counted
     int rank;
     int push_n;                          // ranks to push the amax to (0: no dt push)
     double* const* push_gather;          // [push_n] gather arrays (this step's half)
@@ -57,7 +67,11 @@ struct StageArgs {
     const int* cta_bnd;
     const int2* push_tbl;                // nullptr: no push
     double* const* push_out;             // [world] peer's buffer of this stage's U^(k)
+    // halo_ctr: one monotonic counter per stage slot (halo_seq % 3), never
+    // reset in the kernel: stages overlap (PDL), so a shared or reset counter
+    // could be bumped by the next stage's CTAs before this one completes
     unsigned int* halo_ctr;
+    unsigned int halo_target;            // halo_ctr after this stage's last boundary CTA counted
     unsigned int* const* halo_flag;      // [world] (nullptr: no slabs for that rank)
     int halo_flag_n;
     unsigned int halo_seq;

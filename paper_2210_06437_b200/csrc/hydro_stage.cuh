@@ -24,6 +24,7 @@
 // serves every direction.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 
 #include "hydro_device.cuh"
@@ -680,11 +681,10 @@ __device__ __forceinline__ void halo_push(const StageArgs& A, size_t own, int b)
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        if (atomicAdd(A.halo_ctr, 1u) == (unsigned)A.n_boundary - 1u) {
+        if (atomicAdd(A.halo_ctr, 1u) == A.halo_target - 1u) {
             __threadfence_system();
             for (int q = 0; q < A.halo_flag_n; ++q)
                 if (A.halo_flag[q] != nullptr) atomicExch_system(A.halo_flag[q], A.halo_seq);
-            *A.halo_ctr = 0u;
         }
     }
 }
@@ -709,8 +709,11 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         A.cta_log[4 * blockIdx.x] = sm;
         A.cta_log[4 * blockIdx.x + 1] = globaltimer();
     }
-    const int g = A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x;
+    const int g = A.list_inline_n > 0 ? A.list_inline[blockIdx.x]
+                  : (A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x);
     const int t = threadIdx.x;
+    // stage 1's once-per-step duties (see StageArgs::lead_g1)
+    const bool lead = A.lead_g1 == 0 ? blockIdx.x == 0 : g == A.lead_g1 - 1;
     if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0) {
         // proxies of U^(k-1): pushed by the peers' previous-stage boundary CTAs
         // (released in their first wave, so this rarely spins)
@@ -719,7 +722,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         __syncthreads();
     }
     if (A.pdl_trigger) {
-        if (STAGE == 1 && blockIdx.x == 0) {
+        if (STAGE == 1 && lead) {
             // the slot stage 3 accumulates into is zeroed before any dependent can start
             if (t == 0 && A.amax_reset != nullptr) {
                 *A.amax_reset = 0.0;
@@ -753,12 +756,12 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
     }
     const double dtdx_early = 0.5 * (((A.cfl * A.dx) / amax_in) / level_dx(A, g));
-    if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
+    if (STAGE == 1 && lead && t == 0) {
         if (A.dt_out != nullptr) *A.dt_out = (A.cfl * A.dx) / amax_in;
         if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
     }
 #endif
-    if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
+    if (STAGE == 1 && lead && t == 0) {
         if (A.amax_reset != nullptr && !A.pdl_trigger) *A.amax_reset = 0.0;
     }
     StageCtx c;
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             }
             const double dt = (A.cfl * A.dx) / amax_in;
             c.dtdx = 0.5 * (dt / level_dx(A, g));  // the sweeps carry twice the KT flux (kt2)
-            if (STAGE == 1 && blockIdx.x == 0 && t == 0) {
+            if (STAGE == 1 && lead && t == 0) {
                 if (A.dt_out != nullptr) *A.dt_out = dt;
                 if (A.amax_reset2 != nullptr) *A.amax_reset2 = 0.0;
             }
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         __syncthreads();
         if (t == 0) {
             __threadfence();
-            if (atomicAdd(A.done_ctr, 1u) == (unsigned)A.total_ctas - 1u) {
+            if (atomicAdd(A.done_ctr, 1u) == A.done_target - 1u) {
                 __threadfence();
                 if (STAGE == 3 && A.push_n > 0) {
                     // dt all-reduce: this rank's max into every rank's gather slot
@@ -871,7 +874,6 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                     for (int q = 1; q < A.push_n; ++q) g = fmax(g, A.gather_own[q]);
                     *A.amax_global = g;
                 }
-                *A.done_ctr = 0u;
             }
         }
     }
@@ -888,12 +890,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 template <int NF, int RECON, int STAGE>
 inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
     const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the dynamic shared-memory limit is a per-device function attribute:
+    // set it once on every device this instantiation is launched on
+    static std::atomic<unsigned long long> configured{0ull};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if ((configured.load(std::memory_order_acquire) & bit) == 0ull) {
+        e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     if (!pdl) {
         stage_kernel<NF, RECON, STAGE><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);

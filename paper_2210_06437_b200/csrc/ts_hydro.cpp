@@ -111,6 +111,17 @@ Nccl& nccl() {
     return n;
 }
 
+struct DoneThunk {
+    ts_done_fn fn;
+    void* user;
+    int32_t* list;
+};
+void CUDART_CB done_host(void* p) {
+    auto* t = static_cast<DoneThunk*>(p);
+    if (t->fn) t->fn(t->user);
+    delete t;
+}
+
 struct PendingLaunch {
     uint8_t kind;
     const char* name;
@@ -260,7 +271,9 @@ struct ts_hydro_ctx {
     int32_t* d_flags = nullptr;       // [2 world]
     double* d_gather = nullptr;       // [2][world]
     std::vector<PeerMap> pm;          // by rank
-    unsigned int* d_ctr = nullptr;    // stage-3 CTA counter of the fused dt push
+    unsigned int* d_ctr = nullptr;    // [0] stage-3 CTA count of the tail dt push, [1..3] halo-push counts by stage slot
+    uint32_t done_cnt = 0;            // expected d_ctr[0] (monotonic, wrapping)
+    uint32_t halo_cnt[3] = {0, 0, 0}; // expected d_ctr[1 + slot]
     double** d_push_gather = nullptr; // [2][world] gather arrays (parity halves) of every rank
     unsigned int** d_push_flag = nullptr;  // [world] dt flag word of every peer (nullptr for self)
     uint32_t xseq = 0, aseq = 0;      // exchange / dt-gather sequence numbers (same on every rank)
@@ -293,6 +306,31 @@ struct ts_hydro_ctx {
     bool amr_slab_fill = true;             // TS_HYDRO_AMR_FULLFILL=1: fill whole proxies
     tsh::AmrReflux* d_amr_rec = nullptr;
     int32_t* d_amr_level = nullptr;
+
+    // Per-sub-grid drop-in steps (ts_hydro_launch_stage ... ts_hydro_finish_step).
+    // Launches are ISSUED in dependency order — a stage-k launch is parked on
+    // the host until its sub-grids and their face neighbours have issued stage
+    // k-1 of the step — and ORDERED on the device by the dataflow flags
+    // (d_flow) and the stage-3 count (d_cnt3), so no host barrier separates
+    // the stages and no stream ever waits behind a kernel spinning on work
+    // queued after it.
+    struct DropinLaunch {
+        int stage;
+        std::vector<int32_t> list;
+        uint32_t stream_id;
+        uint64_t guid;
+        ts_done_fn done;
+        void* user;
+    };
+    bool din_open = false;       // a drop-in step is in progress
+    bool din_chained = false;    // the previous step was a drop-in step: its flags / count are on the device
+    uint32_t din_seq = 0;        // flow seq of the open step
+    std::vector<uint8_t> din_req;     // [n_owned] last stage requested in the open step (0..3)
+    std::vector<uint8_t> din_issued;  // [n_owned] last stage issued
+    int64_t din_done3 = 0;            // sub-grids whose stage 3 was issued
+    std::vector<DropinLaunch> din_parked;
+    std::vector<uint8_t> din_streams; // streams used by the open step
+    cudaEvent_t ev_din = nullptr;     // stream-0 work before the step (upload, compute_dt, batched steps)
 
     // stepping
     uint64_t steps_done = 0;
@@ -928,7 +966,8 @@ int do_step(ts_hydro_ctx* c) {
         }
         if (p2p && stage == 3 && !c->dt_kernel) {
             a.done_ctr = c->d_ctr;
-            a.total_ctas = (int)c->n_owned;
+            c->done_cnt += (uint32_t)c->n_owned;
+            a.done_target = c->done_cnt;
             a.rank = c->rank;
         }
         if (p2p && stage == 3 && !c->dt_kernel) {
@@ -991,10 +1030,15 @@ int do_step(ts_hydro_ctx* c) {
             a.cta_bnd = c->d_cta_bnd;
             a.push_tbl = c->d_push_tbl;
             a.push_out = c->d_push_out + (size_t)out_idx * c->world;
-            a.halo_ctr = c->d_ctr + 1;
             a.halo_flag = c->d_halo_flag;
             a.halo_flag_n = c->world;
             a.halo_seq = ++c->xseq;
+            {
+                const int slot = (int)(a.halo_seq % 3u);
+                a.halo_ctr = c->d_ctr + 1 + slot;
+                c->halo_cnt[slot] += (uint32_t)c->boundary.size();
+                a.halo_target = c->halo_cnt[slot];
+            }
             // a stage that began with the copy-engine refresh waits on its
             // event in stream order; the others start in the previous tail
             rc = launch_stage_list(c, a, stage, c->d_order, c->n_owned, 0, 0, 0,
@@ -1057,6 +1101,140 @@ int do_step(ts_hydro_ctx* c) {
     }
     c->flow_chain = flow && !multi;
     c->steps_done++;
+    return TS_OK;
+}
+
+// ---- per-sub-grid drop-in steps (ts_hydro_launch_stage) -------------------
+// Open a step: stage-1 launches of the step wait (stream event) for
+// everything already on the compute stream; when the previous step was not a
+// drop-in step (no flags / stage-3 count on the device for it), dt comes from
+// the stream-ordered signal speed and the max slots this step and the next
+// accumulate into are zeroed here.
+int dropin_open(ts_hydro_ctx* c) {
+    if (!c->dt_valid) return fail(c, TS_ESTATE, "no dt (call ts_hydro_compute_dt first)");
+    cudaStream_t s0;
+    int rc = ensure_stream(c, 0, &s0);
+    if (rc) return rc;
+    if (c->ev_din == nullptr) TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_din, cudaEventDisableTiming));
+    if (!c->din_chained) {
+        TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 1), 0, sizeof(double), s0));
+        TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 2), 0, sizeof(double), s0));
+    }
+    TS_CUDA(c, cudaEventRecord(c->ev_din, s0));
+    c->din_open = true;
+    c->din_seq = ++c->flow_seq;
+    c->din_req.assign((size_t)c->n_owned, 0);
+    c->din_issued.assign((size_t)c->n_owned, 0);
+    c->din_streams.assign(c->streams.size(), 0);
+    c->din_done3 = 0;
+    c->din_parked.clear();
+    return TS_OK;
+}
+
+bool dropin_ready(const ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
+    if (L.stage == 1) return true;
+    const uint8_t need = (uint8_t)(L.stage - 1);
+    for (int32_t g : L.list) {
+        if (c->din_issued[(size_t)g] < need) return false;
+        for (int f = 0; f < 6; ++f) {
+            const int32_t h = c->nbr_local[(size_t)g * 6 + f];
+            if (h >= 0 && h < c->n_owned && c->din_issued[(size_t)h] < need) return false;
+        }
+    }
+    return true;
+}
+
+int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
+    cudaStream_t s;
+    int rc = ensure_stream(c, L.stream_id, &s);
+    if (rc) return rc;
+    const int stage = L.stage;
+    const size_t n = (size_t)c->n_owned;
+    tsh::StageArgs a = stage_args(c, stage);
+    a.amax_in = amax_slot(c, c->steps_done);
+    a.amax_n = 1;
+    a.amax_out = amax_slot(c, c->steps_done + 1);
+    a.flow_n = (int)c->n_owned;
+    a.flow_seq = c->din_seq;
+    a.flow_wait_seq = c->din_seq;
+    a.flow_done = c->d_flow + (size_t)(stage - 1) * n;
+    if (stage > 1) {
+        a.flow_wait = c->d_flow + (size_t)(stage - 2) * n;
+    } else {
+        // everything on the compute stream before the step (upload, dt, a batched step)
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_din, 0));
+        a.lead_g1 = 1;  // sub-grid 0's stage-1 CTA writes dt and zeroes the max slot two steps ahead
+        a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+        a.amax_reset2 = amax_slot(c, c->steps_done + 2);
+        if (c->din_chained) {
+            // U^n of the sub-grid and its neighbours: the previous step's stage-3 flags;
+            // dt: every sub-grid's stage-3 max (the count) before the z sweep
+            a.flow_wait = c->d_flow + 2 * n;
+            a.flow_wait_seq = c->din_seq - 1u;
+            a.cnt_wait = c->d_cnt3;
+            a.cnt_expect = c->cnt3_expect;
+        }
+    }
+    if (stage == 3) a.cnt_done = c->d_cnt3;
+    // the sub-grid list: by value in the launch parameters, or as runs of
+    // consecutive indices (first + blockIdx.x), one launch per run
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)L.stream_id, L.guid, &stamp);
+    if (rc) return rc;
+    a.stamp = stamp;
+    a.list = nullptr;
+    const size_t m = L.list.size();
+    if (m <= (size_t)tsh::StageArgs::kInlineList) {
+        a.list_inline_n = (int)m;
+        for (size_t k = 0; k < m; ++k) a.list_inline[k] = L.list[k];
+        TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)m, s, false));
+    } else {
+        size_t k = 0;
+        while (k < m) {
+            size_t e = k + 1;
+            while (e < m && L.list[e] == L.list[e - 1] + 1) ++e;
+            a.list_inline_n = 0;
+            a.first = L.list[k];
+            TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)(e - k), s, false));
+            k = e;
+        }
+    }
+    if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
+    for (int32_t g : L.list) c->din_issued[(size_t)g] = (uint8_t)stage;
+    if (stage == 3) c->din_done3 += (int64_t)m;
+    if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
+    c->din_streams[L.stream_id] = 1;
+    return TS_OK;
+}
+
+// Issue every parked launch whose producers have been issued, until none is
+// left ready.  Issue order then respects the dataflow, so a kernel spinning on
+// a flag never blocks the stream its producer is queued on.
+int dropin_pump(ts_hydro_ctx* c) {
+    bool progress = true;
+    while (progress && !c->din_parked.empty()) {
+        progress = false;
+        for (size_t k = 0; k < c->din_parked.size();) {
+            if (!dropin_ready(c, c->din_parked[k])) {
+                ++k;
+                continue;
+            }
+            ts_hydro_ctx::DropinLaunch L = std::move(c->din_parked[k]);
+            c->din_parked.erase(c->din_parked.begin() + (std::ptrdiff_t)k);
+            const int rc = dropin_issue(c, L);
+            if (rc) return rc;
+            progress = true;
+        }
+    }
+    return TS_OK;
+}
+
+// Entry points that replace or step the state: not while a drop-in step is
+// open; afterwards the next drop-in step starts stream-ordered.
+int mutating(ts_hydro_ctx* c) {
+    if (c->din_open)
+        return fail(c, TS_ESTATE, "a per-sub-grid step is open (launch stage 3 of every sub-grid, then ts_hydro_finish_step)");
+    c->din_chained = false;
     return TS_OK;
 }
 
@@ -1322,6 +1500,7 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
     int rc = guard(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (n < 1 || nbr == nullptr || owner == nullptr) return fail(c, TS_EINVAL, "empty mesh");
     if (world < 1) return fail(c, TS_EINVAL, "mesh world_size must be positive");
     if (rank < 0 || rank >= world) return fail(c, TS_EINVAL, "rank outside the world");
@@ -1504,9 +1683,11 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         if (!rc) rc = dalloc(c, &c->d_recv, 2 * (size_t)c->n_recv_total * c->nf * kSlab);
         if (!rc) rc = dalloc(c, &c->d_flags, 2 * (size_t)world);
         if (!rc) rc = dalloc(c, &c->d_gather, 2 * (size_t)world);
-        if (!rc) rc = dalloc(c, &c->d_ctr, 2);  // [0] dt push, [1] halo push
+        if (!rc) rc = dalloc(c, &c->d_ctr, 4);  // [0] dt push, [1..3] halo push by stage slot
         if (rc) return rc;
-        TS_CUDA(c, cudaMemset(c->d_ctr, 0, 2 * sizeof(unsigned int)));
+        TS_CUDA(c, cudaMemset(c->d_ctr, 0, 4 * sizeof(unsigned int)));
+        c->done_cnt = 0;
+        std::fill(std::begin(c->halo_cnt), std::end(c->halo_cnt), 0u);
         // fused push targets by boundary position: {peer rank, local index on the peer}
         std::vector<int2> tbl(c->boundary.size() * 6, make_int2(-1, -1));
         std::vector<int32_t> bpos((size_t)c->n_owned, -1);
@@ -1549,6 +1730,7 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
     int rc = guard(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (nl < 1 || nbr == nullptr || level == nullptr) return fail(c, TS_EINVAL, "empty AMR mesh");
     if (np < 0 || nr < 0 || (np > 0 && px == nullptr) || (nr > 0 && rf == nullptr))
         return fail(c, TS_EINVAL, "AMR proxy / reflux tables missing");
@@ -1682,6 +1864,7 @@ int ts_hydro_upload(ts_hydro_ctx* c, int64_t first, int64_t count, const double*
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (first < 0 || count < 0 || first + count > c->n_owned || (count > 0 && host == nullptr))
         return fail(c, TS_EINVAL, "upload range outside the owned sub-grids");
     cudaSetDevice(c->dev);
@@ -1746,6 +1929,7 @@ int ts_hydro_init_random(ts_hydro_ctx* c, uint64_t seed) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     cudaSetDevice(c->dev);
     cudaStream_t s;
     rc = ensure_stream(c, 0, &s);
@@ -1761,12 +1945,13 @@ int ts_hydro_compute_dt(ts_hydro_ctx* c, double* dt_out) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     cudaSetDevice(c->dev);
     rc = do_compute_dt(c);
     if (rc) return rc;
     if (dt_out != nullptr) {
         cudaStream_t s = c->streams[0];
-        const double* src = c->amax_src != nullptr ? c->amax_src : c->d_scal + (c->steps_done & 1);
+        const double* src = c->amax_src != nullptr ? c->amax_src : amax_slot(c, c->steps_done);
         std::vector<double> v((size_t)(c->amax_src != nullptr ? c->amax_n : 1));
         TS_CUDA(c, cudaMemcpyAsync(v.data(), src, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
         TS_CUDA(c, cudaStreamSynchronize(s));
@@ -1781,6 +1966,7 @@ int ts_hydro_step(ts_hydro_ctx* c, uint64_t nsteps) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
     cudaSetDevice(c->dev);
     if (c->world > 1 && c->comm == nullptr && !c->p2p)
@@ -1800,6 +1986,7 @@ int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out,
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
     c->halo_pushed = false;  // a call starts from a copy-engine halo refresh (collective on every rank)
     cudaSetDevice(c->dev);
@@ -1819,18 +2006,6 @@ int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out,
     return TS_OK;
 }
 
-namespace {
-struct DoneThunk {
-    ts_done_fn fn;
-    void* user;
-    int32_t* list;
-};
-void CUDART_CB done_host(void* p) {
-    auto* t = static_cast<DoneThunk*>(p);
-    if (t->fn) t->fn(t->user);
-    delete t;
-}
-}  // namespace
 
 // Pipelined host-buffer steps.  Copies run in xfer_chunks sub-grid ranges on
 // their own streams (H2D 3, D2H 4), so that when a call's input is the
@@ -1845,6 +2020,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (host_in == nullptr || host_out == nullptr) return fail(c, TS_EINVAL, "null host buffer");
     if (c->cfg.stream_count < 5) return fail(c, TS_EINVAL, "pipelined host steps need stream_count >= 5");
     if (c->amr) return fail(c, TS_ESTATE, "pipelined host steps are not available on an AMR mesh (use ts_hydro_step_host)");
@@ -1946,6 +2122,7 @@ int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (ms == nullptr) return fail(c, TS_EINVAL, "null output");
     if (c->world > 1 && c->comm == nullptr && !c->p2p)
         return fail(c, TS_ESTATE, "multi-rank mesh needs ts_hydro_comm_init or ts_hydro_p2p_import before stepping");
@@ -2020,31 +2197,25 @@ int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_i
     if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
     if (c->world > 1) return fail(c, TS_ESTATE, "per-sub-grid launches are single-rank (use ts_hydro_step)");
     if (c->amr) return fail(c, TS_ESTATE, "per-sub-grid launches are not available on an AMR mesh (use ts_hydro_step)");
-    if (!c->dt_valid) return fail(c, TS_ESTATE, "no dt (call ts_hydro_compute_dt first)");
-    std::vector<int32_t> list((size_t)count);
-    for (int64_t k = 0; k < count; ++k) {
-        if (owned_index[k] < 0 || owned_index[k] >= c->n_owned)
-            return fail(c, TS_EINVAL, "sub-grid index outside the owned range");
-        list[(size_t)k] = (int32_t)owned_index[k];
-    }
     cudaSetDevice(c->dev);
-    cudaStream_t s;
-    rc = ensure_stream(c, stream_id, &s);
-    if (rc) return rc;
-    int32_t* d_list = nullptr;
-    TS_CUDA(c, cudaMallocAsync((void**)&d_list, list.size() * sizeof(int32_t), s));
-    TS_CUDA(c, cudaMemcpyAsync(d_list, list.data(), list.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    tsh::StageArgs a = stage_args(c, stage);
-    a.amax_out = c->d_scal + 3;  // dummy: the caller recomputes dt per step
-    rc = launch_stage_list(c, a, stage, d_list, count, 0, stream_id, guid);
-    if (rc) return rc;
-    TS_CUDA(c, cudaFreeAsync(d_list, s));
-    if (done != nullptr) {
-        auto* t = new DoneThunk{done, user, nullptr};
-        TS_CUDA(c, cudaLaunchHostFunc(s, done_host, t));
+    if (!c->din_open) {
+        if (stage != 1) return fail(c, TS_ESTATE, "a per-sub-grid step starts with stage 1");
+        rc = dropin_open(c);
+        if (rc) return rc;
     }
-    // pageable H2D copies are staged before cudaMemcpyAsync returns: `list` may go
-    return TS_OK;
+    ts_hydro_ctx::DropinLaunch L{stage, std::vector<int32_t>((size_t)count), stream_id, guid, done, user};
+    for (int64_t k = 0; k < count; ++k) {
+        const int64_t g = owned_index[k];
+        if (g < 0 || g >= c->n_owned) return fail(c, TS_EINVAL, "sub-grid index outside the owned range");
+        if (c->din_req[(size_t)g] != stage - 1)
+            return fail(c, TS_ESTATE, "sub-grid " + std::to_string(g) + ": stage " + std::to_string(stage) +
+                                          " requested after stage " + std::to_string(c->din_req[(size_t)g]) +
+                                          " of this step (stages run 1, 2, 3 once per step)");
+        L.list[(size_t)k] = (int32_t)g;
+    }
+    for (int32_t g : L.list) c->din_req[(size_t)g] = (uint8_t)stage;
+    c->din_parked.push_back(std::move(L));
+    return dropin_pump(c);
 }
 
 int ts_hydro_finish_step(ts_hydro_ctx* c) {
@@ -2052,10 +2223,27 @@ int ts_hydro_finish_step(ts_hydro_ctx* c) {
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     cudaSetDevice(c->dev);
-    rc = sync_all(c);
+    if (!c->din_open) return fail(c, TS_ESTATE, "no per-sub-grid step is open (ts_hydro_launch_stage stage 1 opens one)");
+    if (c->din_done3 != c->n_owned || !c->din_parked.empty())
+        return fail(c, TS_ESTATE, "finish_step before every owned sub-grid launched stage 3 (" +
+                                      std::to_string(c->din_done3) + " of " + std::to_string(c->n_owned) + ")");
+    // Join every stream the step used into the compute stream (no host wait):
+    // later stream-0 work (downloads, batched steps, the next step's opening
+    // event) is ordered after all of it.
+    cudaStream_t s0;
+    rc = ensure_stream(c, 0, &s0);
     if (rc) return rc;
+    for (size_t id = 0; id < c->din_streams.size(); ++id) {
+        if (!c->din_streams[id] || id == 0) continue;
+        TS_CUDA(c, cudaEventRecord(c->ev_in, c->streams[id]));
+        TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
+    }
+    c->din_open = false;
+    c->din_chained = true;
+    c->cnt3_expect += (uint32_t)c->n_owned;  // every stage-3 CTA of the step counted into d_cnt3
     c->steps_done++;
-    c->dt_valid = false;
+    c->dt_valid = true;  // the step's stage 3 reduced the next dt's signal speed on the device
+    c->amax_src = nullptr;
     return TS_OK;
 }
 
@@ -2131,6 +2319,7 @@ int ts_hydro_comm_init(ts_hydro_ctx* c, const uint8_t id[128], int32_t nranks, i
     int rc = guard(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (id == nullptr || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TS_EINVAL, "bad comm arguments");
     if (c->host_only) return fail(c, TS_ESTATE, "host-only context (device_id = -1) cannot touch the GPU");
     Nccl& n = nccl();
@@ -2205,6 +2394,7 @@ int ts_hydro_p2p_import(ts_hydro_ctx* c, const void* blobs, int32_t world) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (blobs == nullptr || world != c->world) return fail(c, TS_EINVAL, "need one blob per rank of the mesh");
     cudaSetDevice(c->dev);
     rc = sync_all(c);
@@ -2269,6 +2459,7 @@ int ts_hydro_halo_exchange(ts_hydro_ctx* c) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (c->world <= 1) return TS_OK;
     if (c->comm == nullptr && !c->p2p) return fail(c, TS_ESTATE, "no transport (ts_hydro_comm_init / ts_hydro_p2p_import)");
     cudaSetDevice(c->dev);
@@ -2381,6 +2572,7 @@ int ts_hydro_restore(ts_hydro_ctx* c, const char* const* paths, int32_t n_paths)
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
     if (c->amr) return fail(c, TS_ESTATE, "checkpoints of AMR meshes are not supported");
     if (paths == nullptr || n_paths < 1) return fail(c, TS_EINVAL, "no checkpoint files");
     const size_t per = (size_t)c->nf * kNC;

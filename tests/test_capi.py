@@ -57,16 +57,21 @@ def test_uniform_mesh_matches_oracle(hydro, oracle_lib, dims, periodic, world):
     assert np.array_equal(m.owner, owner)
 
 
-@pytest.mark.parametrize("problem", ["sod", "sedov", "random"])
+@pytest.mark.parametrize("problem", ["sod", "sedov", "random", "polytrope", "binary"])
 def test_ic_fill_matches_oracle_bitwise(hydro, oracle_lib, problem):
-    cfg = hydro.HydroConfig(dx=1.0 / 32, n_species=2 if problem == "random" else 0)
-    m = hydro.uniform_mesh(4, 4, 4)
+    species = {"random": 2, "polytrope": 5, "binary": 5}.get(problem, 0)
+    cfg = hydro.HydroConfig(dx=1.0 / 32, n_species=species)
+    m = hydro.uniform_mesh(4, 4, 4) if problem != "binary" else hydro.uniform_mesh(8, 4, 4)
     U = hydro.ic_fill(cfg, problem, m, np.arange(m.n), seed=2210)
     p = oracle_lib.params(nf=cfg.nf, dx=cfg.dx)
     if problem == "sod":
         want = oracle_lib.ic_sod(p, m.pos, 0)
     elif problem == "sedov":
         want = oracle_lib.ic_sedov(p, m.pos, (4, 4, 4))
+    elif problem == "polytrope":
+        want = oracle_lib.ic_polytrope(p, m.pos, (4, 4, 4))
+    elif problem == "binary":
+        want = oracle_lib.ic_binary(p, m.pos, (8, 4, 4))
     else:
         want = oracle_lib.ic_random(p, 0, m.n, 2210)
     assert np.array_equal(U, want)

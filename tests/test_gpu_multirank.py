@@ -1,5 +1,9 @@
-"""Cross-GPU halo exchange (NCCL) parity: runs tools/multigpu_check.py under
-torchrun on 2 GPUs when the box has them (gpurun --gpus 2), else skips."""
+"""Cross-rank halo exchange parity: runs tools/multigpu_check.py under
+torchrun with world size 2 — one rank per GPU when the box has two (gpurun
+--gpus 2), and always both ranks on cuda:0 (two processes sharing one GPU
+through CUDA IPC, time-sliced by the driver), so the fused in-kernel slab push
+(p2p) and the copy-engine exchange (p2p-ce) run on a one-GPU box too.  NCCL
+refuses two ranks on one device, so its cases need two GPUs."""
 import os
 import socket
 import subprocess
@@ -44,6 +48,40 @@ def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args, transport):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
+
+
+SAME_DEVICE_MESHES = [["--dims", "4", "4", "8"],
+                      ["--dims", "2", "4", "4", "--periodic", "xyz", "--species", "5"],
+                      ["--dims", "5", "3", "2", "--periodic", "x", "--recon", "minmod", "--species", "2"]]
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
+@pytest.mark.parametrize("args", SAME_DEVICE_MESHES)
+def test_two_ranks_on_one_gpu_bitwise_equal_to_single_rank(args, transport):
+    """World 2 on one GPU: rank-partitioned steps (Morton chunks, proxies,
+    slab push / copy-engine exchange, dt all-reduce across the ranks) equal
+    the one-rank run bitwise — the partition invariance of
+    test_workload.cpp:317-331 / 448-464 on the cross-rank code path."""
+    if _gpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tools", "multigpu_check.py"), *args, "--transport", transport, "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
+def test_mismatch_on_one_gpu_fails_instead_of_hanging(transport):
+    if _gpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tools", "multigpu_check.py"), "--mismatch", "--transport", transport, "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MISMATCH DETECTED" in r.stdout
 
 
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])

@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--species", type=int, default=0)
     ap.add_argument("--recon", default="ppm")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "p2p-ce", "nccl"])
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (two processes sharing one GPU through CUDA IPC, time-sliced): "
+                         "the cross-rank path on a one-GPU box")
     ap.add_argument("--mismatch", action="store_true",
                     help="rank 1 makes one stepping call too many: it must fail with TS_ECOMM, not hang")
     a = ap.parse_args()
@@ -39,7 +42,9 @@ def main():
     if a.mismatch:
         os.environ["TS_HYDRO_WAIT_TIMEOUT_MS"] = "2000"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = 0 if a.same_device else int(os.environ.get("LOCAL_RANK", rank))
+    if a.same_device and a.transport == "nccl":
+        raise SystemExit("NCCL refuses two ranks on one GPU: --same-device takes p2p / p2p-ce")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = H.HydroConfig(device_id=local, n_species=a.species, dx=1.0 / (8 * a.dims[0]), recon=a.recon)
     mesh = H.uniform_mesh(*a.dims, periodic=a.periodic, world=world)
@@ -104,7 +109,8 @@ def main():
     dist.barrier()
     if rank == 0:
         print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
-              f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}", flush=True)
+              f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}"
+              + (" same-device" if a.same_device else ""), flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 1 else 1
 
