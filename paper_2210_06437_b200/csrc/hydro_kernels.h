@@ -111,6 +111,14 @@ struct StageArgs {
     // counter) while the rest of the stage still runs.
     unsigned int* chunk_ctr;             // nullptr: no counting
     int chunk_n, chunk_owned;
+    // First stage 1 of a chained pipelined host step: U^n arrives by H2D
+    // chunks (sub-grid g in chunk g * chunk_n / chunk_owned) whose landing the
+    // copy stream signals with h2d_flag[chunk] = h2d_seq (a stream memory
+    // write behind each copy: release of the copy's bytes).  A CTA acquires
+    // the flags of its own and its face neighbours' chunks before reading, so
+    // the stage runs under the transfer instead of after all of it.
+    const unsigned int* h2d_flag;        // nullptr: U^n already in place
+    unsigned int h2d_seq;
     // Every cross-GPU spin gives up after wait_ns (globaltimer) and sets
     // *err (mapped host word) instead of hanging the GPU.
     unsigned long long* err;

@@ -732,6 +732,15 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         }
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
+    if (A.h2d_flag != nullptr) {
+        // U^n of this sub-grid and of its face neighbours landed (StageArgs::h2d_flag)
+        if (t < 7) {
+            const int h = t == 0 ? g : __ldg(A.nbr + 6 * g + (t - 1));
+            if (h >= 0 && h < A.chunk_owned)
+                flow_wait_one(A, A.h2d_flag + (int)(((long long)h * A.chunk_n) / A.chunk_owned), A.h2d_seq);
+        }
+        __syncthreads();
+    }
     if (A.flow_wait != nullptr) {
         // U^(k-1) of this sub-grid and of its face neighbours: the previous
         // stage's output.  The seven flags are acquired in parallel, one per

@@ -218,6 +218,11 @@ struct ts_hydro_ctx {
     uint32_t* d_chunk_ctr = nullptr;          // [kXferChunksMax] stage-3 completions per D2H chunk
     uint32_t chunk_expect[kXferChunksMax] = {};  // running totals (wrapping)
     bool chunk_arm = false;                   // next stage-3 launch counts into d_chunk_ctr
+    // chained pipelined host steps: stage 1 starts under the H2D (StageArgs::h2d_flag)
+    bool h2d_gate = true;                     // TS_HYDRO_H2D_GATE=0: stage 1 waits for the whole H2D
+    uint32_t* d_h2d_flag = nullptr;           // [kXferChunksMax] landed-chunk flags
+    uint32_t h2d_seq = 0;
+    bool h2d_arm = false;                     // the next stage 1 acquires the chunk flags of h2d_seq
 
     // mesh
     bool have_mesh = false;
@@ -472,6 +477,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_cnt3);
     dfree(c, &c->d_cta_log);
     dfree(c, &c->d_chunk_ctr);
+    dfree(c, &c->d_h2d_flag);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
     dfree(c, &c->d_gid);
@@ -959,6 +965,13 @@ int do_step(ts_hydro_ctx* c) {
             if (!multi) a.amax_reset2 = amax_slot(c, c->steps_done + 2);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
         }
+        if (stage == 1 && c->h2d_arm) {
+            a.h2d_flag = c->d_h2d_flag;
+            a.h2d_seq = c->h2d_seq;
+            a.chunk_n = c->xfer_chunks;
+            a.chunk_owned = (int)c->n_owned;
+            c->h2d_arm = false;
+        }
         if (stage == 3 && c->chunk_arm) {
             a.chunk_ctr = c->d_chunk_ctr;
             a.chunk_n = c->xfer_chunks;
@@ -1332,6 +1345,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_FLOW_STEPS")) c->flow_steps = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_FULLFILL")) c->amr_slab_fill = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
@@ -2047,9 +2061,25 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     };
     const char* in_b = reinterpret_cast<const char*>(host_in);
     const bool chained = c->prev_out == host_in && c->prev_out_bytes == bytes;
-    // H2D: U^n may still be read by earlier work on the compute stream
-    TS_CUDA(c, cudaEventRecord(c->ev_in, s));
-    TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_in, 0));
+    // Chained on one rank: dt is the previous call's stage-3 signal speed (its
+    // input is this call's input) and stage 1 starts under the H2D, each CTA
+    // once the chunks of its sub-grid and neighbours landed.
+    const bool gate = chained && c->h2d_gate && c->dt_valid && c->world == 1 && nsteps > 0 &&
+                      memops().write32 != nullptr;
+    if (gate && c->d_h2d_flag == nullptr) {
+        rc = dalloc(c, &c->d_h2d_flag, (size_t)ts_hydro_ctx::kXferChunksMax);
+        if (rc) return rc;
+        TS_CUDA(c, cudaMemset(c->d_h2d_flag, 0, ts_hydro_ctx::kXferChunksMax * sizeof(uint32_t)));
+        c->h2d_seq = 0;
+    }
+    // H2D: U^n may still be read by earlier work on the compute stream (when
+    // chained, its readers are the previous call's stage-3 CTAs of the chunk,
+    // which the chunk's D2H already waited for)
+    if (!gate) {
+        TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+        TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_in, 0));
+    }
+    if (gate) ++c->h2d_seq;
     // the previous call's D2H reads U^n: chunk-wise behind it when chained,
     // else behind all of it (an unrecorded event is a no-op wait)
     if (!chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[C - 1], 0));
@@ -2065,11 +2095,14 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
         if (len > 0)
             TS_CUDA(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->U[0]) + off, in_b + off, len,
                                        cudaMemcpyHostToDevice, sh));
+        if (gate && memops().write32(sh, (CUdeviceptr)(c->d_h2d_flag + i), c->h2d_seq,
+                                     CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return fail(c, TS_ECUDA, "cuStreamWriteValue32 on an H2D chunk flag failed");
     }
     TS_CUDA(c, tsh::launch_stamp(stamp, 1, sh));
     TS_CUDA(c, cudaEventRecord(c->ev_h2d, sh));
     // the steps
-    TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
+    if (!gate) TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
     // the last step's stage 3 counts finished sub-grids per chunk, and each
     // D2H chunk waits (stream memory op) for its count instead of the stage
     const bool fine = nsteps > 0 && memops().wait32 != nullptr && c->chunk_overlap;
@@ -2081,14 +2114,19 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
         TS_CUDA(c, cudaStreamSynchronize(s));
         std::fill(std::begin(c->chunk_expect), std::end(c->chunk_expect), 0u);
     }
-    rc = do_compute_dt(c);
-    if (rc) return rc;
+    if (gate) {
+        c->h2d_arm = true;
+    } else {
+        rc = do_compute_dt(c);
+        if (rc) return rc;
+    }
     for (uint64_t k = 0; k < nsteps; ++k) {
         c->chunk_arm = fine && k + 1 == nsteps;
         rc = do_step(c);
         c->chunk_arm = false;
         if (rc) return rc;
     }
+    c->h2d_arm = false;
     TS_CUDA(c, cudaEventRecord(c->ev_comp, s));
     // D2H
     if (!fine) TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));

@@ -28,7 +28,9 @@ def test_adapter_feeds_reference_profiler_on_gpu():
     _need()
     r = subprocess.run([ADAPTER, "run"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "hydro_stage1_kernel calls 8" in r.stdout
+    # 4 drop-in steps x 64 sub-grids on 128 streams, no host barrier, bitwise = the batched steps
+    assert "bitwise = batched" in r.stdout
+    assert "hydro_stage1_kernel calls 256" in r.stdout
 
 
 @pytest.mark.gpu
@@ -48,7 +50,7 @@ def test_reference_exporters_show_the_gpu_activity(tmp_path):
     names = {e["name"] for e in dev}
     assert {"hydro_stage1_kernel", "hydro_stage2_kernel", "hydro_stage3_kernel", "multipole_kernel"} <= names
     stage1 = [e for e in dev if e["name"] == "hydro_stage1_kernel"]
-    assert len(stage1) == 8 and all(e["dur"] > 0 for e in stage1)
+    assert len(stage1) == 256 and all(e["dur"] > 0 for e in stage1)
     rows = [line.split(",") for line in csv.read_text().splitlines()[1:]]
-    assert any(row[1] == "hydro_stage1_kernel" and row[2] == "8" for row in rows)
+    assert any(row[1] == "hydro_stage1_kernel" and row[2] == "256" for row in rows)
 
