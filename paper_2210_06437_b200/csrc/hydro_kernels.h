@@ -1,6 +1,7 @@
 // hydro_kernels.h — host-side launch interface of hydro_kernels.cu.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -8,6 +9,12 @@
 namespace tsh {
 
 struct StageArgs {
+    // TMA descriptor of U^{(k-1)} viewed as rows of 16 doubles (128 B):
+    // one {16, 32} box = one field of one sub-grid (4 KiB), 128-byte swizzled
+    // into shared memory (TS_TMA builds; see hydro_stage.cuh).  First member:
+    // the kernel parameter block keeps its 64-byte alignment.
+    CUtensorMap tmap_prev;
+    int tma;                    // 1: the descriptor is valid
     const double* Uprev;        // U^{(k-1)}: owned + proxy sub-grids
     const double* Un;           // U^n (stages 2, 3)
     double* Uout;               // U^{(k)}

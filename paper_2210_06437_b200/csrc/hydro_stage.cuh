@@ -93,25 +93,58 @@ struct StageSmem {
     static constexpr int doubles = dU + cache;
 };
 
-// Shared-memory slot of linear cell offset o = (z*8 + y)*8 + x: rows XOR-swizzled
-// by y so the x sweep's strided column accesses spread over the banks.
-__device__ __forceinline__ int sm_slot(int o) { return o ^ ((o >> 3) & 7); }
+// TS_TMA: the own sub-grid's U^(k-1) (the 6 marched fields) is staged into
+// shared memory by TMA at the start of the stage (cp.async.bulk.tensor, one
+// 4 KiB box per field, 128-byte swizzle); the x sweep — whose pencils are
+// rows, lane-strided 64 B apart in global memory — reads its own-interior
+// values from there and writes its flux differences over them in place (a
+// cell's U^(k-1) is dead once the cell retires), so the stage's shared memory
+// does not grow.  The y and z sweeps read global memory (coalesced) as before.
+#ifndef TS_TMA
+#define TS_TMA 0
+#endif
+
+// Shared-memory slot of linear cell offset o = (z*8 + y)*8 + x.
+//   default: rows XOR-swizzled by y so the x sweep's strided column accesses
+//            spread over the banks;
+//   TS_TMA:  the TMA 128-byte swizzle (16-byte chunk c of 128-byte row r at
+//            c ^ (r & 7)), so the in-place dU and the staged U^(k-1) share one
+//            layout (lanes per bank pair: x 4, y 2, z 2 — y is 4 with sm_slot).
+__device__ __forceinline__ int sm_slot(int o) {
+#if TS_TMA
+    const int r = o >> 4;
+    return (r << 4) + ((((o >> 1) & 7) ^ (r & 7)) << 1) + (o & 1);
+#else
+    return o ^ ((o >> 3) & 7);
+#endif
+}
 
 struct Pencil {
     const double* __restrict__ own;  // field 0 of this sub-grid in U^(k-1)
     const double* __restrict__ lo;   // field 0 of the -axis neighbour (nullptr: outflow)
     const double* __restrict__ hi;   // field 0 of the +axis neighbour (nullptr: outflow)
+    const double* sown;              // TS_TMA x sweep: field 0 of the staged copy (generic pointer into smem)
     int base;                        // offset of pencil cell 0 within a field
     int ss;                          // stride along the pencil
 };
 
 // Address of field 0 at pencil position s (-3 .. 10): the own interior, the
 // face neighbour's interior, or the clamped boundary cell (outflow).  Uniform
-// across the CTA, computed once per face for all fields.
+// across the CTA, computed once per face for all fields.  SM: own cells from
+// the staged shared-memory copy (a generic pointer, read with ld_pen<true>).
+template <bool SM = false>
 __device__ __forceinline__ const double* paddr(const Pencil& p, int s) {
     if (s < 0) return p.lo != nullptr ? p.lo + p.base + (s + N) * p.ss : p.own + p.base;
     if (s >= N) return p.hi != nullptr ? p.hi + p.base + (s - N) * p.ss : p.own + p.base + (N - 1) * p.ss;
+    if (SM) return p.sown + sm_slot(p.base + s * p.ss);
     return p.own + p.base + s * p.ss;
+}
+// Pencil load: read-only global path, or a generic load when the address may
+// be the staged shared-memory copy.
+template <bool SM>
+__device__ __forceinline__ double ld_pen(const double* a) {
+    if (SM) return *a;
+    return __ldg(a);
 }
 
 // Running reconstruction state of one field along the pencil.  On entry to
@@ -128,9 +161,9 @@ struct Recon {
 
 // (Single-lane march only: measured +0.9 % at nf 6; the lane-pair march at
 // nf 11 loses 6 % with it.)
-template <int RECON>
-__device__ __forceinline__ double retiring_up(const Recon& r, const double* own_row, int j, int ss, int fo) {
-    if (RECON == 0 && TS_PPM_RELOAD_UP) return __ldg(own_row + (j - 1) * ss + fo);
+template <int RECON, bool SM = false>
+__device__ __forceinline__ double retiring_up(const Recon& r, const Pencil& p, int j, int fo) {
+    if (RECON == 0 && TS_PPM_RELOAD_UP) return ld_pen<SM>(paddr<SM>(p, j - 1) + fo);
     return r.wp;
 }
 
@@ -150,10 +183,10 @@ struct BeginVals {
     static constexpr int n = RECON == 0 ? 6 : 4;
     double q[n];
 };
-template <int RECON>
+template <int RECON, bool SM = false>
 __device__ __forceinline__ void load_begin(const Pencil& p, int fo, BeginVals<RECON>& b) {
 #pragma unroll
-    for (int i = 0; i < BeginVals<RECON>::n; ++i) b.q[i] = __ldg(paddr(p, i - (RECON == 0 ? 3 : 2)) + fo);
+    for (int i = 0; i < BeginVals<RECON>::n; ++i) b.q[i] = ld_pen<SM>(paddr<SM>(p, i - (RECON == 0 ? 3 : 2)) + fo);
 }
 
 template <int RECON>
@@ -191,20 +224,20 @@ __device__ __forceinline__ void recon_begin_vals(const BeginVals<RECON>& b, Reco
     }
 }
 
-template <int RECON>
+template <int RECON, bool SM = false>
 __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
     BeginVals<RECON> b;
-    load_begin<RECON>(p, fo, b);
+    load_begin<RECON, SM>(p, fo, b);
     recon_begin_vals<RECON>(b, r);
 }
 
 // Advance to face j: returns uL (right edge of cell j-1) and uR (left edge
 // of cell j); `next` is the address (field 0) of the pencil value the next
 // face needs (any valid address after the last face).
-template <int RECON>
+template <int RECON, bool SM = false>
 __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r, double& uL, double& uR) {
     const double q = r.qn;
-    r.qn = __ldg(next + fo);  // `next` is always a valid address (the value is unused after the last face)
+    r.qn = ld_pen<SM>(next + fo);  // `next` is always a valid address (the value is unused after the last face)
     if (RECON == 0) {
         const double dn = q - r.w1;
         const double Dn = mc_slope2(dn, recon_dl(r));
@@ -244,7 +277,11 @@ struct StageCtx {
     const double* __restrict__ Un;
     double* __restrict__ Uout;
     double* scr;  // species accumulator of this sub-grid (field-major, like the state)
+#if TS_TMA
+    double* dU;                  // shared accumulator (aliases the staged U^(k-1) the x sweep reads)
+#else
     double* __restrict__ dU;     // shared accumulator
+#endif
     double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
     size_t own;                  // element offset of the sub-grid's field 0
     double dtdx;                 // 0.5 dt/dx: fluxes are carried doubled (kt2)
@@ -306,10 +343,10 @@ __device__ __forceinline__ void retire_species(const StageCtx& c, int f, int o, 
 }
 
 // Pencil value address for the face after face j (clamped to a valid cell).
-template <int RECON>
+template <int RECON, bool SM = false>
 __device__ __forceinline__ const double* next_addr(const Pencil& p, int j) {
     const int s = j + 3 - RECON;
-    return paddr(p, s < N + 2 ? s : N + 2);
+    return paddr<SM>(p, s < N + 2 ? s : N + 2);
 }
 
 // Face states -> EOS -> Kurganov–Tadmor flux (fields in n, t1, t2 order).
@@ -340,14 +377,14 @@ template <int NF, int RECON, int STAGE, int MODE>
 __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
     const int t = threadIdx.x;
     constexpr bool kUn = STAGE > 1 && MODE == 2;  // U^n needed by the update
+    constexpr bool SM = TS_TMA && MODE == 0;      // own cells from the TMA-staged copy
     int fo[kFA];
 #pragma unroll
     for (int k = 0; k < kFA; ++k) fo[k] = fm[k] * NC;
     Recon r[kFA];
 #pragma unroll
-    for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
+    for (int k = 0; k < kFA; ++k) recon_begin<RECON, SM>(p, fo[k], r[k]);
     const double* un_row = c.Un + c.own + p.base;
-    const double* own_row = p.own + p.base;
     double un[kFA];
     if (kUn) {
 #pragma unroll
@@ -355,10 +392,10 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
     }
     double Fp[kFA];
     {  // face 0
-        const double* next = next_addr<RECON>(p, 0);
+        const double* next = next_addr<RECON, SM>(p, 0);
         double uL[kFA], uR[kFA];
 #pragma unroll
-        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+        for (int k = 0; k < kFA; ++k) recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         double vL, vR, a;
         kt_face(c.e, uL, uR, Fp, vL, vR, a);
         if (NF > kFA) {
@@ -369,12 +406,12 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
     }
 #pragma unroll FaceUnroll<RECON>::value
     for (int j = 1; j < kFaces; ++j) {
-        const double* next = next_addr<RECON>(p, j);
+        const double* next = next_addr<RECON, SM>(p, j);
         double uL[kFA], uR[kFA], up[kFA];
 #pragma unroll
         for (int k = 0; k < kFA; ++k) {
-            up[k] = retiring_up<RECON>(r[k], own_row, j, p.ss, fo[k]);  // U^(k-1) of cell j-1, retired here
-            recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+            up[k] = retiring_up<RECON, SM>(r[k], p, j, fo[k]);  // U^(k-1) of cell j-1, retired here
+            recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         }
         double F[kFA], vL, vR, a;
         kt_face(c.e, uL, uR, F, vL, vR, a);
@@ -420,7 +457,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
                 double uL, uR;
-                const double upf = retiring_up<RECON>(q, own_row, j, p.ss, fof);
+                const double upf = retiring_up<RECON>(q, p, j, fof);
                 recon_step<RECON>(next_addr<RECON>(p, j), fof, q, uL, uR);
                 const double vL = c.cache[(j * 3 + 0) * kPencils + t];
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
@@ -698,9 +735,53 @@ __device__ __forceinline__ double level_dx(const StageArgs& A, int g) {
     return dx;
 }
 
+// TMA helpers (TS_TMA): mbarrier-tracked 2-D tensor copies into shared memory.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TS_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Dynamic shared memory of a stage CTA: the dU accumulator (TS_TMA: 1024-byte
+// aligned for the 128-byte swizzle, plus the mbarrier) and the nf > 6 cache.
+template <int NF>
+constexpr size_t stage_smem_bytes() {
+    return (size_t)StageSmem<NF>::doubles * sizeof(double) + (TS_TMA ? 1024 + 16 : 0);
+}
+
 template <int NF, int RECON, int STAGE>
-__global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(StageArgs A) {
-    extern __shared__ double smem[];
+__global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(const __grid_constant__ StageArgs A) {
+    extern __shared__ __align__(16) double smem_raw[];
+#if TS_TMA
+    double* smem = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    unsigned long long* tma_bar = reinterpret_cast<unsigned long long*>(smem + StageSmem<NF>::doubles);
+#else
+    double* smem = smem_raw;
+#endif
     if (A.stamp != nullptr && threadIdx.x == 0)
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
     if (A.cta_log != nullptr && threadIdx.x == 0) {
@@ -753,6 +834,24 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         }
         __syncthreads();
     }
+#if TS_TMA
+    // Stage the own sub-grid's U^(k-1) (the marched fields) into the dU
+    // buffer: its flags were acquired above, and the x sweep overwrites each
+    // cell with its flux difference once the cell retired.
+    const bool staged = !Lanes<NF>::pair;
+    if (staged && A.tma == 0) __trap();  // a TS_TMA build needs the descriptor (stage_args sets it)
+    if (staged) {
+        if (threadIdx.x == 0) {
+            mbar_init(tma_bar, 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(tma_bar, (unsigned)(kFA * NC * sizeof(double)));
+            const int g_row = g * NF * (NC / 16);
+#pragma unroll
+            for (int f = 0; f < kFA; ++f) tma_load_2d(smem + f * NC, &A.tmap_prev, 0, g_row + f * (NC / 16), tma_bar);
+        }
+        __syncthreads();  // mbarrier initialised before anyone waits on it
+    }
+#endif
     // TS_LAZY_DT: dt enters only the z sweep's update, so its two IEEE
     // divisions can be done there, off the CTA's start-up path
     if (A.cta_log != nullptr && t == 0) A.cta_log[4 * blockIdx.x + 2] = globaltimer();
@@ -792,6 +891,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         const int nhi = __ldg(A.nbr + 6 * g + 2 * axis + 1);
         Pencil p;
         p.own = own;
+        p.sown = nullptr;
+#if TS_TMA
+        if (axis == 0 && staged) {
+            p.sown = smem;
+            mbar_wait(tma_bar, 0);
+        }
+#endif
         p.lo = nlo >= 0 ? A.Uprev + (size_t)nlo * NF * NC : nullptr;
         p.hi = nhi >= 0 ? A.Uprev + (size_t)nhi * NF * NC : nullptr;
         p.base = axis == 0 ? (b * N + a) * N : (axis == 1 ? b * N * N + a : b * N + a);
@@ -898,7 +1004,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 
 template <int NF, int RECON, int STAGE>
 inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
-    const size_t smem = (size_t)StageSmem<NF>::doubles * sizeof(double);
+    const size_t smem = stage_smem_bytes<NF>();
     // the dynamic shared-memory limit is a per-device function attribute:
     // set it once on every device this instantiation is launched on
     static std::atomic<unsigned long long> configured{0ull};

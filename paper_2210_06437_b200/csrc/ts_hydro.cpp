@@ -130,6 +130,10 @@ struct PendingLaunch {
     uint32_t slot;  // stamp slot
     bool overlap;   // PDL launch: may start before the previous kernel on its stream ended
     uint64_t bytes = 0;  // copies (ts_hydro_enqueue_copy)
+    // Copies of the pipelined host path are timed by CUDA events, not stamp
+    // kernels: a copy stream must never need an SM (stage-1 CTAs waiting for
+    // the H2D chunks may hold every SM slot until the copies land).
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
 // Stream memory operation (driver API, resolved through the runtime so the
@@ -235,6 +239,8 @@ struct ts_hydro_ctx {
 
     // device memory
     double* U[3] = {nullptr, nullptr, nullptr};
+    CUtensorMap tmap[3];           // TMA view of each state buffer: rows of 16 doubles, {16, 32} boxes
+    bool tmap_ok = false;
     int32_t* d_nbr = nullptr;
     std::vector<int64_t> mesh_nbr;    // the bound global mesh (checkpoints)
     std::vector<int32_t> mesh_owner;
@@ -255,7 +261,11 @@ struct ts_hydro_ctx {
     double* d_dt_hist = nullptr;  // [kDtHist]
     static constexpr uint64_t kDtHist = 4096;
     unsigned long long* d_stamps = nullptr;  // [cap][2]
-    unsigned long long* h_clock = nullptr;   // mapped pinned: [0] clock calibration, [1] cross-GPU wait timeout
+    unsigned long long* h_clock = nullptr;   // mapped pinned: [0] clock calibration, [1] cross-GPU wait timeout,
+                                             //   [2] globaltimer at ev_cal (event-timed copies)
+    cudaEvent_t ev_cal = nullptr;            // reference event of the event-timed records
+    bool cal_armed = false;                  // ev_cal / h_clock[2] recorded since the last harvest
+    std::vector<cudaEvent_t> ev_pool;        // timing events for copy records
     unsigned long long wait_ns = 30ull * 1000000000ull;
     std::map<void*, uint64_t> dev_allocs;
     std::map<void*, uint64_t> host_allocs;
@@ -491,6 +501,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_amr_level);
     c->amr = false;
     c->have_mesh = false;
+    c->tmap_ok = false;
 }
 
 // Harvest the stamps of every pending launch (device must be idle).
@@ -515,8 +526,20 @@ int harvest(ts_hydro_ctx* c) {
             r.has_bytes = 1;
             r.bytes = p.bytes;
         }
-        const unsigned long long enc_start = st[2 * (size_t)p.slot];
-        const unsigned long long end = st[2 * (size_t)p.slot + 1];
+        unsigned long long enc_start = st[2 * (size_t)p.slot];
+        unsigned long long end = st[2 * (size_t)p.slot + 1];
+        if (p.e0 != nullptr) {
+            // event-timed: globaltimer of ev_cal + elapsed event time
+            float ms0 = 0.0f, ms1 = 0.0f;
+            const unsigned long long g0 = ((volatile unsigned long long*)c->h_clock)[2];
+            if (cudaEventElapsedTime(&ms0, c->ev_cal, p.e0) != cudaSuccess ||
+                cudaEventElapsedTime(&ms1, c->ev_cal, p.e1) != cudaSuccess) {
+                (void)cudaGetLastError();
+                continue;
+            }
+            enc_start = ~(g0 + (unsigned long long)std::llround(std::max(0.0f, ms0) * 1e6));
+            end = g0 + (unsigned long long)std::llround(std::max(ms0, ms1) * 1e6);
+        }
         if (enc_start == 0 || end == 0) continue;  // launch had no CTA (empty)
         const unsigned long long start = ~enc_start;
         r.start_ns = (uint64_t)((int64_t)start + c->clock_offset);
@@ -528,7 +551,12 @@ int harvest(ts_hydro_ctx* c) {
         it->second = std::max(it->second, r.end_ns);
         c->completed.push_back(r);
     }
+    for (const PendingLaunch& p : c->pending) {
+        if (p.e0 != nullptr) c->ev_pool.push_back(p.e0);
+        if (p.e1 != nullptr) c->ev_pool.push_back(p.e1);
+    }
     c->pending.clear();
+    c->cal_armed = false;
     c->next_slot = 0;
     TS_CUDA(c, cudaMemset(c->d_stamps, 0, (size_t)cap * 2 * sizeof(unsigned long long)));
     // legacy-stream work does not order against our non-blocking streams
@@ -573,6 +601,38 @@ int begin_launch(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream
 }
 
 // Host-timed copy record (synchronous copies).
+// An event-timed record (see PendingLaunch::e0): the reference event ev_cal is
+// recorded on the compute stream right behind a one-thread clock kernel
+// (globaltimer into h_clock[2]) once per harvest period.
+int begin_event_record(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream_id, uint64_t bytes,
+                       PendingLaunch** out) {
+    unsigned long long* stamp = nullptr;
+    int rc = begin_launch(c, kind, name, stream_id, 0, &stamp);
+    if (rc) return rc;
+    c->launches--;  // no kernel
+    if (!c->cal_armed) {
+        cudaStream_t s0;
+        rc = ensure_stream(c, 0, &s0);
+        if (rc) return rc;
+        if (c->ev_cal == nullptr) TS_CUDA(c, cudaEventCreate(&c->ev_cal));
+        TS_CUDA(c, tsh::launch_clock(c->h_clock + 2, s0));
+        TS_CUDA(c, cudaEventRecord(c->ev_cal, s0));
+        c->cal_armed = true;
+    }
+    PendingLaunch& p = c->pending.back();
+    for (cudaEvent_t* e : {&p.e0, &p.e1}) {
+        if (!c->ev_pool.empty()) {
+            *e = c->ev_pool.back();
+            c->ev_pool.pop_back();
+        } else {
+            TS_CUDA(c, cudaEventCreate(e));
+        }
+    }
+    p.bytes = bytes;
+    *out = &p;
+    return TS_OK;
+}
+
 void record_copy(ts_hydro_ctx* c, uint8_t kind, uint64_t bytes, uint64_t t0, uint64_t t1) {
     ts_activity_record r{};
     r.kind = kind;
@@ -703,6 +763,10 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     double* B = c->U[1];
     double* C = c->U[2];
     a.Uprev = stage == 1 ? A : (stage == 2 ? B : C);
+    if (c->tmap_ok) {
+        a.tmap_prev = c->tmap[stage - 1];  // U[0], U[1], U[2] = A, B, C
+        a.tma = 1;
+    }
     a.Un = A;
     a.Uout = stage == 1 ? B : (stage == 2 ? C : A);
     // free during the stage: stage 1 writes B (C unused), stage 2 writes C,
@@ -1378,7 +1442,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
         rc = cuda_fail(c, e, "cudaMemset");
     if (!rc && (e = cudaMemset(c->d_scal, 0, 8 * sizeof(double))) != cudaSuccess) rc = cuda_fail(c, e, "cudaMemset");
     if (!rc && (e = cudaDeviceSynchronize()) != cudaSuccess) rc = cuda_fail(c, e, "cudaDeviceSynchronize");
-    if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, 2 * sizeof(unsigned long long), cudaHostAllocMapped)) !=
+    if (!rc && (e = cudaHostAlloc((void**)&c->h_clock, 3 * sizeof(unsigned long long), cudaHostAllocMapped)) !=
                    cudaSuccess)
         rc = cuda_fail(c, e, "cudaHostAlloc");
     if (!rc) c->h_clock[1] = 0ull;
@@ -1444,6 +1508,13 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
         if (ctx->h_clock) cudaFreeHost(ctx->h_clock);
         if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+        if (ctx->ev_cal) cudaEventDestroy(ctx->ev_cal);
+        if (ctx->ev_din) cudaEventDestroy(ctx->ev_din);
+        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+        for (const PendingLaunch& p : ctx->pending) {
+            if (p.e0) cudaEventDestroy(p.e0);
+            if (p.e1) cudaEventDestroy(p.e1);
+        }
         if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
         if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
         if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
@@ -1576,6 +1647,37 @@ int ts_hydro_set_mesh(ts_hydro_ctx* c, int64_t n, const int64_t* nbr, const int3
 
 // Device side of a mesh whose owned / proxy lists, local neighbour table and
 // interior / boundary lists are in place (ts_hydro_set_mesh, _set_amr_mesh).
+// TMA descriptors of the three state buffers (used by TS_TMA kernel builds):
+// a buffer as a 2-D tensor of 128-byte rows (16 doubles), rows = slots x nf x
+// 32; one {16, 32} box = one 4 KiB field of one sub-grid, 128-byte swizzle.
+// cuTensorMapEncodeTiled is resolved through the runtime (no link-time libcuda).
+static int encode_tmaps(ts_hydro_ctx* c) {
+    c->tmap_ok = false;
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode enc = nullptr;
+    if (enc == nullptr) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+            return TS_OK;  // no TMA descriptors: TS_TMA builds trap, the default build never reads them
+        enc = reinterpret_cast<Encode>(f);
+    }
+    const cuuint64_t rows = (cuuint64_t)(c->n_owned + c->n_proxy) * (cuuint64_t)c->nf * (kNC / 16);
+    const cuuint64_t dims[2] = {16, rows};
+    const cuuint64_t strides[1] = {16 * sizeof(double)};
+    const cuuint32_t box[2] = {16, kNC / 16};
+    const cuuint32_t estr[2] = {1, 1};
+    for (int k = 0; k < 3; ++k)
+        if (enc(&c->tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->U[k], dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(c, TS_ECUDA, "cuTensorMapEncodeTiled failed for a state buffer");
+    c->tmap_ok = true;
+    return TS_OK;
+}
+
 static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, int32_t world) {
     int rc = build_plans(c, nbr, owner);
     if (rc) return rc;
@@ -1590,7 +1692,8 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         if (rc) return rc;
         TS_CUDA(c, cudaMemset(b, 0, elems * sizeof(double)));
     }
-    rc = dalloc(c, &c->d_nbr, (size_t)nl * 6);
+    rc = encode_tmaps(c);
+    if (!rc) rc = dalloc(c, &c->d_nbr, (size_t)nl * 6);
     if (!rc) rc = dalloc(c, &c->d_interior, c->interior.size());
     if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
     if (!rc) rc = dalloc(c, &c->d_order, (size_t)c->n_owned);
@@ -2083,11 +2186,11 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     // the previous call's D2H reads U^n: chunk-wise behind it when chained,
     // else behind all of it (an unrecorded event is a no-op wait)
     if (!chained) TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[C - 1], 0));
-    unsigned long long* stamp = nullptr;
-    rc = begin_launch(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, 0, &stamp);
+    PendingLaunch* rec = nullptr;
+    rc = begin_event_record(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, bytes, &rec);
     if (rc) return rc;
-    c->pending.back().bytes = bytes;
-    TS_CUDA(c, tsh::launch_stamp(stamp, 0, sh));
+    cudaEvent_t h2d_e1 = rec->e1;
+    TS_CUDA(c, cudaEventRecord(rec->e0, sh));
     for (int i = 0; i < C; ++i) {
         size_t off, len;
         chunk(i, &off, &len);
@@ -2099,7 +2202,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
                                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
             return fail(c, TS_ECUDA, "cuStreamWriteValue32 on an H2D chunk flag failed");
     }
-    TS_CUDA(c, tsh::launch_stamp(stamp, 1, sh));
+    TS_CUDA(c, cudaEventRecord(h2d_e1, sh));
     TS_CUDA(c, cudaEventRecord(c->ev_h2d, sh));
     // the steps
     if (!gate) TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
@@ -2130,10 +2233,10 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     TS_CUDA(c, cudaEventRecord(c->ev_comp, s));
     // D2H
     if (!fine) TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));
-    rc = begin_launch(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, 0, &stamp);
+    rc = begin_event_record(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, bytes, &rec);
     if (rc) return rc;
-    c->pending.back().bytes = bytes;
-    TS_CUDA(c, tsh::launch_stamp(stamp, 0, sd));
+    cudaEvent_t d2h_e1 = rec->e1;
+    TS_CUDA(c, cudaEventRecord(rec->e0, sd));
     char* out_b = reinterpret_cast<char*>(host_out);
     for (int i = 0; i < C; ++i) {
         size_t off, len;
@@ -2149,7 +2252,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
                                        cudaMemcpyDeviceToHost, sd));
         TS_CUDA(c, cudaEventRecord(c->ev_d2h[i], sd));
     }
-    TS_CUDA(c, tsh::launch_stamp(stamp, 1, sd));
+    TS_CUDA(c, cudaEventRecord(d2h_e1, sd));
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(sd, done_host, new DoneThunk{done, user, nullptr}));
     c->prev_out = host_out;
     c->prev_out_bytes = bytes;
