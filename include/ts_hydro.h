@@ -324,6 +324,12 @@ int ts_hydro_debug_cta_log(ts_hydro_ctx* ctx, uint64_t* out, uint64_t cap, uint6
 
 /* ---- timing hook -------------------------------------------------------------- */
 int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void* user);
+/* The profiling arms of the reference's overhead harness (ProfilingArm,
+ * harness.hpp; arm_config harness.cpp:33-52): enabled (default) = every
+ * launch stamps its activity record ("full"); 0 = no stamps and no records
+ * ("disabled": profiler.enabled = false).  compute_overhead of the two step
+ * times is the per-kernel timing hook's o(n) (harness.cpp:15-20). */
+int ts_hydro_set_profiling(ts_hydro_ctx* ctx, int32_t enabled);
 /* SimDevice::flush_activity: waits for in-flight work, returns completed
  * records not yet delivered (at most once).  out == NULL -> count only. */
 int ts_hydro_flush_activity(ts_hydro_ctx* ctx, ts_activity_record* out, uint64_t cap, uint64_t* n_out);

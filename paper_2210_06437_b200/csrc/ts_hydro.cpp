@@ -351,6 +351,7 @@ struct ts_hydro_ctx {
     uint64_t steps_done = 0;
     uint64_t launches = 0;
     bool dt_valid = false;
+    bool profiling = true;  // ts_hydro_set_profiling: activity stamps and records on every launch
 
     // activity
     std::vector<PendingLaunch> pending;  // launches holding a stamp slot
@@ -593,6 +594,11 @@ int begin_launch(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream
         if (rc) return rc;
         deliver_to_sink(c);
     }
+    if (!c->profiling) {  // the harness's "disabled" arm: no stamps, no records
+        *stamp = nullptr;
+        c->launches++;
+        return TS_OK;
+    }
     const uint32_t slot = c->next_slot++;
     c->pending.push_back({kind, name, stream_id, guid, slot, false});
     *stamp = c->d_stamps + 2 * (size_t)slot;
@@ -607,9 +613,11 @@ int begin_launch(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream
 int begin_event_record(ts_hydro_ctx* c, uint8_t kind, const char* name, int32_t stream_id, uint64_t bytes,
                        PendingLaunch** out) {
     unsigned long long* stamp = nullptr;
+    *out = nullptr;
     int rc = begin_launch(c, kind, name, stream_id, 0, &stamp);
     if (rc) return rc;
     c->launches--;  // no kernel
+    if (stamp == nullptr) return TS_OK;  // profiling disabled
     if (!c->cal_armed) {
         cudaStream_t s0;
         rc = ensure_stream(c, 0, &s0);
@@ -800,7 +808,7 @@ int launch_stage_list(ts_hydro_ctx* c, tsh::StageArgs a, int stage, const int32_
     unsigned long long* stamp = nullptr;
     rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)stream_id, guid, &stamp);
     if (rc) return rc;
-    c->pending.back().overlap = pdl;
+    if (stamp != nullptr) c->pending.back().overlap = pdl;
     a.list = d_list;
     a.first = first;
     a.stamp = stamp;
@@ -2189,8 +2197,8 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     PendingLaunch* rec = nullptr;
     rc = begin_event_record(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, bytes, &rec);
     if (rc) return rc;
-    cudaEvent_t h2d_e1 = rec->e1;
-    TS_CUDA(c, cudaEventRecord(rec->e0, sh));
+    cudaEvent_t h2d_e1 = rec != nullptr ? rec->e1 : nullptr;
+    if (rec != nullptr) TS_CUDA(c, cudaEventRecord(rec->e0, sh));
     for (int i = 0; i < C; ++i) {
         size_t off, len;
         chunk(i, &off, &len);
@@ -2202,7 +2210,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
                                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
             return fail(c, TS_ECUDA, "cuStreamWriteValue32 on an H2D chunk flag failed");
     }
-    TS_CUDA(c, cudaEventRecord(h2d_e1, sh));
+    if (h2d_e1 != nullptr) TS_CUDA(c, cudaEventRecord(h2d_e1, sh));
     TS_CUDA(c, cudaEventRecord(c->ev_h2d, sh));
     // the steps
     if (!gate) TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d, 0));
@@ -2235,8 +2243,8 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     if (!fine) TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_comp, 0));
     rc = begin_event_record(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, bytes, &rec);
     if (rc) return rc;
-    cudaEvent_t d2h_e1 = rec->e1;
-    TS_CUDA(c, cudaEventRecord(rec->e0, sd));
+    cudaEvent_t d2h_e1 = rec != nullptr ? rec->e1 : nullptr;
+    if (rec != nullptr) TS_CUDA(c, cudaEventRecord(rec->e0, sd));
     char* out_b = reinterpret_cast<char*>(host_out);
     for (int i = 0; i < C; ++i) {
         size_t off, len;
@@ -2252,7 +2260,7 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
                                        cudaMemcpyDeviceToHost, sd));
         TS_CUDA(c, cudaEventRecord(c->ev_d2h[i], sd));
     }
-    TS_CUDA(c, cudaEventRecord(d2h_e1, sd));
+    if (d2h_e1 != nullptr) TS_CUDA(c, cudaEventRecord(d2h_e1, sd));
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(sd, done_host, new DoneThunk{done, user, nullptr}));
     c->prev_out = host_out;
     c->prev_out_bytes = bytes;
@@ -2622,6 +2630,14 @@ int ts_hydro_set_activity_sink(ts_hydro_ctx* c, ts_activity_sink_fn sink, void* 
     return TS_OK;
 }
 
+int ts_hydro_set_profiling(ts_hydro_ctx* c, int32_t enabled) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->profiling = enabled != 0;
+    return TS_OK;
+}
+
 int ts_hydro_flush_activity(ts_hydro_ctx* c, ts_activity_record* out, uint64_t cap, uint64_t* n_out) {
     if (c == nullptr || n_out == nullptr) return TS_EINVAL;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
@@ -2810,7 +2826,7 @@ int ts_hydro_enqueue_copy(ts_hydro_ctx* c, int32_t kind, uint64_t bytes, uint32_
     unsigned long long* stamp = nullptr;
     rc = begin_launch(c, (uint8_t)kind, name, (int32_t)stream_id, guid, &stamp);
     if (rc) return rc;
-    c->pending.back().bytes = bytes;
+    if (stamp != nullptr) c->pending.back().bytes = bytes;
     char* d = static_cast<char*>(c->stage_dev);
     TS_CUDA(c, tsh::launch_stamp(stamp, 0, s));
     if (kind == TS_ACTIVITY_COPY_H2D)

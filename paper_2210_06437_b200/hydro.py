@@ -152,6 +152,7 @@ _SIGNATURES = {
     "ts_hydro_p2p_export": (ctypes.c_int, [_vp, ctypes.c_void_p]),
     "ts_hydro_p2p_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32]),
     "ts_hydro_set_activity_sink": (ctypes.c_int, [_vp, SINK_FN, _vp]),
+    "ts_hydro_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "ts_hydro_flush_activity": (ctypes.c_int, [_vp, ctypes.POINTER(_Record), ctypes.c_uint64, _u64p]),
     "ts_hydro_memory_state": (ctypes.c_int, [_vp, ctypes.POINTER(_MemState)]),
     "ts_hydro_clock_ns": (ctypes.c_uint64, []),
@@ -659,6 +660,10 @@ class CudaDevice:
                                r.end_ns, r.bytes if r.has_bytes else None, r.correlation_guid)
                 for r in buf[:n.value]]
 
+    def set_profiling(self, enabled: bool) -> None:
+        """ProfilingArm full (True) / disabled (False): activity stamps and records on or off."""
+        self._check(lib().ts_hydro_set_profiling(self._h, 1 if enabled else 0), "set_profiling")
+
     def set_activity_sink(self, fn) -> None:
         def thunk(recs, n, _u):
             fn([ActivityRecord(ACTIVITY_KINDS[recs[i].kind], recs[i].name.decode(), recs[i].device_id,
@@ -781,6 +786,94 @@ class WorkloadSession:
         seconds = time.perf_counter() - t0
         return ScalingPoint(n=self.mesh.world_size, total_time_s=seconds,
                             cells_per_second=self.mesh.total_cells() * self.config.num_steps / seconds)
+
+
+# ---------------------------------------------------------------------------
+# Overhead / scaling harness (reference proj/core/src/harness.cpp): the
+# profiling-overhead percentage, the sweep rows derived from per-count times,
+# and the CSV writer — restated so a sweep over GPU counts produces the
+# reference's own row format.  The "with" arm runs the per-kernel timing hook
+# (activity stamps), "without" runs with it disabled (ts_hydro_set_profiling).
+# ---------------------------------------------------------------------------
+def compute_overhead(n: int, comp_apex_s: float, comp_no_apex_s: float) -> float:
+    """harness.cpp:15-20: (with / without) * 100 - 100 percent."""
+    del n
+    if not comp_no_apex_s > 0.0:
+        raise ValueError("overhead baseline must be positive")
+    return (comp_apex_s / comp_no_apex_s) * 100.0 - 100.0
+
+
+@dataclasses.dataclass
+class SweepRow:
+    """harness.hpp:66-75."""
+    n: int = 1
+    time_with_s: float = 0.0
+    time_without_s: float = 0.0
+    cells_per_second_with: float = 0.0
+    cells_per_second_without: float = 0.0
+    o_percent: float = 0.0
+    speedup_with: float = 1.0     # relative to the smallest count, same arm
+    speedup_without: float = 1.0
+
+
+def _validate_counts(counts: Sequence[int]) -> None:
+    """harness.cpp:125-132."""
+    if len(counts) == 0:
+        raise ValueError("sweep needs at least one locality count")
+    for i, c in enumerate(counts):
+        if c < 1:
+            raise ValueError("locality counts must be positive")
+        if i > 0 and c <= counts[i - 1]:
+            raise ValueError("locality counts must be strictly ascending")
+
+
+def sweep_rows_from_times(total_cells: int, num_steps: int, counts: Sequence[int], with_s: Sequence[float],
+                          without_s: Sequence[float]) -> list:
+    """harness.cpp:136-167.  cells processed = the world-1 mesh's total cells
+    x num_steps (the reference rebuilds build_mesh(levels, 1, ...) for it;
+    here the caller passes that mesh's total_cells — for weak scaling the
+    per-count mesh differs, and tools/sweep.py passes each row's own)."""
+    _validate_counts(counts)
+    if len(with_s) != len(counts) or len(without_s) != len(counts):
+        raise ValueError("sweep needs one time per arm per locality count")
+    for a, b in zip(with_s, without_s):
+        if not (a > 0.0) or not (b > 0.0):
+            raise ValueError("sweep times must be positive")
+    cells_processed = float(total_cells) * float(num_steps)
+    rows = []
+    for i, n in enumerate(counts):
+        rows.append(SweepRow(n=n, time_with_s=with_s[i], time_without_s=without_s[i],
+                             cells_per_second_with=cells_processed / with_s[i],
+                             cells_per_second_without=cells_processed / without_s[i],
+                             o_percent=compute_overhead(n, with_s[i], without_s[i]),
+                             speedup_with=with_s[0] / with_s[i], speedup_without=without_s[0] / without_s[i]))
+    return rows
+
+
+def write_sweep_csv(out, rows) -> None:
+    """harness.cpp:188-201: fixed header, doubles as %.17g (exact round trip)."""
+    out.write("n,time_with,time_without,cells_per_second_with,cells_per_second_without,"
+              "o_percent,speedup_with,speedup_without\n")
+    for r in rows:
+        vals = (r.time_with_s, r.time_without_s, r.cells_per_second_with, r.cells_per_second_without,
+                r.o_percent, r.speedup_with, r.speedup_without)
+        out.write(str(r.n) + "".join("," + ("%.17g" % v) for v in vals) + "\n")
+
+
+def measure_arm(session: "WorkloadSession", profiling: bool, repetitions: int = 3) -> float:
+    """harness.cpp:72-101 on the GPU: min over repetitions of the timed
+    stepping (run_benchmark) with the timing hook on (full) or off (disabled)."""
+    if repetitions < 1:
+        raise ValueError("repetitions must be positive")
+    session.device.set_profiling(profiling)
+    try:
+        best = float("inf")
+        for _ in range(repetitions):
+            best = min(best, session.run_benchmark().total_time_s)
+    finally:
+        session.device.set_profiling(True)
+    session.device.flush_activity()
+    return best
 
 
 # ---------------------------------------------------------------------------
