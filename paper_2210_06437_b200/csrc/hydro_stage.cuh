@@ -53,6 +53,27 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 #define TS_PPM_RELOAD_UP 1
 #endif
 
+#ifndef TS_PREFETCH
+#define TS_PREFETCH 1
+#endif
+// U^n of the retiring cell (stages 2, 3, z sweep): loaded at the top of the
+// face that retires it (not carried across faces: 12 fewer loop-carried
+// registers) instead of prefetched one face ahead.
+#ifndef TS_UN_LATE
+#define TS_UN_LATE 0
+#endif
+// L1 prefetch one face beyond the register prefetch (ncu source view: ptxas
+// sinks the pencil / U^n loads of a face to the end of the previous one, so
+// the face's first instructions wait on them).  Bit 0: the next pencil
+// values, bit 1: U^n of the next retiring cell, bit 2: the retiring cell's
+// U^(k-1) reload.  Applied in the sweeps set by TS_PF_L1_MODES (bit m = mode m).
+#ifndef TS_PF_L1
+#define TS_PF_L1 0
+#endif
+#ifndef TS_PF_L1_MODES
+#define TS_PF_L1_MODES 4
+#endif
+
 constexpr int kFA = 6;        // fields marched together: rho, s_n, s_t1, s_t2, E, tau
 constexpr int kFaces = N + 1;
 
@@ -161,9 +182,12 @@ struct Recon {
 
 // (Single-lane march only: measured +0.9 % at nf 6; the lane-pair march at
 // nf 11 loses 6 % with it.)
-template <int RECON, bool SM = false>
+#ifndef TS_RELOAD_UP_MODES
+#define TS_RELOAD_UP_MODES 7  // sweeps (bit = mode) that reload rather than carry
+#endif
+template <int RECON, bool SM = false, int MODE = 0>
 __device__ __forceinline__ double retiring_up(const Recon& r, const Pencil& p, int j, int fo) {
-    if (RECON == 0 && TS_PPM_RELOAD_UP) return ld_pen<SM>(paddr<SM>(p, j - 1) + fo);
+    if (RECON == 0 && TS_PPM_RELOAD_UP && ((TS_RELOAD_UP_MODES >> MODE) & 1)) return ld_pen<SM>(paddr<SM>(p, j - 1) + fo);
     return r.wp;
 }
 
@@ -234,6 +258,10 @@ __device__ __forceinline__ void recon_begin(const Pencil& p, int fo, Recon& r) {
 // Advance to face j: returns uL (right edge of cell j-1) and uR (left edge
 // of cell j); `next` is the address (field 0) of the pencil value the next
 // face needs (any valid address after the last face).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <int RECON, bool SM = false>
 __device__ __forceinline__ void recon_step(const double* next, int fo, Recon& r, double& uL, double& uR) {
     const double q = r.qn;
@@ -386,7 +414,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
     for (int k = 0; k < kFA; ++k) recon_begin<RECON, SM>(p, fo[k], r[k]);
     const double* un_row = c.Un + c.own + p.base;
     double un[kFA];
-    if (kUn) {
+    if (kUn && !TS_UN_LATE) {
 #pragma unroll
         for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + fo[k]);
     }
@@ -407,10 +435,22 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll FaceUnroll<RECON>::value
     for (int j = 1; j < kFaces; ++j) {
         const double* next = next_addr<RECON, SM>(p, j);
+        if (TS_PF_L1 != 0 && ((TS_PF_L1_MODES >> MODE) & 1) && !SM) {
+            const double* nn = next_addr<RECON>(p, j + 1 < kFaces ? j + 1 : j);
+            const double* un_nn = c.Un + c.own + p.base + (j < N ? j : N - 1) * p.ss;
+            const double* up_nn = p.own + p.base + (j < N ? j : N - 1) * p.ss;
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) {
+                if (TS_PF_L1 & 1) prefetch_l1(nn + fo[k]);
+                if ((TS_PF_L1 & 2) && kUn) prefetch_l1(un_nn + fo[k]);
+                if (TS_PF_L1 & 4) prefetch_l1(up_nn + fo[k]);
+            }
+        }
         double uL[kFA], uR[kFA], up[kFA];
 #pragma unroll
         for (int k = 0; k < kFA; ++k) {
-            up[k] = retiring_up<RECON, SM>(r[k], p, j, fo[k]);  // U^(k-1) of cell j-1, retired here
+            up[k] = retiring_up<RECON, SM, MODE>(r[k], p, j, fo[k]);  // U^(k-1) of cell j-1, retired here
+            if (kUn && TS_UN_LATE) un[k] = __ldg(un_row + (j - 1) * p.ss + fo[k]);
             recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         }
         double F[kFA], vL, vR, a;
@@ -426,7 +466,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
         if (STAGE == 3 && MODE == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
             amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
-        if (kUn) {
+        if (kUn && !TS_UN_LATE) {
             const int jn = j < N ? j : N - 1;  // cell retired at the next face (a dummy reload after the last)
 #pragma unroll
             for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + jn * p.ss + fo[k]);
@@ -765,6 +805,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// L2 prefetch of a contiguous range (one instruction, no registers, no
+// completion to wait for: a hint that turns the first touch of U^n in the
+// z sweep from an HBM miss into an L2 hit).
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Dynamic shared memory of a stage CTA: the dU accumulator (TS_TMA: 1024-byte
 // aligned for the 128-byte swizzle, plus the mbarrier) and the nf > 6 cache.
 template <int NF>
@@ -784,6 +831,16 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 #endif
     if (A.stamp != nullptr && threadIdx.x == 0)
         atomicMax(A.stamp, ~globaltimer());  // start stored inverted: one zero-initialised ring serves both ends
+#if TS_PREFETCH
+    // U^n of this sub-grid is first read by the z sweep, one face ahead of
+    // its use: measured (ncu source view) as the z sweep's long-scoreboard
+    // stall in stages 2 and 3.  Ask L2 for all of it now.
+    if (STAGE > 1 && threadIdx.x == 32) {
+        const int gp = A.list_inline_n > 0 ? A.list_inline[blockIdx.x]
+                       : (A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x);
+        prefetch_l2(A.Un + (size_t)gp * NF * NC, (unsigned)(NF * NC * sizeof(double)));
+    }
+#endif
     if (A.cta_log != nullptr && threadIdx.x == 0) {
         unsigned int sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
