@@ -215,10 +215,18 @@ int ts_hydro_launch_count(const ts_hydro_ctx* ctx, uint64_t* launches);
 
 /* The compute_fluxes drop-in (workload.cpp:544-552): one fused RK stage
  * (1..3) over `count` owned sub-grids on stream `stream_id`; `done` fires once
- * the device finished.  dt comes from the last ts_hydro_compute_dt. */
+ * the device finished.  Stage 1 opens a step; every owned sub-grid then runs
+ * stages 1, 2, 3 once, in that order, in any interleaving across sub-grids
+ * and streams — no host barrier: each CTA waits on the device for its own
+ * and its face neighbours' previous stage (and stage 1 for the previous
+ * step's stage-3 count, which carries dt); a launch whose producers were not
+ * issued yet is parked and issued once they are.  dt: ts_hydro_compute_dt
+ * before the first step, then from the device.  Single rank (TS_ESTATE
+ * otherwise); state-changing calls fail with TS_ESTATE while a step is open. */
 int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned_index, int64_t count,
                           uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
-/* Rotate buffers after a manual stage-3 sequence. */
+/* Close the open per-sub-grid step (every owned sub-grid launched stage 3):
+ * joins the step's streams into the compute stream, no host wait. */
 int ts_hydro_finish_step(ts_hydro_ctx* ctx);
 
 /* ---- ghost exchange --------------------------------------------------------- */
