@@ -338,6 +338,16 @@ int ts_hydro_set_activity_sink(ts_hydro_ctx* ctx, ts_activity_sink_fn sink, void
  * ("disabled": profiler.enabled = false).  compute_overhead of the two step
  * times is the per-kernel timing hook's o(n) (harness.cpp:15-20). */
 int ts_hydro_set_profiling(ts_hydro_ctx* ctx, int32_t enabled);
+
+/* Self-check builds (TS_CHECK=1; the race / bounds detector standing in for
+ * compute-sanitizer, which this pool does not allow — DESIGN.md §13): the
+ * stage kernels bounds-check every state load / store and re-check every
+ * acquired dataflow / halo flag at CTA exit.  out = {failures, first code,
+ * operand a, operand b, OR of (1 << code) over all failures}; waits for the
+ * device first.  Always 0 failures in a normal build (nothing is checked). */
+int ts_hydro_debug_check(ts_hydro_ctx* ctx, uint64_t out[5], int32_t reset);
+/* 1 when this library is a TS_CHECK build. */
+int ts_hydro_check_build(void);
 /* SimDevice::flush_activity: waits for in-flight work, returns completed
  * records not yet delivered (at most once).  out == NULL -> count only. */
 int ts_hydro_flush_activity(ts_hydro_ctx* ctx, ts_activity_record* out, uint64_t cap, uint64_t* n_out);

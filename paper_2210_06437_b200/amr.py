@@ -172,6 +172,30 @@ def amr_mesh(nx: int, ny: int, nz: int,
     return AmrMesh((nx, ny, nz), used, level, pos, nbr, level_first, prox, refl)
 
 
+def from_reference_mesh(level, pos) -> AmrMesh:
+    """The leaves of a reference octree (``build_mesh``, workload.cpp:264-327:
+    every existing node, refined parents included, with its level and position
+    at that level).  The root is one level-0 sub-grid; a node is refined iff
+    its children exist (TreeBuilder::refine creates all 8), and the builder's
+    force_exists pass makes every refined node's face neighbours exist
+    (workload.cpp:234-248), i.e. the leaves are 2:1 balanced across faces —
+    which ``amr_mesh`` checks again."""
+    level = np.asarray(level, np.int64)
+    pos = np.asarray(pos, np.int64).reshape(-1, 3)
+    nodes = {(int(L), tuple(int(v) for v in p)) for L, p in zip(level, pos)}
+    refined = set()
+    for L, p in nodes:
+        if L > 0:
+            refined.add((L - 1, p[0] >> 1, p[1] >> 1, p[2] >> 1))
+    for L, x, y, z in refined:
+        if (L, (x, y, z)) not in nodes:
+            raise ValueError(f"node ({L}, {x}, {y}, {z}) has children but does not exist")
+    max_level = int(level.max()) if len(level) else 0
+    if (0, (0, 0, 0)) not in nodes:
+        raise ValueError("the reference octree has one level-0 root at (0, 0, 0)")
+    return amr_mesh(1, 1, 1, refined, max_level=max_level)
+
+
 def ic_blast(mesh: AmrMesh, nf: int, dx: float, gamma: float = 1.4, centre=None, width: float = 0.1,
              amp: float = 4.0, drift=(0.0, 0.0, 0.0)) -> np.ndarray:
     """Smooth pressure / density bump (Gaussian) on a uniform background, with an

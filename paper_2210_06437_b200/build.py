@@ -56,7 +56,7 @@ def _compile(src: str, force: bool):
     if src.endswith(".cu"):
         cmd = [NVCC, *NVCC_FLAGS, *EXTRA, "-c", src, "-o", obj]
     else:
-        cmd = ["g++", *CXX_FLAGS, "-c", src, "-o", obj]
+        cmd = ["g++", *CXX_FLAGS, *EXTRA, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -19,6 +19,23 @@ struct StageArgs {
     const double* Un;           // U^n (stages 2, 3)
     double* Uout;               // U^{(k)}
     double* scratch;            // a state buffer free during this stage (species accumulators, nf > 6)
+    // nf > 6: species accumulators in a small ring of per-SM slots instead of
+    // the sub-grid's own slot of `scratch`: a CTA takes a free slot of its SM
+    // (scr_mask[smid] bit) and frees it at exit, so the same ~12 MB of lines
+    // are rewritten while still in L2 and never written back to HBM (the
+    // state-buffer scratch cost nf 11 ~20 % extra DRAM traffic).
+    // Self-check builds (TS_CHECK=1): every pencil load,
+    // U^n load and U^(k) store is bounds-checked against the buffers, and
+    // every acquired dataflow / halo flag is re-read at the CTA's end (a
+    // value past the awaited one means a producer overtook its consumer).
+    // Failures are counted in check[0], the first one in check[1..3],
+    // check[4] = OR of (1 << code) over all of them.
+    unsigned long long* check;
+    long long n_local;          // sub-grid slots in each state buffer
+    long long n_owned;          // sub-grids this rank updates
+    double* scr_ring;           // [n_sm * scr_k][nf - 6][512] (nullptr: use scratch)
+    unsigned int* scr_mask;     // [256] busy-slot bits per SM id
+    int scr_k;                  // slots per SM (<= 32)
     const int* nbr;             // [local][6] local neighbour index, -1 = outflow
     const int* list;            // CTA -> local sub-grid (nullable: first + blockIdx.x)
     int first;

@@ -160,11 +160,53 @@ __device__ __forceinline__ const double* paddr(const Pencil& p, int s) {
     if (SM) return p.sown + sm_slot(p.base + s * p.ss);
     return p.own + p.base + s * p.ss;
 }
+// Self-check build (TS_CHECK=1; StageArgs::check): bounds of the buffers a
+// CTA touches, in shared memory so the pencil helpers need no argument.
+#ifndef TS_CHECK
+#define TS_CHECK 0
+#endif
+struct CheckBounds {
+    const double* prev_lo;
+    const double* prev_hi;
+    const double* un_lo;
+    const double* un_hi;
+    unsigned long long* out;
+};
+#if TS_CHECK
+__shared__ CheckBounds s_chk;
+#endif
+__device__ __forceinline__ void chk_fail(unsigned long long* out, unsigned code, long long a, long long b) {
+    if (out == nullptr) return;
+    atomicOr(out + 4, 1ull << (code & 63u));  // every code seen
+    if (atomicAdd(out, 1ull) == 0ull) {
+        out[1] = code;
+        out[2] = (unsigned long long)a;
+        out[3] = (unsigned long long)b;
+    }
+}
+// code 1: U^(k-1) load outside the buffer, 2: U^n load outside the buffer
+__device__ __forceinline__ void chk_load(const double* a, int which) {
+#if TS_CHECK
+    if (__isShared(a)) return;
+    const double* lo = which == 1 ? s_chk.prev_lo : s_chk.un_lo;
+    const double* hi = which == 1 ? s_chk.prev_hi : s_chk.un_hi;
+    if (a < lo || a >= hi) chk_fail(s_chk.out, (unsigned)which, (long long)(a - lo), (long long)(hi - lo));
+#else
+    (void)a;
+    (void)which;
+#endif
+}
+
 // Pencil load: read-only global path, or a generic load when the address may
 // be the staged shared-memory copy.
 template <bool SM>
 __device__ __forceinline__ double ld_pen(const double* a) {
+    chk_load(a, 1);
     if (SM) return *a;
+    return __ldg(a);
+}
+__device__ __forceinline__ double ld_un(const double* a) {
+    chk_load(a, 2);
     return __ldg(a);
 }
 
@@ -340,6 +382,9 @@ __device__ __forceinline__ double retire_m(const StageCtx& c, int f, int o, doub
         } else {
             out = fma(1.0 / 3.0, un, (2.0 / 3.0) * ustar);
         }
+#if TS_CHECK
+        if (o < 0 || o >= NC || !isfinite(out)) chk_fail(s_chk.out, isfinite(out) ? 3u : 20u, o, f);
+#endif
         c.Uout[c.own + (size_t)f * NC + o] = out;
         return out;
     }
@@ -416,7 +461,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
     double un[kFA];
     if (kUn && !TS_UN_LATE) {
 #pragma unroll
-        for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + fo[k]);
+        for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + fo[k]);
     }
     double Fp[kFA];
     {  // face 0
@@ -450,7 +495,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
         for (int k = 0; k < kFA; ++k) {
             up[k] = retiring_up<RECON, SM, MODE>(r[k], p, j, fo[k]);  // U^(k-1) of cell j-1, retired here
-            if (kUn && TS_UN_LATE) un[k] = __ldg(un_row + (j - 1) * p.ss + fo[k]);
+            if (kUn && TS_UN_LATE) un[k] = ld_un(un_row + (j - 1) * p.ss + fo[k]);
             recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         }
         double F[kFA], vL, vR, a;
@@ -469,7 +514,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         if (kUn && !TS_UN_LATE) {
             const int jn = j < N ? j : N - 1;  // cell retired at the next face (a dummy reload after the last)
 #pragma unroll
-            for (int k = 0; k < kFA; ++k) un[k] = __ldg(un_row + jn * p.ss + fo[k]);
+            for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + jn * p.ss + fo[k]);
         }
 #pragma unroll
         for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
@@ -487,7 +532,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             }
             Recon q;
             recon_begin<RECON>(p, fof, q);
-            double unf = kUn ? __ldg(un_row + fof) : 0.0;
+            double unf = kUn ? ld_un(un_row + fof) : 0.0;
             double Fq;
             {
                 double uL, uR;
@@ -505,7 +550,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
-                if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
+                if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
         }
@@ -539,7 +584,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
     double un[3];
     if (kUn) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + fo[k]);
+        for (int k = 0; k < 3; ++k) un[k] = ld_un(un_row + fo[k]);
     }
     double Fp[3];
 #pragma unroll 1
@@ -597,7 +642,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
             if (kUn) {
                 const int jn = j < N ? j : N - 1;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) un[k] = __ldg(un_row + jn * p.ss + fo[k]);
+                for (int k = 0; k < 3; ++k) un[k] = ld_un(un_row + jn * p.ss + fo[k]);
             }
         }
 #pragma unroll
@@ -620,7 +665,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
             }
             Recon q;
             recon_begin<RECON>(p, fof, q);
-            double unf = kUn ? __ldg(un_row + fof) : 0.0;
+            double unf = kUn ? ld_un(un_row + fof) : 0.0;
             double Fq;
             {
                 double uL, uR;
@@ -638,7 +683,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
-                if (kUn) unf = __ldg(un_row + (j < N ? j : N - 1) * p.ss + fof);
+                if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
                 Fq = F;
             }
         }
@@ -758,7 +803,12 @@ __device__ __forceinline__ void halo_push(const StageArgs& A, size_t own, int b)
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        if (atomicAdd(A.halo_ctr, 1u) == A.halo_target - 1u) {
+        const unsigned prior = atomicAdd(A.halo_ctr, 1u);
+#if TS_CHECK
+        // a count past this stage's target: another stage counted into the same slot
+        if ((int)(prior - A.halo_target) >= 0) chk_fail(A.check, 12u, prior, A.halo_target);
+#endif
+        if (prior == A.halo_target - 1u) {
             __threadfence_system();
             for (int q = 0; q < A.halo_flag_n; ++q)
                 if (A.halo_flag[q] != nullptr) atomicExch_system(A.halo_flag[q], A.halo_seq);
@@ -852,6 +902,14 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     const int t = threadIdx.x;
     // stage 1's once-per-step duties (see StageArgs::lead_g1)
     const bool lead = A.lead_g1 == 0 ? blockIdx.x == 0 : g == A.lead_g1 - 1;
+#if TS_CHECK
+    if (t == 0) {
+        const size_t span = (size_t)A.n_local * NF * NC;
+        s_chk = CheckBounds{A.Uprev, A.Uprev + span, A.Un, A.Un + span, A.check};
+        if (g < 0 || g >= A.n_owned) chk_fail(A.check, 4u, g, A.n_owned);  // CTA -> sub-grid outside the owned range
+    }
+    __syncthreads();
+#endif
     if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0) {
         // proxies of U^(k-1): pushed by the peers' previous-stage boundary CTAs
         // (released in their first wave, so this rarely spins)
@@ -936,6 +994,25 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     c.cache = smem + StageSmem<NF>::dU;
     c.own = (size_t)g * NF * NC;
     c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
+    __shared__ int scr_slot;
+    if (NF > kFA && A.scr_ring != nullptr) {
+        if (t == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            unsigned* mask = A.scr_mask + (sm & 255u);
+            int slot = -1;
+            while (slot < 0) {  // a free bit exists: at most scr_k CTAs of stage kernels are resident per SM
+                const unsigned m = *reinterpret_cast<volatile unsigned*>(mask);
+                const unsigned free_bits = ~m & ((A.scr_k >= 32) ? 0xffffffffu : ((1u << A.scr_k) - 1u));
+                if (free_bits == 0u) continue;
+                const int b = __ffs(free_bits) - 1;
+                if ((atomicOr(mask, 1u << b) & (1u << b)) == 0u) slot = (int)(sm & 255u) * A.scr_k + b;
+            }
+            scr_slot = slot;
+        }
+        __syncthreads();
+        c.scr = A.scr_ring + (size_t)scr_slot * (NF - kFA) * NC - (size_t)kFA * NC;
+    }
     c.e = EosParams{A.gamma, A.gm1, A.p_floor};
     const double* own = A.Uprev + c.own;
     const int pen = Lanes<NF>::pair ? t >> 1 : t;
@@ -968,6 +1045,9 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                 if (t == 0) flow_wait_one(A, A.cnt_wait, A.cnt_expect);
                 __syncthreads();
                 amax_in = *reinterpret_cast<const volatile double*>(A.amax_in);
+#if TS_CHECK
+                if (t == 0 && !(amax_in > 0.0 && isfinite(amax_in))) chk_fail(A.check, 13u, g, 0);
+#endif
             }
             const double dt = (A.cfl * A.dx) / amax_in;
             c.dtdx = 0.5 * (dt / level_dx(A, g));  // the sweeps carry twice the KT flux (kt2)
@@ -994,6 +1074,26 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             sweep<NF, RECON, STAGE, 2>(c, p, fm, amax);
         if (axis < 2) __syncthreads();
     }
+#if TS_CHECK
+    // every flag this CTA acquired still holds exactly the awaited value: a
+    // later one would mean a producer already ran its NEXT use of the data
+    // this CTA read (flow: the next step's same stage of a neighbour; halo:
+    // a peer's next stage), i.e. the ordering protocol let it overtake
+    if (A.flow_wait != nullptr && t < 7) {
+        const int h = t == 0 ? g : __ldg(A.nbr + 6 * g + (t - 1));
+        if (h >= 0 && h < A.flow_n) {
+            const unsigned v = ld_acquire_gpu(A.flow_wait + h);
+            if (v != A.flow_wait_seq) chk_fail(A.check, 10u, h, (long long)(int)(v - A.flow_wait_seq));
+        }
+    }
+    if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0 && t < 64 &&
+        ((A.halo_wait_mask >> t) & 1ull)) {
+        // a peer may already have pushed its NEXT stage (into the other buffer
+        // of the rotation: +1), never the one after (it needs this CTA's push)
+        const int d = (int)(ld_acquire_sys(A.halo_wait + t) - A.halo_wait_seq);
+        if (d < 0 || d > 1) chk_fail(A.check, 11u, t, d);
+    }
+#endif
     if (A.push_tbl != nullptr) {
         const int b = __ldg(A.cta_bnd + blockIdx.x);
         if (b >= 0) halo_push<NF>(A, c.own, b);
@@ -1047,6 +1147,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
                     *A.amax_global = g;
                 }
             }
+        }
+    }
+    if (NF > kFA && A.scr_ring != nullptr) {
+        __syncthreads();  // every species accumulator read / write of this CTA is done
+        if (t == 0) {
+            const int b = scr_slot % A.scr_k;
+            atomicAnd(A.scr_mask + scr_slot / A.scr_k, ~(1u << b));
         }
     }
     if (A.stamp != nullptr) {

@@ -239,6 +239,11 @@ struct ts_hydro_ctx {
 
     // device memory
     double* U[3] = {nullptr, nullptr, nullptr};
+    unsigned long long* d_check = nullptr;  // [5] self-check failures (TS_CHECK builds write it)
+    double* d_scr_ring = nullptr;   // nf > 6: species accumulators, kScrK slots per SM id (StageArgs::scr_ring)
+    unsigned int* d_scr_mask = nullptr;
+    static constexpr int kScrK = 8;
+    bool scr_ring = true;           // TS_HYDRO_SCR_RING=0: accumulate in the free state buffer
     CUtensorMap tmap[3];           // TMA view of each state buffer: rows of 16 doubles, {16, 32} boxes
     bool tmap_ok = false;
     int32_t* d_nbr = nullptr;
@@ -489,6 +494,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_cta_log);
     dfree(c, &c->d_chunk_ctr);
     dfree(c, &c->d_h2d_flag);
+    dfree(c, &c->d_scr_ring);
+    dfree(c, &c->d_scr_mask);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
     dfree(c, &c->d_gid);
@@ -774,6 +781,14 @@ tsh::StageArgs stage_args(ts_hydro_ctx* c, int stage) {
     if (c->tmap_ok) {
         a.tmap_prev = c->tmap[stage - 1];  // U[0], U[1], U[2] = A, B, C
         a.tma = 1;
+    }
+    a.check = c->d_check;
+    a.n_local = c->n_owned + c->n_proxy;
+    a.n_owned = c->n_owned;
+    if (c->d_scr_ring != nullptr) {
+        a.scr_ring = c->d_scr_ring;
+        a.scr_mask = c->d_scr_mask;
+        a.scr_k = ts_hydro_ctx::kScrK;
     }
     a.Un = A;
     a.Uout = stage == 1 ? B : (stage == 2 ? C : A);
@@ -1070,6 +1085,11 @@ int do_step(ts_hydro_ctx* c) {
             const bool steps = !multi && c->flow_steps;  // stage 3 feeds the next stage 1 too
             a.flow_seq = c->flow_seq;
             a.flow_wait_seq = c->flow_seq;
+#if defined(TS_CHECK) && TS_CHECK
+            // detector self-test (check builds only): wait for the PREVIOUS
+            // step's flags, i.e. a broken ordering the exit re-check must catch
+            if (stage > 1 && std::getenv("TS_HYDRO_DEBUG_BREAK_FLOW") != nullptr) a.flow_wait_seq = c->flow_seq - 1;
+#endif
             a.flow_n = (int)c->n_owned;
             a.pdl_trigger = stage < 3 || steps;
             a.flow_wait = stage > 1 ? c->d_flow + (size_t)(stage - 2) * n : nullptr;
@@ -1418,6 +1438,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_SCR_RING")) c->scr_ring = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_FULLFILL")) c->amr_slab_fill = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
@@ -1506,6 +1527,7 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         ctx->comm = nullptr;
         free_mesh(ctx);
         dfree(ctx, &ctx->d_scal);
+        dfree(ctx, &ctx->d_check);
         dfree(ctx, &ctx->d_dt_hist);
         dfree(ctx, &ctx->d_stamps);
         for (auto& kv : ctx->host_allocs) cudaFreeHost(kv.first);
@@ -1701,6 +1723,15 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         TS_CUDA(c, cudaMemset(b, 0, elems * sizeof(double)));
     }
     rc = encode_tmaps(c);
+    if (!rc && c->d_check == nullptr) {
+        rc = dalloc(c, &c->d_check, 5);
+        if (!rc) TS_CUDA(c, cudaMemset(c->d_check, 0, 5 * sizeof(unsigned long long)));
+    }
+    if (!rc && c->nf > 6 && c->scr_ring) {
+        rc = dalloc(c, &c->d_scr_ring, (size_t)256 * ts_hydro_ctx::kScrK * (c->nf - 6) * kNC);
+        if (!rc) rc = dalloc(c, &c->d_scr_mask, 256);
+        if (!rc) TS_CUDA(c, cudaMemset(c->d_scr_mask, 0, 256 * sizeof(unsigned int)));
+    }
     if (!rc) rc = dalloc(c, &c->d_nbr, (size_t)nl * 6);
     if (!rc) rc = dalloc(c, &c->d_interior, c->interior.size());
     if (!rc) rc = dalloc(c, &c->d_boundary, c->boundary.size());
@@ -2628,6 +2659,29 @@ int ts_hydro_set_activity_sink(ts_hydro_ctx* c, ts_activity_sink_fn sink, void* 
     c->sink = sink;
     c->sink_user = user;
     return TS_OK;
+}
+
+int ts_hydro_debug_check(ts_hydro_ctx* c, uint64_t out[5], int32_t reset) {
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (out == nullptr) return fail(c, TS_EINVAL, "null output");
+    for (int k = 0; k < 5; ++k) out[k] = 0;
+    if (c->host_only || c->d_check == nullptr) return TS_OK;
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpy(out, c->d_check, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (reset) TS_CUDA(c, cudaMemset(c->d_check, 0, 5 * sizeof(unsigned long long)));
+    return TS_OK;
+}
+
+int ts_hydro_check_build(void) {
+#if defined(TS_CHECK) && TS_CHECK
+    return 1;
+#else
+    return 0;
+#endif
 }
 
 int ts_hydro_set_profiling(ts_hydro_ctx* c, int32_t enabled) {

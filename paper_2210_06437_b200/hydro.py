@@ -48,6 +48,11 @@ kKernelReconstruct = "reconstruct_kernel"
 kKernelFlux = "flux_kernel"
 
 
+# TS_HYDRO_CHECK_STRICT with a TS_CHECK library: failures recorded by devices
+# at close (tests/conftest.py asserts it stays empty after every test)
+CHECK_FAILURES: list = []
+
+
 class TsError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
@@ -153,6 +158,8 @@ _SIGNATURES = {
     "ts_hydro_p2p_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32]),
     "ts_hydro_set_activity_sink": (ctypes.c_int, [_vp, SINK_FN, _vp]),
     "ts_hydro_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "ts_hydro_debug_check": (ctypes.c_int, [_vp, _u64p, ctypes.c_int32]),
+    "ts_hydro_check_build": (ctypes.c_int, []),
     "ts_hydro_flush_activity": (ctypes.c_int, [_vp, ctypes.POINTER(_Record), ctypes.c_uint64, _u64p]),
     "ts_hydro_memory_state": (ctypes.c_int, [_vp, ctypes.POINTER(_MemState)]),
     "ts_hydro_clock_ns": (ctypes.c_uint64, []),
@@ -451,8 +458,18 @@ class CudaDevice:
 
     def close(self) -> None:
         if self._h:
+            bad = None
+            if os.environ.get("TS_HYDRO_CHECK_STRICT") and lib().ts_hydro_check_build():
+                try:
+                    bad = self.debug_check()
+                except Exception:  # e.g. a shut-down device
+                    bad = None
             lib().ts_hydro_destroy(self._h)
             self._h = None
+            if bad is not None and bad[0] != 0:
+                CHECK_FAILURES.append(bad)
+                raise AssertionError(f"self-check build recorded {bad[0]} protocol / bounds failures "
+                                     f"(first: code {bad[1]}, operands {bad[2]}, {bad[3]}; DESIGN.md section 13)")
 
     def __del__(self):
         try:
@@ -659,6 +676,12 @@ class CudaDevice:
         return [ActivityRecord(ACTIVITY_KINDS[r.kind], r.name.decode(), r.device_id, r.stream_id, r.start_ns,
                                r.end_ns, r.bytes if r.has_bytes else None, r.correlation_guid)
                 for r in buf[:n.value]]
+
+    def debug_check(self, reset: bool = False):
+        """Self-check build counters: (failures, first code, a, b, code bitmask) — DESIGN.md §13."""
+        out = np.zeros(5, np.uint64)
+        self._check(lib().ts_hydro_debug_check(self._h, _p(out, _u64p), 1 if reset else 0), "debug_check")
+        return tuple(int(x) for x in out)
 
     def set_profiling(self, enabled: bool) -> None:
         """ProfilingArm full (True) / disabled (False): activity stamps and records on or off."""

@@ -52,3 +52,19 @@ def golden():
         vec = json.load(f)
     ghosts = dict(np.load(os.path.join(d, "reference_ghosts.npz")))
     return vec, ghosts
+
+
+@pytest.fixture(autouse=True)
+def _self_check_build_clean():
+    """With TS_HYDRO_CHECK_STRICT=1 and a TS_CHECK library (TS_HYDRO_LIB), every
+    device a test closed or dropped must have recorded no protocol / bounds
+    failure (the stand-in for compute-sanitizer)."""
+    yield
+    if not os.environ.get("TS_HYDRO_CHECK_STRICT"):
+        return
+    import gc
+    from paper_2210_06437_b200 import hydro as H
+    gc.collect()
+    bad = list(H.CHECK_FAILURES)
+    H.CHECK_FAILURES.clear()
+    assert not bad, f"self-check failures recorded: {bad}"

@@ -215,3 +215,48 @@ def test_set_amr_mesh_validates(hydro):
     rf[0, 1 + 4 * f] = rf[0, 0]
     with pytest.raises(ValueError, match="one level finer"):
         d.set_amr_mesh(bad(reflux=rf))
+
+
+def test_reference_build_mesh_octrees_become_amr_leaf_meshes(golden):
+    """The reference's own octrees (build_mesh output, golden vectors drawn
+    from the compiled reference): the leaves are the nodes without children,
+    every same-level link between two leaves is the reference's link
+    (workload.cpp:306-314), and the 2:1 balance the TreeBuilder enforces
+    (workload.cpp:234-248) is accepted."""
+    vec, _ = golden
+    for m in vec["build_mesh"]:
+        lvl = np.asarray(m["level"])
+        pos = np.asarray(m["pos"]).reshape(-1, 3)
+        nbr = np.asarray(m["nbr"]).reshape(-1, 6)
+        a = amr.from_reference_mesh(lvl, pos)
+        parents = {(int(L) - 1, *(int(v) >> 1 for v in p)) for L, p in zip(lvl, pos) if L > 0}
+        ref_leaf = {(int(L), *map(int, p)): i for i, (L, p) in enumerate(zip(lvl, pos))
+                    if (int(L), *map(int, p)) not in parents}
+        ours = {(int(L), *map(int, p)): i for i, (L, p) in enumerate(zip(a.level, a.pos))}
+        assert set(ours) == set(ref_leaf)
+        for key, i in ours.items():
+            r = ref_leaf[key]
+            for f in range(6):
+                rn = int(nbr[r, f])
+                rkey = (int(lvl[rn]), *map(int, pos[rn])) if rn >= 0 else None
+                if rkey is not None and rkey in ref_leaf:
+                    # a same-level leaf neighbour in the reference: the same leaf here
+                    assert a.nbr[i, f] >= 0 and a.nbr[i, f] < a.n_leaves
+                    assert (int(a.level[a.nbr[i, f]]), *map(int, a.pos[a.nbr[i, f]])) == rkey
+                elif a.nbr[i, f] >= 0 and a.nbr[i, f] < a.n_leaves:
+                    raise AssertionError(f"leaf {key} face {f}: a same-level leaf link the reference lacks")
+
+
+def test_reference_octree_amr_oracle_conserves_and_keeps_free_stream(oracle_lib, golden):
+    """The AMR oracle on the reference's levels-4 octree: a uniform drifting
+    state stays uniform bit for bit across the coarse-fine faces."""
+    vec, _ = golden
+    m = max(vec["build_mesh"], key=lambda e: len(e["level"]))
+    a = amr.from_reference_mesh(m["level"], m["pos"])
+    dx = 1.0 / (8 << a.max_level)
+    U = np.zeros((a.n_total, 6, 512))
+    U[:, 0] = 1.0
+    U[:, 1] = 0.3
+    U[:, 4] = 2.0
+    out, _ = oracle_lib.run_amr(oracle_lib.params(nf=6, dx=dx), a, U, 2)
+    assert np.array_equal(out[:a.n_leaves], U[:a.n_leaves])
