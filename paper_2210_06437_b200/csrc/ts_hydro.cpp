@@ -1012,6 +1012,20 @@ int do_step_amr(ts_hydro_ctx* c) {
                                               c->amr_n_rec, stage, dt_ptr, stamp, s));
         }
     }
+    if (c->amr_n_rec > 0) {
+        // The stage-3 kernel reduced the signal speed of U^{n+1} as it wrote
+        // it, but the reflux after it corrects coarse cells: the next dt must
+        // come from the corrected state (the oracle's max_signal_speed of the
+        // final U^{n+1}).  Found by the reference-octree AMR parity test
+        // (minmod: the maximum sat on a refluxed cell).
+        double* slot = amax_slot(c, c->steps_done + 1);
+        TS_CUDA(c, cudaMemsetAsync(slot, 0, sizeof(double), s));
+        unsigned long long* stamp = nullptr;
+        rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameSignal, 0, 0, &stamp);
+        if (rc) return rc;
+        TS_CUDA(c, tsh::launch_signal(c->U[0], c->nf, c->n_owned, c->cfg.gamma, c->cfg.p_floor, slot, stamp,
+                                      c->sms, s));
+    }
     c->amax_src = nullptr;
     c->flow_chain = false;
     c->steps_done++;
