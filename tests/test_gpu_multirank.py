@@ -32,6 +32,19 @@ def _port():
     return p
 
 
+def _torchrun(script_args, timeout):
+    """torchrun world 2 on 127.0.0.1; a rendezvous port taken between picking
+    and binding it (EADDRINUSE) is retried with a fresh one."""
+    for _ in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+               os.path.join(ROOT, "tools", "multigpu_check.py"), *script_args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            return r
+    return r
+
+
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce", "nccl"])
 @pytest.mark.parametrize("args", [["--dims", "4", "4", "8"], ["--dims", "2", "4", "4", "--periodic", "xyz", "--species", "5"],
                                   ["--dims", "4", "2", "6", "--recon", "minmod", "--steps", "2"],
@@ -42,10 +55,7 @@ def test_two_gpu_step_is_bitwise_equal_to_single_gpu(args, transport):
     n = _gpus()
     if n < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multigpu_check.py"), *args, "--transport", transport]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = _torchrun([*args, "--transport", transport], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
 
@@ -64,10 +74,7 @@ def test_two_ranks_on_one_gpu_bitwise_equal_to_single_rank(args, transport):
     test_workload.cpp:317-331 / 448-464 on the cross-rank code path."""
     if _gpus() < 1:
         pytest.skip("needs a GPU")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multigpu_check.py"), *args, "--transport", transport, "--same-device"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = _torchrun([*args, "--transport", transport, "--same-device"], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
 
@@ -76,10 +83,7 @@ def test_two_ranks_on_one_gpu_bitwise_equal_to_single_rank(args, transport):
 def test_mismatch_on_one_gpu_fails_instead_of_hanging(transport):
     if _gpus() < 1:
         pytest.skip("needs a GPU")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multigpu_check.py"), "--mismatch", "--transport", transport, "--same-device"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    r = _torchrun(["--mismatch", "--transport", transport, "--same-device"], 300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MISMATCH DETECTED" in r.stdout
 
@@ -91,9 +95,6 @@ def test_mismatched_collective_call_fails_instead_of_hanging(transport):
     n = _gpus()
     if n < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multigpu_check.py"), "--mismatch", "--transport", transport]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    r = _torchrun(["--mismatch", "--transport", transport], 300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MISMATCH DETECTED" in r.stdout
