@@ -59,6 +59,15 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 // U^n of the retiring cell (stages 2, 3, z sweep): loaded at the top of the
 // face that retires it (not carried across faces: 12 fewer loop-carried
 // registers) instead of prefetched one face ahead.
+// Measured same-box A/B (round 2), both neutral or slower, kept off: release
+// store / red for the dataflow flags instead of fence + atomic (±0 %), the six
+// neighbour ids loaded before the waits (−0.5 %).
+#ifndef TS_REL_FLAGS
+#define TS_REL_FLAGS 0
+#endif
+#ifndef TS_NBR_EARLY
+#define TS_NBR_EARLY 0
+#endif
 #ifndef TS_UN_LATE
 #define TS_UN_LATE 0
 #endif
@@ -902,6 +911,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     const int t = threadIdx.x;
     // stage 1's once-per-step duties (see StageArgs::lead_g1)
     const bool lead = A.lead_g1 == 0 ? blockIdx.x == 0 : g == A.lead_g1 - 1;
+#if TS_NBR_EARLY
+    // the six face neighbours, loaded before the waits (ncu: the per-sweep
+    // table load was a long-scoreboard stall at the start of every sweep)
+    int nb6[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) nb6[f] = __ldg(A.nbr + 6 * g + f);
+#endif
 #if TS_CHECK
     if (t == 0) {
         const size_t span = (size_t)A.n_local * NF * NC;
@@ -1021,8 +1037,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 
 #pragma unroll 1
     for (int axis = 0; axis < 3; ++axis) {
+#if TS_NBR_EARLY
+        const int nlo = axis == 0 ? nb6[0] : (axis == 1 ? nb6[2] : nb6[4]);
+        const int nhi = axis == 0 ? nb6[1] : (axis == 1 ? nb6[3] : nb6[5]);
+#else
         const int nlo = __ldg(A.nbr + 6 * g + 2 * axis);
         const int nhi = __ldg(A.nbr + 6 * g + 2 * axis + 1);
+#endif
         Pencil p;
         p.own = own;
         p.sown = nullptr;
@@ -1117,9 +1138,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         // one gpu-scope fence, flag / count
         __syncthreads();
         if (t == 0) {
+#if TS_REL_FLAGS
+            // release operations (cumulative over the CTA's writes that the
+            // barrier ordered before them) instead of a full fence + atomic
+            if (A.flow_done != nullptr)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.flow_done + g), "r"(A.flow_seq) : "memory");
+            if (STAGE == 3 && A.cnt_done != nullptr)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.cnt_done) : "memory");
+#else
             __threadfence();
             if (A.flow_done != nullptr) atomicExch(A.flow_done + g, A.flow_seq);
             if (STAGE == 3 && A.cnt_done != nullptr) atomicAdd(A.cnt_done, 1u);
+#endif
         }
     }
     if (A.done_ctr != nullptr) {
