@@ -229,6 +229,22 @@ int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned
  * joins the step's streams into the compute stream, no host wait. */
 int ts_hydro_finish_step(ts_hydro_ctx* ctx);
 
+/* ---- gravity (first slice) -------------------------- */
+/* The near-field monopole P2P behind the reference's `p2p_kernel` launches
+ * (gravity_kernel_name workload.cpp:365-372; 6 per sub-grid and step,
+ * 565-569): for every cell, phi = -G h^2 sum rho_j / |d| and g = G h sum
+ * rho_j d / |d|^3 over the same-level cells at offsets 0 < |d|^2 <= radius^2
+ * (radius 1..6 cells, across faces, edges and corners; vacuum outside the
+ * mesh) — oracle/hydro_oracle.h orc_gravity_p2p, bitwise.  The multipole,
+ * p2m and root parts of the FMM are not built.  owned_index == NULL or
+ * count <= 0: every owned sub-grid.  Runs after everything on the compute
+ * stream; single rank, uniform mesh, not while a per-sub-grid step is open.
+ * Activity record name "p2p_kernel". */
+int ts_hydro_gravity_p2p(ts_hydro_ctx* ctx, double G, int32_t radius, const int64_t* owned_index, int64_t count,
+                         uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
+/* [count][4][512] = (phi, gx, gy, gz) of owned sub-grids first..first+count-1 (waits). */
+int ts_hydro_download_gravity(ts_hydro_ctx* ctx, int64_t first, int64_t count, double* host);
+
 /* ---- ghost exchange --------------------------------------------------------- */
 /* The reference's 1-deep face exchange of field 0 (workload.cpp:487-542):
  * ghost[g][face][j] = neighbour cell face_cell_index(8, face^1, j), 0 where no

@@ -94,6 +94,10 @@ def lib():
         L.orc_ic_binary.restype = ctypes.c_int
         L.orc_ic_binary.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i32p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_int, _f64p]
+        L.orc_p2p_stencil.restype = ctypes.c_int
+        L.orc_p2p_stencil.argtypes = [ctypes.c_int, _i32p, _f64p, ctypes.c_int]
+        L.orc_gravity_p2p.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i64p, _f64p, ctypes.c_int,
+                                      ctypes.c_double, _f64p]
         L.orc_amr_fill.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _f64p]
         L.orc_amr_reflux.argtypes = [ctypes.POINTER(Params), _i64p, _i32p, ctypes.c_int, ctypes.c_int64, _i32p,
                                      _f64p, _f64p, ctypes.c_int, ctypes.c_double]
@@ -182,6 +186,26 @@ def ic_binary(p: Params, pos, dims):
                            dims[2], _p(U, _f64p)) != 0:
         raise MemoryError("oracle binary initial model")
     return U
+
+
+def p2p_stencil(radius):
+    """The gravity P2P stencil of radius R: offsets [n][3] and coefficients
+    [n][4] = (1/|d|, d/|d|^3) in the summation order (hydro_oracle.h)."""
+    off = np.zeros((1024, 3), np.int32)
+    coef = np.zeros((1024, 4), np.float64)
+    n = lib().orc_p2p_stencil(radius, _p(off, _i32p), _p(coef, _f64p), 1024)
+    if n < 0:
+        raise ValueError("radius outside 1..6")
+    return off[:n], coef[:n]
+
+
+def gravity_p2p(p: Params, nbr, U, radius=4, G=1.0):
+    """Near-field monopole potential and acceleration: [n][4][512] = (phi, gx, gy, gz)."""
+    nbr = np.ascontiguousarray(nbr, np.int64)
+    U = np.ascontiguousarray(U, np.float64)
+    out = np.zeros((U.shape[0], 4, NC), np.float64)
+    lib().orc_gravity_p2p(ctypes.byref(p), U.shape[0], _p(nbr, _i64p), _p(U, _f64p), radius, G, _p(out, _f64p))
+    return out
 
 
 def max_signal_speed(p: Params, U):

@@ -825,3 +825,83 @@ void orc_debug_face_fluxes(const orc_params* p, const int64_t* nbr, const double
                            int b, double* F) {
     for (int j = 0; j <= N; ++j) face_flux(p, nbr, U, g, axis, a, b, j, F + (size_t)j * p->nf);
 }
+
+/* ---------------------------------------------------------------------------
+ * Gravity, near-field monopole P2P (hydro_oracle.h).  The reference launches
+ * p2p_kernel for leaves without refined neighbours (gravity_kernel_name,
+ * workload.cpp:365-372) and only sleeps; Octo-Tiger computes the cell-to-cell
+ * interactions of non-refined sub-grids there.  This slice is
+ * the monopole near field of an FMM: the stencil of same-level cells within a
+ * sphere of radius R cells; the far field (multipoles, p2m, root) is not
+ * restated.
+ * ------------------------------------------------------------------------- */
+int orc_p2p_stencil(int radius, int32_t* off, double* coef, int cap) {
+    if (radius < 1 || radius > ORC_P2P_RMAX) return -1;
+    int n = 0;
+    for (int r2 = 1; r2 <= radius * radius; ++r2)
+        for (int dz = -radius; dz <= radius; ++dz)
+            for (int dy = -radius; dy <= radius; ++dy)
+                for (int dx = -radius; dx <= radius; ++dx) {
+                    if (dx * dx + dy * dy + dz * dz != r2) continue;
+                    if (n < cap) {
+                        const double c0 = 1.0 / sqrt((double)r2);
+                        const double c3 = c0 / (double)r2;
+                        off[3 * n] = dx;
+                        off[3 * n + 1] = dy;
+                        off[3 * n + 2] = dz;
+                        coef[4 * n] = c0;
+                        coef[4 * n + 1] = (double)dx * c3;
+                        coef[4 * n + 2] = (double)dy * c3;
+                        coef[4 * n + 3] = (double)dz * c3;
+                    }
+                    ++n;
+                }
+    return n;
+}
+
+/* density of the cell at in-sub-grid coordinates (x, y, z) in [-8, 15],
+ * walking the face links x, then y, then z; vacuum outside the mesh */
+static double p2p_rho(int nf, const int64_t* nbr, const double* U, int64_t g, int x, int y, int z) {
+    int c[3] = {x, y, z};
+    int64_t h = g;
+    for (int axis = 0; axis < 3; ++axis) {
+        if (c[axis] < 0) {
+            h = nbr[6 * h + 2 * axis];
+            c[axis] += N;
+        } else if (c[axis] >= N) {
+            h = nbr[6 * h + 2 * axis + 1];
+            c[axis] -= N;
+        }
+        if (h < 0) return 0.0;
+    }
+    return U[(h * nf) * NC + cidx(c[0], c[1], c[2])];
+}
+
+void orc_gravity_p2p(const orc_params* p, int64_t ngrids, const int64_t* nbr, const double* U, int radius, double G,
+                     double* out) {
+    int32_t off[3 * 1024];
+    double coef[4 * 1024];
+    const int ns = orc_p2p_stencil(radius, off, coef, 1024);
+    if (ns < 0 || ns > 1024) return;
+    const double h = p->dx;
+    const double kphi = -G * (h * h), kg = G * h;
+    for (int64_t g = 0; g < ngrids; ++g)
+        for (int z = 0; z < N; ++z)
+            for (int y = 0; y < N; ++y)
+                for (int x = 0; x < N; ++x) {
+                    double s0 = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+                    for (int k = 0; k < ns; ++k) {
+                        const double rho = p2p_rho(p->nf, nbr, U, g, x + off[3 * k], y + off[3 * k + 1],
+                                                   z + off[3 * k + 2]);
+                        s0 = fma(rho, coef[4 * k], s0);
+                        sx = fma(rho, coef[4 * k + 1], sx);
+                        sy = fma(rho, coef[4 * k + 2], sy);
+                        sz = fma(rho, coef[4 * k + 3], sz);
+                    }
+                    double* o = out + g * 4 * NC + cidx(x, y, z);
+                    o[0] = kphi * s0;
+                    o[NC] = kg * sx;
+                    o[2 * NC] = kg * sy;
+                    o[3 * NC] = kg * sz;
+                }
+}

@@ -124,6 +124,24 @@ int orc_run_amr(const orc_params* p, int64_t n_total, const int64_t* nbr, const 
                 const int64_t* level_first, int max_level, int64_t n_proxy, const orc_amr_proxy* px,
                 int64_t n_rec, const orc_amr_reflux_rec* rf, double* U, int nsteps, double* dt_hist);
 
+/* --- gravity, near-field slice (the reference's
+ * p2p_kernel launches, workload.cpp:365-372, 565-569; Octo-Tiger's "p2p
+ * interactions kernel: cell to cell interactions in non-refined sub-grids",
+ * PAPER.md:355) ---
+ * Monopole cell-to-cell interactions of every cell with the same-level cells
+ * at offsets 0 < |d|^2 <= R^2 (R <= ORC_P2P_RMAX), across sub-grid faces,
+ * edges and corners (walking the face links axis by axis; a missing
+ * neighbour is vacuum).  Stencil order: |d|^2 ascending, then (dz, dy, dx)
+ * lexicographic, so the stencil of R is a prefix of the stencil of RMAX.
+ * Per entry: c0 = 1/sqrt(|d|^2), c3 = c0/|d|^2, c = d c3.  Per cell, in
+ * stencil order: S0 = fma(rho_j, c0, S0), S = fma(rho_j, c, S); then
+ * phi = (-G h^2) S0, g = (G h) S  (m_j = rho_j h^3; g = -grad phi).
+ * out[g][4][512] = (phi, gx, gy, gz). */
+#define ORC_P2P_RMAX 6
+int orc_p2p_stencil(int radius, int32_t* off, double* coef, int cap);
+void orc_gravity_p2p(const orc_params* p, int64_t ngrids, const int64_t* nbr, const double* U, int radius, double G,
+                     double* out);
+
 #ifdef __cplusplus
 }
 #endif

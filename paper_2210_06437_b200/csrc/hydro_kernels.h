@@ -205,6 +205,24 @@ cudaError_t launch_amr_reflux(const double* Uprev, double* Uout, int nf, int rec
                               const int* nbr, const int* level, int max_level, double dx, const AmrReflux* rf,
                               long long n, int stage, const double* dt, unsigned long long* stamp,
                               cudaStream_t s);
+// Gravity slice (gravity_kernels.cu): near-field monopole P2P, one CTA per
+// sub-grid (list_inline or first + blockIdx.x); out [n][4][512] = (phi, g).
+constexpr int kP2PRMax = 6;
+struct P2PArgs {
+    const double* U;   // state (field 0 = density)
+    int nf;
+    const int* nbr;    // [local][6]
+    double* out;
+    int list_inline_n;
+    int list_inline[StageArgs::kInlineList];
+    int first;
+    int radius;        // 1..kP2PRMax
+    int n_stencil;     // entries of the radius' stencil (a prefix of the R = 6 table)
+    double kphi, kg;   // -G h^2, G h
+    unsigned long long* stamp;
+};
+int p2p_stencil_host(int radius, int* off3, double* coef4, int cap);
+cudaError_t launch_p2p(const P2PArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
                                  int sms, cudaStream_t s);
 

@@ -46,6 +46,7 @@ constexpr int kSlab = 3 * kN * kN;
 constexpr const char* kNameStage[4] = {"", "hydro_stage1_kernel", "hydro_stage2_kernel",
                                        "hydro_stage3_kernel"};
 constexpr const char* kNameSignal = "signal_speed_kernel";
+constexpr const char* kNameP2P = "p2p_kernel";  // the reference's kKernelP2P (workload.hpp:46)
 constexpr const char* kNamePack = "halo_pack_kernel";
 constexpr const char* kNameUnpack = "halo_unpack_kernel";
 constexpr const char* kNameAmrFill = "amr_ghost_fill_kernel";
@@ -240,6 +241,7 @@ struct ts_hydro_ctx {
     // device memory
     double* U[3] = {nullptr, nullptr, nullptr};
     unsigned long long* d_check = nullptr;  // [5] self-check failures (TS_CHECK builds write it)
+    double* d_grav = nullptr;               // [n_owned][4][512] gravity P2P output (phi, gx, gy, gz)
     double* d_scr_ring = nullptr;   // nf > 6: species accumulators, kScrK slots per SM id (StageArgs::scr_ring)
     unsigned int* d_scr_mask = nullptr;
     static constexpr int kScrK = 8;
@@ -495,6 +497,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_chunk_ctr);
     dfree(c, &c->d_h2d_flag);
     dfree(c, &c->d_scr_ring);
+    dfree(c, &c->d_grav);
     dfree(c, &c->d_scr_mask);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
@@ -2410,6 +2413,91 @@ int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_i
     for (int32_t g : L.list) c->din_req[(size_t)g] = (uint8_t)stage;
     c->din_parked.push_back(std::move(L));
     return dropin_pump(c);
+}
+
+// Gravity slice: near-field monopole P2P of the listed owned sub-grids
+// (nullptr / count <= 0: all) on stream `stream_id`, after everything on the
+// compute stream (a closed per-sub-grid step is joined into it).
+int ts_hydro_gravity_p2p(ts_hydro_ctx* c, double G, int32_t radius, const int64_t* owned_index, int64_t count,
+                         uint32_t stream_id, uint64_t guid, ts_done_fn done, void* user) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (radius < 1 || radius > tsh::kP2PRMax) return fail(c, TS_EINVAL, "P2P radius must be 1..6 cells");
+    if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
+    if (c->world > 1) return fail(c, TS_ESTATE, "the gravity slice is single-rank (halos deeper than 3 cells)");
+    if (c->amr) return fail(c, TS_ESTATE, "the gravity slice needs a uniform mesh (same-level neighbours)");
+    if (c->din_open) return fail(c, TS_ESTATE, "gravity reads the state: close the per-sub-grid step first");
+    std::vector<int32_t> list;
+    if (owned_index != nullptr && count > 0) {
+        list.resize((size_t)count);
+        for (int64_t k = 0; k < count; ++k) {
+            if (owned_index[k] < 0 || owned_index[k] >= c->n_owned)
+                return fail(c, TS_EINVAL, "sub-grid index outside the owned range");
+            list[(size_t)k] = (int32_t)owned_index[k];
+        }
+    }
+    cudaSetDevice(c->dev);
+    if (c->d_grav == nullptr) {
+        rc = dalloc(c, &c->d_grav, (size_t)c->n_owned * 4 * kNC);
+        if (rc) return rc;
+    }
+    cudaStream_t s, s0;
+    rc = ensure_stream(c, stream_id, &s);
+    if (!rc) rc = ensure_stream(c, 0, &s0);
+    if (rc) return rc;
+    if (s != s0) {
+        TS_CUDA(c, cudaEventRecord(c->ev_in, s0));
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_in, 0));
+    }
+    int off3[3 * 1024];
+    double coef[4 * 1024];
+    tsh::P2PArgs a{};
+    a.U = c->U[0];
+    a.nf = c->nf;
+    a.nbr = c->d_nbr;
+    a.out = c->d_grav;
+    a.radius = radius;
+    a.n_stencil = tsh::p2p_stencil_host(radius, off3, coef, 1024);
+    a.kphi = -G * (c->cfg.dx * c->cfg.dx);
+    a.kg = G * c->cfg.dx;
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameP2P, (int32_t)stream_id, guid, &stamp);
+    if (rc) return rc;
+    a.stamp = stamp;
+    if (list.empty()) {
+        a.first = 0;
+        TS_CUDA(c, tsh::launch_p2p(a, (int)c->n_owned, s));
+    } else if (list.size() <= (size_t)tsh::StageArgs::kInlineList) {
+        a.list_inline_n = (int)list.size();
+        for (size_t k = 0; k < list.size(); ++k) a.list_inline[k] = list[k];
+        TS_CUDA(c, tsh::launch_p2p(a, (int)list.size(), s));
+    } else {
+        for (size_t k = 0; k < list.size();) {
+            size_t e = k + 1;
+            while (e < list.size() && list[e] == list[e - 1] + 1) ++e;
+            a.first = list[k];
+            TS_CUDA(c, tsh::launch_p2p(a, (int)(e - k), s));
+            k = e;
+        }
+    }
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    return TS_OK;
+}
+
+int ts_hydro_download_gravity(ts_hydro_ctx* c, int64_t first, int64_t count, double* host) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (host == nullptr || first < 0 || count < 0 || first + count > c->n_owned)
+        return fail(c, TS_EINVAL, "range outside the owned sub-grids");
+    if (c->d_grav == nullptr) return fail(c, TS_ESTATE, "no gravity computed yet (ts_hydro_gravity_p2p)");
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    TS_CUDA(c, cudaMemcpy(host, c->d_grav + (size_t)first * 4 * kNC, (size_t)count * 4 * kNC * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    return TS_OK;
 }
 
 int ts_hydro_finish_step(ts_hydro_ctx* c) {

@@ -158,6 +158,9 @@ _SIGNATURES = {
     "ts_hydro_p2p_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int32]),
     "ts_hydro_set_activity_sink": (ctypes.c_int, [_vp, SINK_FN, _vp]),
     "ts_hydro_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "ts_hydro_gravity_p2p": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int32, _i64p, ctypes.c_int64,
+                                            ctypes.c_uint32, ctypes.c_uint64, DONE_FN, _vp]),
+    "ts_hydro_download_gravity": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _f64p]),
     "ts_hydro_debug_check": (ctypes.c_int, [_vp, _u64p, ctypes.c_int32]),
     "ts_hydro_check_build": (ctypes.c_int, []),
     "ts_hydro_flush_activity": (ctypes.c_int, [_vp, ctypes.POINTER(_Record), ctypes.c_uint64, _u64p]),
@@ -616,6 +619,23 @@ class CudaDevice:
             self._callbacks.append(cb)
         self._check(lib().ts_hydro_launch_stage(self._h, stage, _p(idx, _i64p), len(idx), stream_id, guid, cb, None),
                     "launch_stage")
+
+    def gravity_p2p(self, G: float = 1.0, radius: int = 4, owned_index=None, stream_id: int = 0, guid: int = 0,
+                    done=None) -> None:
+        """Near-field monopole P2P (the reference's p2p_kernel launches, workload.cpp:365-372)."""
+        if owned_index is None:
+            idx, n = None, 0
+        else:
+            idx = np.ascontiguousarray(np.asarray(owned_index, np.int64))
+            n = len(idx)
+        self._check(lib().ts_hydro_gravity_p2p(self._h, G, radius, None if idx is None else _p(idx, _i64p), n,
+                                               stream_id, guid, self._done(done), None), "gravity_p2p")
+
+    def download_gravity(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        n = self.local_counts()[0] if count is None else count
+        out = np.zeros((n, 4, N * N * N), np.float64)
+        self._check(lib().ts_hydro_download_gravity(self._h, first, n, _p(out, _f64p)), "download_gravity")
+        return out
 
     def finish_step(self) -> None:
         self._check(lib().ts_hydro_finish_step(self._h), "finish_step")
