@@ -71,6 +71,21 @@ public:
         return token;
     }
 
+    // The gravity launch of execute_step_body (workload.cpp:565-569) for a
+    // sub-grid gravity_kernel_name calls a p2p_kernel (workload.cpp:365-372):
+    // the near-field monopole P2P of that sub-grid, for real.
+    CompletionToken launch_gravity_p2p(std::int64_t owned_index, std::uint32_t stream_id, Guid guid,
+                                       double G = 1.0, int radius = 4) {
+        auto* promise = new PromiseHandle();
+        CompletionToken token = promise->token();
+        const int rc = ts_hydro_gravity_p2p(ctx_, G, radius, &owned_index, 1, stream_id, guid, &fulfil, promise);
+        if (rc != TS_OK) {
+            delete promise;
+            check(rc, "launch_gravity_p2p");
+        }
+        return token;
+    }
+
     // The rest of SimDevice's public surface (device.hpp:57-64) on the GPU, so
     // a CudaHydroDevice stands in for the SimDevice a Locality owns: named
     // launches occupy their stream for the requested time (the gravity

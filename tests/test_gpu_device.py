@@ -139,31 +139,36 @@ def test_memory_tracking_follows_device_allocs_and_frees(hydro):
     assert [(r.kind, r.bytes) for r in recs] == [("alloc", 100), ("alloc", 50), ("free", 100), ("free", 50)]
 
 
-def test_reference_step_schedule_runs_on_the_gpu(hydro):
-    """One reference step of workload.cpp:554-570 on a real device: per
-    sub-grid 3 fused hydro stages (ts_hydro_launch_stage) and the 6 gravity
-    launches as named timed kernels, each on its own rotating stream."""
+def test_reference_step_schedule_runs_on_the_gpu(hydro, oracle_lib):
+    """One reference step of workload.cpp:554-570 on a real device, no host
+    barrier: per sub-grid 3 fused hydro stages (ts_hydro_launch_stage), then
+    gravity_iterations_per_step = 6 launches of the kernel gravity_kernel_name
+    picks (workload.cpp:365-372: p2p_kernel for a leaf without refined
+    neighbours — every sub-grid of a uniform mesh), now the real near-field
+    P2P (ts_hydro_gravity_p2p), each launch on the next rotating stream."""
     m = hydro.uniform_mesh(2, 2, 2)
     d = _dev(hydro, dx=1.0 / 16)
     d.set_mesh(m)
     d.init_random(1)
     d.compute_dt()
     d.flush_activity()
-    names = ["multipole_kernel", "p2p_kernel", "p2m_kernel", "root_kernel", "m2l_kernel", "l2p_kernel"]
     stream = 0
     for stage in (1, 2, 3):
-        d.synchronize()
         for g in range(m.n):
             d.launch_stage(stage, [g], stream_id=stream % 12, guid=g + 1)
             stream += 1
-    d.synchronize()
     d.finish_step()
     for g in range(m.n):
-        for nm in names:
-            d.launch_kernel(nm, stream % 12, 5_000, guid=g + 1)
+        for _ in range(6):
+            d.gravity_p2p(radius=4, owned_index=[g], stream_id=stream % 12, guid=g + 1)
             stream += 1
     d.synchronize()
     recs = [r for r in d.flush_activity() if r.kind == "kernel"]
+    grav = d.download_gravity()
+    U = d.download()
     d.close()
-    assert len(recs) == m.n * (3 + len(names))  # 9 launches per sub-grid per step (+3 fused, not 6 simulated)
-    assert {r.name for r in recs} >= set(names) | {"hydro_stage1_kernel", "hydro_stage3_kernel"}
+    assert len(recs) == m.n * (3 + 6)  # 9 launches per sub-grid per step (3 fused hydro + 6 gravity)
+    assert {r.name for r in recs} == {"hydro_stage1_kernel", "hydro_stage2_kernel", "hydro_stage3_kernel",
+                                      "p2p_kernel"}
+    want = oracle_lib.gravity_p2p(oracle_lib.params(nf=6, dx=1.0 / 16), m.neighbor_ids, U, radius=4)
+    assert np.array_equal(grav, want)
