@@ -165,6 +165,8 @@ def main(argv=None):
     ap.add_argument("--workload", default="sedov", choices=sorted(WORKLOADS))
     ap.add_argument("--recon", default="ppm", choices=["ppm", "minmod"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--order", default="morton", choices=["morton", "row"],
+                    help="sub-grid numbering of the uniform mesh (launch order, e2e chunks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -208,7 +210,7 @@ def main(argv=None):
         dist.init_process_group("gloo", rank=rank, world_size=world)
     dims = BINARY_DIMS if strong else (edge, edge, edge * world)
     dx = 1.0 / (dims[0] * 8)
-    mesh = H.uniform_mesh(*dims, world=world)
+    mesh = H.uniform_mesh(*dims, world=world, order=a.order)
     cfg = H.HydroConfig(device_id=local_rank, n_species=species, dx=dx, recon=a.recon)
     dev = H.CudaDevice(cfg)
     session = H.WorkloadSession(mesh, dev, H.StepConfig(num_steps=a.steps), rank=rank)

@@ -125,7 +125,10 @@ int ts_hydro_num_fields(const ts_hydro_ctx* ctx);
 /* ---- mesh (Mesh / SubGrid, workload.hpp:53-97) ---------------------------- */
 /* Product-side uniform mesh builder: nx*ny*nz same-level sub-grids numbered
  * along the Morton curve, owners dealt in contiguous chunks like build_mesh
- * (workload.cpp:298-323).  periodic_mask bit d wraps axis d. */
+ * (workload.cpp:298-323).  periodic_mask bit d wraps axis d; with
+ * TS_MESH_ROW_ORDER set the numbering is row-major, x fastest (the shape of
+ * make_row_mesh in the reference's tests, test_workload.cpp:38-54). */
+#define TS_MESH_ROW_ORDER 8
 int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_mask, int32_t world,
                           int64_t* neighbor_ids, int32_t* pos, int32_t* owner);
 /* Binds the global mesh; validates it like Mesh::validate (workload.cpp:140-168).

@@ -1587,9 +1587,15 @@ int ts_hydro_uniform_mesh(int32_t nx, int32_t ny, int32_t nz, int32_t periodic_m
     };
     std::vector<K> keys;
     keys.reserve((size_t)n);
+    // numbering: the Morton curve (build_mesh's order, workload.cpp:298-313),
+    // or with TS_MESH_ROW_ORDER row-major, x fastest (make_row_mesh of the
+    // reference's tests, test_workload.cpp:38-54)
+    const bool row = (periodic_mask & TS_MESH_ROW_ORDER) != 0;
     for (int z = 0; z < nz; ++z)
         for (int y = 0; y < ny; ++y)
-            for (int x = 0; x < nx; ++x) keys.push_back({morton3((uint32_t)x, (uint32_t)y, (uint32_t)z), x, y, z});
+            for (int x = 0; x < nx; ++x)
+                keys.push_back({row ? (uint64_t)(((int64_t)z * ny + y) * nx + x) : morton3((uint32_t)x, (uint32_t)y, (uint32_t)z),
+                                x, y, z});
     std::sort(keys.begin(), keys.end(), [](const K& a, const K& b) { return a.key < b.key; });
     std::vector<int64_t> id_of((size_t)n);
     for (int64_t g = 0; g < n; ++g) {

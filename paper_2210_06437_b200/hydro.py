@@ -381,12 +381,15 @@ class Mesh:
         return int((self.owner[g[m]] == self.owner[nb[m]]).sum()) // 2
 
 
-def uniform_mesh(nx: int, ny: int, nz: int, periodic: str = "", world: int = 1) -> Mesh:
+def uniform_mesh(nx: int, ny: int, nz: int, periodic: str = "", world: int = 1, order: str = "morton") -> Mesh:
+    """order: "morton" (build_mesh's curve) or "row" (x fastest, z slowest)."""
+    if order not in ("morton", "row"):
+        raise ValueError(f"unknown mesh order '{order}'")
     n = nx * ny * nz
     nbr = np.zeros((n, 6), np.int64)
     pos = np.zeros((n, 3), np.int32)
     owner = np.zeros(n, np.int32)
-    mask = sum(1 << "xyz".index(ch) for ch in periodic)
+    mask = sum(1 << "xyz".index(ch) for ch in periodic) | (8 if order == "row" else 0)
     rc = lib().ts_hydro_uniform_mesh(nx, ny, nz, mask, world, _p(nbr, _i64p), _p(pos, _i32p), _p(owner, _i32p))
     if rc != TS_OK:
         raise ValueError("mesh extents and world size must be positive")
