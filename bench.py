@@ -165,8 +165,9 @@ def main(argv=None):
     ap.add_argument("--workload", default="sedov", choices=sorted(WORKLOADS))
     ap.add_argument("--recon", default="ppm", choices=["ppm", "minmod"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--order", default="morton", choices=["morton", "row"],
-                    help="sub-grid numbering of the uniform mesh (launch order, e2e chunks)")
+    ap.add_argument("--order", default="row", choices=["morton", "row"],
+                    help="sub-grid numbering of the uniform mesh = the CTA launch order: row-major (x fastest; "
+                         "make_row_mesh's shape) measured +1.1 %% over the Morton curve on the Sedov mesh")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -375,6 +376,7 @@ def main(argv=None):
             "config": {"workload": f"{a.workload}: {sub_per_gpu} sub-grids (8^3 + 3-deep halo) per GPU, "
                                    f"domain {dims[0]}x{dims[1]}x{dims[2]} sub-grids",
                        "problem": problem, "nf": nf, "recon": a.recon, "total_cells": total_cells,
+                       "numbering": a.order,
                        "parallelism": f"domain decomposition over {world} GPU(s)"
                                       + (f", {a.transport} halos" if world > 1 else ""),
                        "l2": f"working set {state_bytes / 2**20:.0f} MiB (3 state buffers) > 126 MiB L2; no flush"},
