@@ -168,6 +168,18 @@ typedef struct {
 int ts_hydro_set_amr_mesh(ts_hydro_ctx* ctx, int64_t n_leaves, const int64_t* neighbor_ids, const int32_t* level,
                           int32_t max_level, int64_t n_proxy, const ts_amr_proxy* proxies, int64_t n_reflux,
                           const ts_amr_reflux* reflux);
+/* The same global AMR mesh partitioned over `world` ranks (owner[leaf]; the
+ * reference deals leaves along the Morton curve, workload.cpp:298-323):
+ * this rank steps its owned leaves; the remote leaves it reads — same-level
+ * face neighbours, sources of the proxies it fills, the fine leaves of its
+ * reflux records — are refreshed whole before every stage over the context's
+ * transport (ts_hydro_p2p_import or ts_hydro_comm_init); dt is reduced over
+ * the ranks.  Bitwise equal to the one-rank run.  owner == NULL or world == 1:
+ * ts_hydro_set_amr_mesh. */
+int ts_hydro_set_amr_mesh_partitioned(ts_hydro_ctx* ctx, int64_t n_leaves, const int64_t* neighbor_ids,
+                                      const int32_t* level, int32_t max_level, int64_t n_proxy,
+                                      const ts_amr_proxy* proxies, int64_t n_reflux, const ts_amr_reflux* reflux,
+                                      const int32_t* owner, int32_t world, int32_t rank);
 int ts_hydro_local_counts(const ts_hydro_ctx* ctx, int64_t* n_owned, int64_t* n_proxy,
                           int64_t* n_interior);
 int ts_hydro_owned_ids(const ts_hydro_ctx* ctx, int64_t* global_ids);

@@ -172,6 +172,28 @@ def amr_mesh(nx: int, ny: int, nz: int,
     return AmrMesh((nx, ny, nz), used, level, pos, nbr, level_first, prox, refl)
 
 
+def partition(mesh: AmrMesh, world: int) -> np.ndarray:
+    """Owner of every leaf: the reference's deal (build_mesh, workload.cpp:298-323)
+    — sort by the Morton key of the position scaled to the finest level,
+    coarser first on ties, and hand out contiguous chunks, the first
+    n % world ranks one larger."""
+    if world < 1:
+        raise ValueError("world must be positive")
+    shift = mesh.max_level - mesh.level.astype(np.int64)
+    keys = [(_morton3(int(p[0]) << int(s), int(p[1]) << int(s), int(p[2]) << int(s)), int(L), i)
+            for i, (p, s, L) in enumerate(zip(mesh.pos, shift, mesh.level))]
+    keys.sort()
+    n = mesh.n_leaves
+    owner = np.zeros(n, np.int32)
+    base, extra = divmod(n, world)
+    cursor = 0
+    for r in range(world):
+        for _ in range(base + (1 if r < extra else 0)):
+            owner[keys[cursor][2]] = r
+            cursor += 1
+    return owner
+
+
 def from_reference_mesh(level, pos) -> AmrMesh:
     """The leaves of a reference octree (``build_mesh``, workload.cpp:264-327:
     every existing node, refined parents included, with its level and position

@@ -95,19 +95,21 @@ __device__ __forceinline__ int slab_cell(int face, int k) {
     }
 }
 
+// cells = SLAB: entry {sub-grid, face} = the 3-deep slab of that face;
+// cells = NC: entry {sub-grid, -} = the whole sub-grid (AMR ghost leaves)
 __global__ void __launch_bounds__(256) pack_kernel(const double* __restrict__ U, int nf,
                                                    const int2* __restrict__ entries, long long n_entries,
-                                                   double* __restrict__ buf, unsigned long long* stamp) {
+                                                   double* __restrict__ buf, unsigned long long* stamp, int cells) {
     if (stamp != nullptr && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
-    const long long total = n_entries * nf * SLAB;
+    const long long total = n_entries * nf * cells;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int k = (int)(i % SLAB);
-        const long long ef = i / SLAB;
+        const int k = (int)(i % cells);
+        const long long ef = i / cells;
         const int f = (int)(ef % nf);
         const long long e = ef / nf;
         const int2 en = entries[e];
-        buf[i] = __ldg(U + ((size_t)en.x * nf + f) * NC + slab_cell(en.y, k));
+        buf[i] = __ldg(U + ((size_t)en.x * nf + f) * NC + (cells == NC ? k : slab_cell(en.y, k)));
     }
     if (stamp != nullptr) {
         __syncthreads();
@@ -117,17 +119,18 @@ __global__ void __launch_bounds__(256) pack_kernel(const double* __restrict__ U,
 
 __global__ void __launch_bounds__(256) unpack_kernel(double* __restrict__ U, int nf,
                                                      const int2* __restrict__ entries, long long n_entries,
-                                                     const double* __restrict__ buf, unsigned long long* stamp) {
+                                                     const double* __restrict__ buf, unsigned long long* stamp,
+                                                     int cells) {
     if (stamp != nullptr && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
-    const long long total = n_entries * nf * SLAB;
+    const long long total = n_entries * nf * cells;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int k = (int)(i % SLAB);
-        const long long ef = i / SLAB;
+        const int k = (int)(i % cells);
+        const long long ef = i / cells;
         const int f = (int)(ef % nf);
         const long long e = ef / nf;
         const int2 en = entries[e];
-        U[((size_t)en.x * nf + f) * NC + slab_cell(en.y, k)] = buf[i];
+        U[((size_t)en.x * nf + f) * NC + (cells == NC ? k : slab_cell(en.y, k))] = buf[i];
     }
     if (stamp != nullptr) {
         __syncthreads();
@@ -293,16 +296,16 @@ cudaError_t launch_init_random(double* U, int nf, const long long* gid, long lon
 }
 
 cudaError_t launch_pack(const double* U, int nf, const int2* entries, long long n, double* buf, int sms,
-                        cudaStream_t s, unsigned long long* stamp) {
+                        cudaStream_t s, unsigned long long* stamp, int cells) {
     if (n <= 0) return cudaSuccess;
-    pack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp);
+    pack_kernel<<<grid_for(n * nf * cells, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp, cells);
     return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(double* U, int nf, const int2* entries, long long n, const double* buf, int sms,
-                          cudaStream_t s, unsigned long long* stamp) {
+                          cudaStream_t s, unsigned long long* stamp, int cells) {
     if (n <= 0) return cudaSuccess;
-    unpack_kernel<<<grid_for(n * nf * SLAB, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp);
+    unpack_kernel<<<grid_for(n * nf * cells, 256, sms), 256, 0, s>>>(U, nf, entries, n, buf, stamp, cells);
     return cudaGetLastError();
 }
 

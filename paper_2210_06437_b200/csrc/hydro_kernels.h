@@ -179,10 +179,11 @@ cudaError_t launch_signal(const double* U, int nf, long long n_grids, double gam
                           double* amax, unsigned long long* stamp, int sms, cudaStream_t s);
 cudaError_t launch_init_random(double* U, int nf, const long long* gid, long long n_grids, uint64_t seed,
                                double gamma, int sms, cudaStream_t s);
+// cells per entry: SLAB (3-deep face slab {sub-grid, face}) or NC (whole sub-grid)
 cudaError_t launch_pack(const double* U, int nf, const int2* entries, long long n, double* buf, int sms,
-                        cudaStream_t s, unsigned long long* stamp);
+                        cudaStream_t s, unsigned long long* stamp, int cells = 3 * 8 * 8);
 cudaError_t launch_unpack(double* U, int nf, const int2* entries, long long n, const double* buf, int sms,
-                          cudaStream_t s, unsigned long long* stamp);
+                          cudaStream_t s, unsigned long long* stamp, int cells = 3 * 8 * 8);
 cudaError_t launch_face_exchange(const double* U, int nf, const int* nbr, long long n_owned, double* ghost,
                                  int sms, cudaStream_t s);
 cudaError_t launch_fill_halo(const double* U, int nf, const int* nbr, long long n_owned, int h,

@@ -320,9 +320,15 @@ struct ts_hydro_ctx {
 
     // coarse-fine AMR mesh (ts_hydro_set_amr_mesh): leaves level-major, proxies after them
     bool amr = false;
+    // multi-rank AMR (ts_hydro_set_amr_mesh_partitioned): owned leaves, then
+    // ghost leaves (whole-sub-grid copies of remote leaves the rank reads),
+    // then the proxies it fills; halo entries move whole sub-grids
+    bool amr_mr = false;
+    int xfer_cells = kSlab;  // cells per halo entry: a 3-deep slab, or a whole sub-grid (multi-rank AMR)
     int amr_max_level = 0;
     std::vector<int64_t> amr_level_first;  // [max_level + 2]
     int64_t amr_n_proxy = 0, amr_n_rec = 0;
+    int64_t amr_proxy_first = 0;            // local index of the first proxy (n_owned; + ghosts on several ranks)
     tsh::AmrProxy* d_amr_proxy = nullptr;
     unsigned char* d_amr_pmask = nullptr;  // per proxy: faces read (launch_amr_fill)
     bool amr_slab_fill = true;             // TS_HYDRO_AMR_FULLFILL=1: fill whole proxies
@@ -511,6 +517,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_amr_rec);
     dfree(c, &c->d_amr_level);
     c->amr = false;
+    c->amr_mr = false;
+    c->xfer_cells = kSlab;
     c->have_mesh = false;
     c->tmap_ok = false;
 }
@@ -700,6 +708,7 @@ uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
 }
 
 int build_plans(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner) {
+    if (c->amr_mr) return TS_OK;  // multi-rank AMR plans are built by ts_hydro_set_amr_mesh_partitioned
     c->peers.clear();
     if (c->world <= 1) return TS_OK;
     std::vector<Peer> peers((size_t)c->world);
@@ -845,7 +854,8 @@ int pack_on_comm(ts_hydro_ctx* c, const double* buf) {
         unsigned long long* stamp = nullptr;
         rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNamePack, 1, 0, &stamp);
         if (rc) return rc;
-        TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs, stamp));
+        TS_CUDA(c, tsh::launch_pack(buf, c->nf, c->d_send_entries, c->n_send_total, c->d_send, c->sms, cs, stamp,
+                                    c->xfer_cells));
     }
     return TS_OK;
 }
@@ -858,7 +868,7 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf, bool packed = false) {
         rc = pack_on_comm(c, buf);
         if (rc) return rc;
     }
-    const size_t per = (size_t)c->nf * kSlab;
+    const size_t per = (size_t)c->nf * c->xfer_cells;
     double* recv = c->d_recv;
     if (c->p2p) {
         StreamMemOps& m = memops();
@@ -894,7 +904,8 @@ int exchange_on_comm(ts_hydro_ctx* c, double* buf, bool packed = false) {
         unsigned long long* stamp = nullptr;
         rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameUnpack, 1, 0, &stamp);
         if (rc) return rc;
-        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, recv, c->sms, cs, stamp));
+        TS_CUDA(c, tsh::launch_unpack(buf, c->nf, c->d_recv_entries, c->n_recv_total, recv, c->sms, cs, stamp,
+                                      c->xfer_cells));
     }
     return TS_OK;
 }
@@ -967,9 +978,22 @@ int do_step_amr(ts_hydro_ctx* c) {
     int rc = ensure_stream(c, 0, &s);
     if (rc) return rc;
     const double* dt_ptr = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+    const bool multi = c->world > 1;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
         unsigned long long* stamp = nullptr;
+        if (multi) {
+            // ghost leaves of U^(k-1): whole sub-grids from their owners
+            cudaStream_t cs;
+            rc = ensure_stream(c, 1, &cs);
+            if (rc) return rc;
+            TS_CUDA(c, cudaEventRecord(c->ev_in, s));
+            TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+            rc = exchange_on_comm(c, const_cast<double*>(a.Uprev));
+            if (rc) return rc;
+            TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
+            TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+        }
         if (c->amr_n_proxy > 0) {
             rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrFill, 0, 0, &stamp);
             if (rc) return rc;
@@ -1015,13 +1039,13 @@ int do_step_amr(ts_hydro_ctx* c) {
                                               c->amr_n_rec, stage, dt_ptr, stamp, s));
         }
     }
+    double* slot = amax_slot(c, c->steps_done + 1);
     if (c->amr_n_rec > 0) {
         // The stage-3 kernel reduced the signal speed of U^{n+1} as it wrote
         // it, but the reflux after it corrects coarse cells: the next dt must
         // come from the corrected state (the oracle's max_signal_speed of the
         // final U^{n+1}).  Found by the reference-octree AMR parity test
         // (minmod: the maximum sat on a refluxed cell).
-        double* slot = amax_slot(c, c->steps_done + 1);
         TS_CUDA(c, cudaMemsetAsync(slot, 0, sizeof(double), s));
         unsigned long long* stamp = nullptr;
         rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameSignal, 0, 0, &stamp);
@@ -1030,6 +1054,12 @@ int do_step_amr(ts_hydro_ctx* c) {
                                       c->sms, s));
     }
     c->amax_src = nullptr;
+    if (multi) {
+        // the global max over the ranks (p2p gather or NCCL all-reduce), the
+        // next step's dt (reduce_amax points amax_src at the result)
+        rc = reduce_amax(c, slot, s);
+        if (rc) return rc;
+    }
     c->flow_chain = false;
     c->steps_done++;
     return TS_OK;
@@ -1857,9 +1887,9 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         }
         rc = dalloc(c, &c->d_send_entries, se.size());
         if (!rc) rc = dalloc(c, &c->d_recv_entries, re.size());
-        if (!rc) rc = dalloc(c, &c->d_send, (size_t)c->n_send_total * c->nf * kSlab);
+        if (!rc) rc = dalloc(c, &c->d_send, (size_t)c->n_send_total * c->nf * c->xfer_cells);
         // two halves: the P2P transport alternates them by exchange parity
-        if (!rc) rc = dalloc(c, &c->d_recv, 2 * (size_t)c->n_recv_total * c->nf * kSlab);
+        if (!rc) rc = dalloc(c, &c->d_recv, 2 * (size_t)c->n_recv_total * c->nf * c->xfer_cells);
         if (!rc) rc = dalloc(c, &c->d_flags, 2 * (size_t)world);
         if (!rc) rc = dalloc(c, &c->d_gather, 2 * (size_t)world);
         if (!rc) rc = dalloc(c, &c->d_ctr, 4);  // [0] dt push, [1..3] halo push by stage slot
@@ -1874,6 +1904,7 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         c->halo_recv_mask = 0;
         for (const Peer& p : c->peers) {
             if (p.n_recv > 0) c->halo_recv_mask |= 1ull << p.rank;
+            if (c->amr_mr) continue;  // no fused push on the AMR path
             for (int64_t k = 0; k < p.n_send; ++k) {
                 const int64_t l = local_of(c, p.send_pairs[(size_t)(2 * k)]);
                 const int f = (int)p.send_pairs[(size_t)(2 * k + 1)];
@@ -1902,21 +1933,17 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
     return TS_OK;
 }
 
-int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const int32_t* level, int32_t max_level,
-                          int64_t np, const ts_amr_proxy* px, int64_t nr, const ts_amr_reflux* rf) {
-    static_assert(sizeof(ts_amr_proxy) == sizeof(tsh::AmrProxy), "proxy layout");
-    static_assert(sizeof(ts_amr_reflux) == sizeof(tsh::AmrReflux), "reflux layout");
-    int rc = guard(c);
-    if (rc) return rc;
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
-    if ((rc = mutating(c)) != TS_OK) return rc;
+static int amr_validate(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const int32_t* level, int32_t max_level,
+                        int64_t np, const ts_amr_proxy* px, int64_t nr, const ts_amr_reflux* rf,
+                        std::vector<int64_t>& first) {
+    int rc = TS_OK;
     if (nl < 1 || nbr == nullptr || level == nullptr) return fail(c, TS_EINVAL, "empty AMR mesh");
     if (np < 0 || nr < 0 || (np > 0 && px == nullptr) || (nr > 0 && rf == nullptr))
         return fail(c, TS_EINVAL, "AMR proxy / reflux tables missing");
     if (max_level < 0 || max_level > 30) return fail(c, TS_EINVAL, "max_level outside 0..30");
     if (nl + np > (int64_t)INT32_MAX / 2) return fail(c, TS_EINVAL, "too many sub-grids");
     const int64_t nt = nl + np;
-    std::vector<int64_t> first((size_t)max_level + 2, 0);
+    first.assign((size_t)max_level + 2, 0);
     for (int64_t i = 0; i < nl; ++i) {
         const std::string where = "leaf " + std::to_string(i) + ": ";
         if (level[i] < 0 || level[i] > max_level) return fail(c, TS_EINVAL, where + "level outside 0..max_level");
@@ -1952,6 +1979,20 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
                     return fail(c, TS_EINVAL, where + "fine ids must be leaves one level finer");
         }
     }
+    return rc;
+}
+
+int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const int32_t* level, int32_t max_level,
+                          int64_t np, const ts_amr_proxy* px, int64_t nr, const ts_amr_reflux* rf) {
+    static_assert(sizeof(ts_amr_proxy) == sizeof(tsh::AmrProxy), "proxy layout");
+    static_assert(sizeof(ts_amr_reflux) == sizeof(tsh::AmrReflux), "reflux layout");
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
+    std::vector<int64_t> first;
+    if ((rc = amr_validate(c, nl, nbr, level, max_level, np, px, nr, rf, first)) != TS_OK) return rc;
+    const int64_t nt = nl + np;
     if (!c->host_only) {
         cudaSetDevice(c->dev);
         rc = sync_all(c);
@@ -2000,6 +2041,204 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
         if (nr > 0)
             TS_CUDA(c, cudaMemcpy(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaMemcpy(c->d_amr_level, level, (size_t)nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    c->amr = true;
+    return TS_OK;
+}
+
+// Multi-rank AMR.  Every rank derives, from the global leaf mesh and the
+// owner of every leaf, what each rank reads: its owned leaves, the remote
+// leaves it needs whole (same-level face neighbours of owned leaves, sources
+// of the proxies it fills, the fine leaves of its reflux records), and the
+// proxies it fills (those its owned leaves point at, and those through which
+// a reflux fine leaf reads the coarse side).  Ghost leaves are refreshed
+// whole before every stage (pack -> copy engine / NCCL -> unpack), then the
+// proxies are filled from local data and the stage / reflux kernels run on
+// the owned leaves exactly as on one rank.
+namespace {
+struct AmrNeeds {
+    std::vector<int64_t> owned, ghosts, proxies;
+};
+AmrNeeds amr_needs(int64_t nl, const int64_t* nbr, const ts_amr_proxy* px, int64_t nr, const ts_amr_reflux* rf,
+                   const int32_t* owner, int32_t r) {
+    AmrNeeds n;
+    std::set<int64_t> ghosts, proxies;
+    for (int64_t g = 0; g < nl; ++g) {
+        if (owner[g] != r) continue;
+        n.owned.push_back(g);
+        for (int f = 0; f < 6; ++f) {
+            const int64_t h = nbr[6 * g + f];
+            if (h < 0) continue;
+            if (h >= nl) proxies.insert(h);
+            else if (owner[h] != r) ghosts.insert(h);
+        }
+    }
+    for (int64_t k = 0; k < nr; ++k) {
+        const ts_amr_reflux& rec = rf[k];
+        if (owner[rec.coarse] != r) continue;
+        for (int f = 0; f < 6; ++f) {
+            if (rec.fine[f][0] < 0) continue;
+            for (int q = 0; q < 4; ++q) {
+                const int64_t fl = rec.fine[f][q];
+                if (owner[fl] != r) ghosts.insert(fl);
+                const int64_t via = nbr[6 * fl + (f ^ 1)];  // the fine leaf's view of the coarse side
+                if (via >= nl) proxies.insert(via);
+            }
+        }
+    }
+    for (int64_t p : proxies) {
+        const ts_amr_proxy& q = px[p - nl];
+        for (int o = 0; o < (q.kind == 0 ? 1 : 8); ++o)
+            if (owner[q.src[o]] != r) ghosts.insert(q.src[o]);
+    }
+    n.ghosts.assign(ghosts.begin(), ghosts.end());
+    n.proxies.assign(proxies.begin(), proxies.end());
+    return n;
+}
+}  // namespace
+
+int ts_hydro_set_amr_mesh_partitioned(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const int32_t* level,
+                                      int32_t max_level, int64_t np, const ts_amr_proxy* px, int64_t nr,
+                                      const ts_amr_reflux* rf, const int32_t* owner, int32_t world, int32_t rank) {
+    if (owner == nullptr || world == 1) return ts_hydro_set_amr_mesh(c, nl, nbr, level, max_level, np, px, nr, rf);
+    int rc = guard(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
+    if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return fail(c, TS_EINVAL, "bad world / rank");
+    std::vector<int64_t> first_global;
+    if ((rc = amr_validate(c, nl, nbr, level, max_level, np, px, nr, rf, first_global)) != TS_OK) return rc;
+    for (int64_t g = 0; g < nl; ++g)
+        if (owner[g] < 0 || owner[g] >= world) return fail(c, TS_EINVAL, "leaf " + std::to_string(g) + ": owner out of range");
+    std::vector<AmrNeeds> need((size_t)world);
+    for (int r = 0; r < world; ++r) need[(size_t)r] = amr_needs(nl, nbr, px, nr, rf, owner, r);
+    const AmrNeeds& me = need[(size_t)rank];
+    if (me.owned.empty()) return fail(c, TS_EINVAL, "a rank owns no leaf");
+    if (!c->host_only) {
+        cudaSetDevice(c->dev);
+        rc = sync_all(c);
+        if (rc) return rc;
+        free_mesh(c);
+    }
+    const int64_t nt = nl + np;
+    std::vector<int64_t> loc((size_t)nt, -1);
+    int64_t k = 0;
+    for (int64_t g : me.owned) loc[(size_t)g] = k++;
+    for (int64_t g : me.ghosts) loc[(size_t)g] = k++;
+    for (int64_t p : me.proxies) loc[(size_t)p] = k++;
+    const int64_t n_owned = (int64_t)me.owned.size(), n_ghost = (int64_t)me.ghosts.size();
+    const int64_t n_leaf_local = n_owned + n_ghost, n_local = k;
+    c->world = world;
+    c->rank = rank;
+    c->n_global = nl;
+    c->mesh_nbr.assign(nbr, nbr + 6 * nl);
+    c->mesh_owner.assign(owner, owner + nl);
+    c->owned_gid = me.owned;
+    c->proxy_gid = me.ghosts;
+    c->proxy_gid.insert(c->proxy_gid.end(), me.proxies.begin(), me.proxies.end());
+    c->n_owned = n_owned;
+    c->n_proxy = n_local - n_owned;
+    c->nbr_local.assign((size_t)n_local * 6, -1);
+    for (int64_t i = 0; i < n_leaf_local; ++i) {
+        const int64_t g = i < n_owned ? me.owned[(size_t)i] : me.ghosts[(size_t)(i - n_owned)];
+        for (int f = 0; f < 6; ++f) {
+            const int64_t h = nbr[6 * g + f];
+            const int64_t l = h >= 0 ? loc[(size_t)h] : -1;
+            if (i < n_owned && h >= 0 && l < 0)
+                return fail(c, TS_EINVAL, "internal: an owned leaf's neighbour is not local");
+            c->nbr_local[(size_t)i * 6 + f] = (int32_t)l;
+        }
+    }
+    c->interior.resize((size_t)n_owned);
+    for (int64_t i = 0; i < n_owned; ++i) c->interior[(size_t)i] = (int32_t)i;
+    c->boundary.clear();
+    // halo plan: whole sub-grids, my owned leaves each peer holds as ghosts / my ghosts it owns
+    std::vector<Peer> peers((size_t)world);
+    for (int q = 0; q < world; ++q) {
+        Peer& p = peers[(size_t)q];
+        p.rank = q;
+        if (q == rank) continue;
+        for (int64_t g : need[(size_t)q].ghosts)
+            if (owner[g] == rank) {
+                p.send_pairs.push_back(g);
+                p.send_pairs.push_back(6);
+                p.send_dst.push_back(-1);
+            }
+        for (int64_t g : me.ghosts)
+            if (owner[g] == q) {
+                p.recv_pairs.push_back(g);
+                p.recv_pairs.push_back(6);
+            }
+    }
+    int64_t so = 0, ro = 0;
+    for (Peer& p : peers) {
+        p.n_send = (int64_t)p.send_pairs.size() / 2;
+        p.n_recv = (int64_t)p.recv_pairs.size() / 2;
+        p.send_off = so;
+        p.recv_off = ro;
+        so += p.n_send;
+        ro += p.n_recv;
+    }
+    c->n_send_total = so;
+    c->n_recv_total = ro;
+    c->peers = std::move(peers);
+    c->amr_mr = true;
+    c->xfer_cells = kNC;
+    rc = bind_mesh(c, nullptr, nullptr, world);
+    if (rc) return rc;
+    // local AMR tables: proxies, reflux records of owned coarse leaves, levels
+    std::vector<tsh::AmrProxy> lpx;
+    for (int64_t p : me.proxies) {
+        const ts_amr_proxy& q = px[p - nl];
+        tsh::AmrProxy r{};
+        r.dst = (int)loc[(size_t)p];
+        r.kind = q.kind;
+        r.octant = q.octant;
+        for (int o = 0; o < 8; ++o) r.src[o] = (q.kind == 0 && o > 0) ? -1 : (int)loc[(size_t)q.src[o]];
+        lpx.push_back(r);
+    }
+    std::vector<tsh::AmrReflux> lrf;
+    for (int64_t i = 0; i < nr; ++i) {
+        if (owner[rf[i].coarse] != rank) continue;
+        tsh::AmrReflux r{};
+        r.coarse = (int)loc[(size_t)rf[i].coarse];
+        for (int f = 0; f < 6; ++f)
+            for (int q = 0; q < 4; ++q) r.fine[f][q] = rf[i].fine[f][0] < 0 ? -1 : (int)loc[(size_t)rf[i].fine[f][q]];
+        lrf.push_back(r);
+    }
+    std::vector<int32_t> llev((size_t)n_leaf_local);
+    for (int64_t i = 0; i < n_leaf_local; ++i)
+        llev[(size_t)i] = level[i < n_owned ? me.owned[(size_t)i] : me.ghosts[(size_t)(i - n_owned)]];
+    std::vector<int64_t> first((size_t)max_level + 2, 0);
+    for (int L = 0; L <= max_level + 1; ++L)
+        first[(size_t)L] = std::lower_bound(llev.begin(), llev.begin() + n_owned, L) - llev.begin();
+    c->amr_max_level = max_level;
+    c->amr_level_first = first;
+    c->amr_proxy_first = n_leaf_local;  // proxies follow the ghost leaves
+    c->amr_n_proxy = (int64_t)lpx.size();
+    c->amr_n_rec = (int64_t)lrf.size();
+    if (!c->host_only) {
+        const int64_t npl = (int64_t)lpx.size(), nrl = (int64_t)lrf.size();
+        rc = dalloc(c, &c->d_amr_proxy, (size_t)std::max<int64_t>(npl, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_pmask, (size_t)std::max<int64_t>(npl, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_rec, (size_t)std::max<int64_t>(nrl, 1));
+        if (!rc) rc = dalloc(c, &c->d_amr_level, (size_t)n_leaf_local);
+        if (rc) return rc;
+        if (npl > 0) {
+            TS_CUDA(c, cudaMemcpy(c->d_amr_proxy, lpx.data(), (size_t)npl * sizeof(tsh::AmrProxy), cudaMemcpyHostToDevice));
+            // local leaf i reads proxy p = nbr_local[i][f] through p's face f ^ 1
+            std::vector<unsigned char> pm((size_t)npl, 0);
+            for (int64_t i = 0; i < n_leaf_local; ++i)
+                for (int f = 0; f < 6; ++f) {
+                    const int32_t h = c->nbr_local[(size_t)i * 6 + f];
+                    if (h >= n_leaf_local) pm[(size_t)(h - n_leaf_local)] |= (unsigned char)(1u << (f ^ 1));
+                }
+            TS_CUDA(c, cudaMemcpy(c->d_amr_pmask, pm.data(), (size_t)npl, cudaMemcpyHostToDevice));
+        }
+        if (nrl > 0)
+            TS_CUDA(c, cudaMemcpy(c->d_amr_rec, lrf.data(), (size_t)nrl * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
+        TS_CUDA(c, cudaMemcpy(c->d_amr_level, llev.data(), (size_t)n_leaf_local * sizeof(int32_t),
+                              cudaMemcpyHostToDevice));
     }
     c->amr = true;
     return TS_OK;

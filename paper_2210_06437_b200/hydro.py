@@ -126,6 +126,9 @@ _SIGNATURES = {
     "ts_hydro_set_mesh": (ctypes.c_int, [_vp, ctypes.c_int64, _i64p, _i32p, ctypes.c_int32, ctypes.c_int32]),
     "ts_hydro_set_amr_mesh": (ctypes.c_int, [_vp, ctypes.c_int64, _i64p, _i32p, ctypes.c_int32, ctypes.c_int64,
                                              _i32p, ctypes.c_int64, _i32p]),
+    "ts_hydro_set_amr_mesh_partitioned": (ctypes.c_int, [_vp, ctypes.c_int64, _i64p, _i32p, ctypes.c_int32,
+                                                         ctypes.c_int64, _i32p, ctypes.c_int64, _i32p, _i32p,
+                                                         ctypes.c_int32, ctypes.c_int32]),
     "ts_hydro_local_counts": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
     "ts_hydro_owned_ids": (ctypes.c_int, [_vp, _i64p]),
     "ts_hydro_halo_plan": (ctypes.c_int, [_vp, ctypes.c_int32, _i64p, _i64p, _i64p, _i64p]),
@@ -495,18 +498,26 @@ class CudaDevice:
         self.mesh = mesh
         self.rank = rank
 
-    def set_amr_mesh(self, mesh) -> None:
-        """Bind a coarse-fine AMR mesh (paper_2210_06437_b200.amr.AmrMesh), single rank."""
+    def set_amr_mesh(self, mesh, owner=None, rank: int = 0, world: Optional[int] = None) -> None:
+        """Bind a coarse-fine AMR mesh (paper_2210_06437_b200.amr.AmrMesh); with
+        owner (per leaf, e.g. amr.partition) the rank's part of a multi-rank run."""
         nbr = np.ascontiguousarray(mesh.nbr, np.int64)
         lev = np.ascontiguousarray(mesh.level, np.int32)
         px = np.ascontiguousarray(mesh.proxies, np.int32)
         rf = np.ascontiguousarray(mesh.reflux, np.int32)
-        self._check(lib().ts_hydro_set_amr_mesh(self._h, mesh.n_leaves, _p(nbr, _i64p), _p(lev, _i32p),
-                                                mesh.max_level, mesh.n_proxy, _p(px, _i32p), len(rf),
-                                                _p(rf, _i32p)), "set_amr_mesh")
+        if owner is None:
+            self._check(lib().ts_hydro_set_amr_mesh(self._h, mesh.n_leaves, _p(nbr, _i64p), _p(lev, _i32p),
+                                                    mesh.max_level, mesh.n_proxy, _p(px, _i32p), len(rf),
+                                                    _p(rf, _i32p)), "set_amr_mesh")
+        else:
+            own = np.ascontiguousarray(owner, np.int32)
+            world = int(own.max()) + 1 if world is None else world
+            self._check(lib().ts_hydro_set_amr_mesh_partitioned(
+                self._h, mesh.n_leaves, _p(nbr, _i64p), _p(lev, _i32p), mesh.max_level, mesh.n_proxy,
+                _p(px, _i32p), len(rf), _p(rf, _i32p), _p(own, _i32p), world, rank), "set_amr_mesh")
         self.mesh = None
         self.amr_mesh = mesh
-        self.rank = 0
+        self.rank = rank
 
     def local_counts(self):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -260,3 +260,34 @@ def test_reference_octree_amr_oracle_conserves_and_keeps_free_stream(oracle_lib,
     U[:, 4] = 2.0
     out, _ = oracle_lib.run_amr(oracle_lib.params(nf=6, dx=dx), a, U, 2)
     assert np.array_equal(out[:a.n_leaves], U[:a.n_leaves])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_amr_plans_pair_up_across_ranks(hydro, golden, world):
+    """Multi-rank AMR host plans (ts_hydro_set_amr_mesh_partitioned on
+    host-only contexts): the reference's Morton deal over the leaves of its
+    own levels-4 octree; every whole-sub-grid ghost a rank receives from a
+    peer is exactly what that peer sends it, in the same order."""
+    vec, _ = golden
+    m = max(vec["build_mesh"], key=lambda e: len(e["level"]))
+    a = amr.from_reference_mesh(m["level"], m["pos"])
+    owner = amr.partition(a, world)
+    assert np.bincount(owner).tolist() == [len(owner) // world + (1 if r < len(owner) % world else 0)
+                                           for r in range(world)]
+    plans = []
+    for r in range(world):
+        d = hydro.CudaDevice(hydro.HydroConfig(device_id=-1))
+        d.set_amr_mesh(a, owner=owner, rank=r, world=world)
+        n_owned, n_extra, _ = d.local_counts()
+        assert n_owned == int((owner == r).sum())
+        plans.append({q: d.halo_plan(q) for q in range(world) if q != r})
+        d.close()
+    for r in range(world):
+        for q in range(world):
+            if q == r:
+                continue
+            send_rq = plans[r][q][0]
+            recv_qr = plans[q][r][1]
+            assert np.array_equal(send_rq, recv_qr)
+            assert (send_rq[:, 1] == 6).all()  # whole sub-grids
+            assert (owner[send_rq[:, 0]] == r).all()

@@ -98,3 +98,22 @@ def test_mismatched_collective_call_fails_instead_of_hanging(transport):
     r = _torchrun(["--mismatch", "--transport", transport], 300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MISMATCH DETECTED" in r.stdout
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("args", [["--amr", "lshape", "--steps", "3"],
+                                  ["--amr", "ref4", "--steps", "3", "--species", "5"],
+                                  ["--amr", "ref4", "--steps", "2", "--recon", "minmod"]])
+def test_multi_rank_amr_bitwise_equal_to_single_rank(args, transport):
+    """Coarse-fine AMR partitioned over two ranks (the reference's Morton deal
+    of the leaves, workload.cpp:298-323; ghost leaves refreshed whole before
+    every stage; dt reduced over the ranks): bitwise the one-rank run.  On one
+    GPU the two ranks share it (CUDA IPC, copy-engine transport); NCCL needs
+    two GPUs."""
+    n = _gpus()
+    if n < 1 or (transport == "nccl" and n < 2):
+        pytest.skip("needs a GPU (NCCL: two)")
+    extra = ["--same-device"] if n < 2 else []
+    r = _torchrun([*args, "--transport", transport, *extra], 600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout

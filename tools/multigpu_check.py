@@ -34,6 +34,9 @@ def main():
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (two processes sharing one GPU through CUDA IPC, time-sliced): "
                          "the cross-rank path on a one-GPU box")
+    ap.add_argument("--amr", default="", choices=["", "lshape", "ref4"],
+                    help="multi-rank coarse-fine AMR: an L-shaped refinement of a 4^3 box, or the reference's own "
+                         "levels-4 build_mesh octree (tests/golden), dealt along the Morton curve")
     ap.add_argument("--mismatch", action="store_true",
                     help="rank 1 makes one stepping call too many: it must fail with TS_ECOMM, not hang")
     a = ap.parse_args()
@@ -46,6 +49,8 @@ def main():
     if a.same_device and a.transport == "nccl":
         raise SystemExit("NCCL refuses two ranks on one GPU: --same-device takes p2p / p2p-ce")
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    if a.amr:
+        return amr_check(a, rank, world, local)
     cfg = H.HydroConfig(device_id=local, n_species=a.species, dx=1.0 / (8 * a.dims[0]), recon=a.recon)
     mesh = H.uniform_mesh(*a.dims, periodic=a.periodic, world=world)
     dev = H.CudaDevice(cfg)
@@ -111,6 +116,63 @@ def main():
         print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
               f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}"
               + (" same-device" if a.same_device else ""), flush=True)
+    dist.destroy_process_group()
+    return 0 if flag.item() == 1 else 1
+
+
+def amr_check(a, rank, world, local):
+    """Multi-rank AMR: each rank steps its Morton chunk of the leaves (ghost
+    leaves refreshed whole before every stage, dt reduced over the ranks) and
+    compares its leaves bitwise with the one-rank AMR run on its own GPU."""
+    import json
+    from paper_2210_06437_b200 import amr
+    if a.amr == "lshape":
+        mesh = amr.amr_mesh(4, 4, 4, {(0, 1, 1, 1), (0, 2, 1, 1), (0, 1, 2, 1), (0, 1, 1, 2), (0, 2, 2, 2)})
+        dx, centre = 1.0 / 64, (0.625, 0.625, 0.5)
+    else:
+        vec = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_vectors.json")))
+        m = max(vec["build_mesh"], key=lambda e: len(e["level"]))
+        mesh = amr.from_reference_mesh(m["level"], m["pos"])
+        dx, centre = 1.0 / (8 << mesh.max_level), (0.4, 0.55, 0.5)
+    nf = 6 + a.species
+    U0 = amr.ic_blast(mesh, nf, dx, width=0.08, centre=centre, drift=(0.3, -0.1, 0.2))
+    owner = amr.partition(mesh, world)
+    cfg = H.HydroConfig(device_id=local, n_species=a.species, dx=dx, recon=a.recon)
+    dev = H.CudaDevice(cfg)
+    dev.set_amr_mesh(mesh, owner=owner, rank=rank, world=world)
+    if a.transport == "nccl":
+        uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.comm_init(uid[0], world, rank)
+    else:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dev.p2p_export())
+        dev.p2p_import(blobs)
+    owned = dev.owned_ids()
+    dev.upload(U0[owned])
+    dev.step(1)
+    if a.steps > 1:
+        dev.step(a.steps - 1)
+    got = dev.download()
+    dt = dev.last_dt()
+    n_owned, n_extra, _ = dev.local_counts()
+    dev.close()
+    ref = H.CudaDevice(cfg)
+    ref.set_amr_mesh(mesh)
+    ref.upload(U0[:mesh.n_leaves])
+    ref.step(a.steps)
+    want = ref.download()[owned]
+    dt_ref = ref.last_dt()
+    ref.close()
+    ok = bool(np.array_equal(got, want)) and dt == dt_ref
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    print(f"rank {rank}: owned leaves {n_owned} ghost leaves + proxies {n_extra} bitwise={ok} dt={dt!r}", flush=True)
+    dist.barrier()
+    if rank == 0:
+        print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
+              f" AMR {a.amr} world={world} leaves={mesh.n_leaves} steps={a.steps} species={a.species} "
+              f"transport={a.transport}" + (" same-device" if a.same_device else ""), flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 1 else 1
 
