@@ -62,6 +62,9 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 // Measured same-box A/B (round 2), both neutral or slower, kept off: release
 // store / red for the dataflow flags instead of fence + atomic (±0 %), the six
 // neighbour ids loaded before the waits (−0.5 %).
+#ifndef TS_SLOT2
+#define TS_SLOT2 0  // measured: -0.1 % (the bank conflicts it removes are not on the critical path)
+#endif
 #ifndef TS_REL_FLAGS
 #define TS_REL_FLAGS 0
 #endif
@@ -145,7 +148,14 @@ __device__ __forceinline__ int sm_slot(int o) {
     const int r = o >> 4;
     return (r << 4) + ((((o >> 1) & 7) ^ (r & 7)) << 1) + (o & 1);
 #else
+#if TS_SLOT2
+    // x ^= y within the row and, from z >= 2 on, y ^= 1 inside its pair of
+    // planes: every sweep's 32 lanes hit each 8-byte bank pair exactly twice
+    // (the minimum, 2 wavefronts; the plain row swizzle left x and y at 4)
+    return o ^ ((o >> 3) & 7) ^ ((o >> 4) & 8);
+#else
     return o ^ ((o >> 3) & 7);
+#endif
 #endif
 }
 
