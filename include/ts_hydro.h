@@ -184,7 +184,8 @@ int ts_hydro_local_counts(const ts_hydro_ctx* ctx, int64_t* n_owned, int64_t* n_
                           int64_t* n_interior);
 int ts_hydro_owned_ids(const ts_hydro_ctx* ctx, int64_t* global_ids);
 /* Halo plan toward `peer`: number of 3-deep slabs sent, and per slab the
- * (global sub-grid id, face of that sub-grid) pairs in wire order. */
+ * (global sub-grid id, face of that sub-grid) pairs in wire order (face 6:
+ * the whole sub-grid — the ghost leaves of a partitioned AMR mesh). */
 int ts_hydro_halo_plan(const ts_hydro_ctx* ctx, int32_t peer, int64_t* n_send, int64_t* send_pairs,
                        int64_t* n_recv, int64_t* recv_pairs);
 
@@ -216,7 +217,12 @@ int ts_hydro_step_host(ts_hydro_ctx* ctx, const double* host_in, double* host_ou
  * in sub-grid chunks on their own streams; when host_in is the previous
  * call's host_out (a simulation chained through host memory) each H2D chunk
  * starts as soon as the previous call's D2H of that chunk landed, so the two
- * PCIe directions overlap.  Host buffers must stay valid until `done`. */
+ * PCIe directions overlap.  A chained call also takes the step's dt from the
+ * previous call's stage-3 reduction (its input IS that call's output) and
+ * starts stage 1 under the H2D: the host must not modify host_in between the
+ * two calls (pass a different buffer to restart from new data — that call is
+ * not chained and recomputes dt after its H2D).  Host buffers must stay valid
+ * until `done`. */
 int ts_hydro_step_host_async(ts_hydro_ctx* ctx, const double* host_in, double* host_out, uint64_t nsteps,
                              ts_done_fn done, void* user);
 int ts_hydro_synchronize(ts_hydro_ctx* ctx);
