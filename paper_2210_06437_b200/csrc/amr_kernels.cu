@@ -249,7 +249,55 @@ __global__ void __launch_bounds__(kRefluxThreads) amr_reflux_kernel(const double
     stamp_end(stamp);
 }
 
+// Reflux from the flux register (StageArgs::rf_slot): the stage kernel
+// stored the doubled (kt2) flux of every coarse-fine face, both sides, while
+// sweeping; here one 64-thread CTA per coarse leaf applies, face by face in
+// order (an edge cell corrected through two faces keeps the oracle's order),
+//   avg2 = 0.25 ((K1 + K2) + (K3 + K4)),  corr = 0.5 (side ? Kc - avg2 : avg2 - Kc),
+// which is bitwise the recomputing kernel's corr (every flux there is 0.5 K,
+// and scaling by 2 commutes with the roundings).
+__global__ void __launch_bounds__(N * N) amr_reflux_reg_kernel(double* Uout, int nf, const int* level,
+                                                              int max_level, double dx, const AmrReflux* rf,
+                                                              const int* rf_slot, const double* rf_flux, int stage,
+                                                              const double* dt_ptr, unsigned long long* stamp) {
+    stamp_begin(stamp);
+    const AmrReflux& r = rf[blockIdx.x];
+    const int g = r.coarse;
+    const double w = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
+    const double dtdx = *dt_ptr / ldexp(dx, max_level - level[g]);
+    const int cell = threadIdx.x, a = cell & 7, b = cell >> 3;
+    for (int face = 0; face < 6; ++face) {
+        if (r.fine[face][0] < 0) continue;
+        const int axis = face >> 1, side = face & 1;
+        const double* Kc = rf_flux + (size_t)rf_slot[6 * g + face] * nf * NC / N;
+        const int fl = r.fine[face][(a >> 2) + 2 * (b >> 2)];
+        const double* Kf = rf_flux + (size_t)rf_slot[6 * fl + (face ^ 1)] * nf * NC / N;
+        const int c0 = 2 * (a & 3) + 8 * (2 * (b & 3));  // fine face cell of quadrant q: c0 + (q & 1) + 8 (q >> 1)
+        const int ic = side ? N - 1 : 0;
+        const int c = axis == 0 ? cidx(ic, a, b) : (axis == 1 ? cidx(a, ic, b) : cidx(a, b, ic));
+        for (int f = 0; f < nf; ++f) {
+            const double* kf = Kf + f * N * N + c0;
+            const double avg2 = 0.25 * ((kf[0] + kf[1]) + (kf[N] + kf[N + 1]));
+            const double kc = Kc[f * N * N + cell];
+            const double corr = 0.5 * (side ? kc - avg2 : avg2 - kc);
+            double* u = Uout + ((size_t)g * nf + f) * NC + c;
+            *u = *u + w * (dtdx * corr);
+        }
+        __syncthreads();
+    }
+    stamp_end(stamp);
+}
+
 }  // namespace
+
+cudaError_t launch_amr_reflux_reg(double* Uout, int nf, const int* level, int max_level, double dx,
+                                  const AmrReflux* rf, long long n, const int* rf_slot, const double* rf_flux,
+                                  int stage, const double* dt, unsigned long long* stamp, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    amr_reflux_reg_kernel<<<(unsigned)n, N * N, 0, s>>>(Uout, nf, level, max_level, dx, rf, rf_slot, rf_flux, stage,
+                                                          dt, stamp);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_amr_fill(double* U, int nf, const AmrProxy* px, const unsigned char* face_mask, long long n,
                             unsigned long long* stamp, cudaStream_t s) {

@@ -155,6 +155,14 @@ struct StageArgs {
     // AMR, all levels in one launch: sub-grid g (level-major) is updated
     // with lvl_dx[L] for the last L < lvl_n with g >= lvl_first[L]
     // (lvl_n = 0: dx_upd for every CTA)
+    // AMR flux register: for a leaf face that is a coarse-fine face (either
+    // side), rf_slot[6 g + face] >= 0 names a slot of rf_flux where the sweep
+    // stores that face's (doubled, kt2) flux of every field and face cell
+    // ([slot][nf][64], cell a + 8 b in the sweep's transverse axes); the
+    // reflux kernel then corrects the coarse cells from the stored fluxes
+    // instead of reconstructing them again (nullptr: no register)
+    const int* rf_slot;
+    double* rf_flux;
     static constexpr int kMaxLevels = 8;
     int lvl_n;
     int lvl_first[kMaxLevels];
@@ -224,6 +232,10 @@ struct P2PArgs {
 };
 int p2p_stencil_host(int radius, int* off3, double* coef4, int cap);
 cudaError_t launch_p2p(const P2PArgs& a, int n_ctas, cudaStream_t s);
+// Reflux from the stage kernel's flux register (StageArgs::rf_slot / rf_flux).
+cudaError_t launch_amr_reflux_reg(double* Uout, int nf, const int* level, int max_level, double dx,
+                                  const AmrReflux* rf, long long n, const int* rf_slot, const double* rf_flux,
+                                  int stage, const double* dt, unsigned long long* stamp, cudaStream_t s);
 cudaError_t launch_selftest_math(unsigned long long n, unsigned long long seed, int emax, unsigned long long* bad,
                                  int sms, cudaStream_t s);
 

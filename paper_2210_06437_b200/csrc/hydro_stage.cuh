@@ -375,7 +375,18 @@ struct StageCtx {
     size_t own;                  // element offset of the sub-grid's field 0
     double dtdx;                 // 0.5 dt/dx: fluxes are carried doubled (kt2)
     EosParams e;
+    // AMR flux register (StageArgs::rf_slot): where this sweep's first / last
+    // face fluxes go when that face is a coarse-fine face, else nullptr;
+    // rf_cell = the pencil's face cell a + 8 b
+    double* rf_lo;
+    double* rf_hi;
+    int rf_cell;
 };
+
+// Store the (doubled) face flux of field f of this pencil into a flux register slot.
+__device__ __forceinline__ void rf_store(double* slot, int f, int cell, double F) {
+    if (slot != nullptr) slot[f * (N * N) + cell] = F;
+}
 
 // Retire the flux difference d of cell offset `o`, field f (uprev = U^(k-1)
 // of that cell, un = its U^n).
@@ -495,6 +506,10 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             c.cache[(0 * 3 + 1) * kPencils + t] = vR;
             c.cache[(0 * 3 + 2) * kPencils + t] = a;
         }
+        if (c.rf_lo != nullptr) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) rf_store(c.rf_lo, fm[k], c.rf_cell, Fp[k]);
+        }
     }
 #pragma unroll FaceUnroll<RECON>::value
     for (int j = 1; j < kFaces; ++j) {
@@ -523,6 +538,10 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             c.cache[(j * 3 + 0) * kPencils + t] = vL;
             c.cache[(j * 3 + 1) * kPencils + t] = vR;
             c.cache[(j * 3 + 2) * kPencils + t] = a;
+        }
+        if (j == kFaces - 1 && c.rf_hi != nullptr) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) rf_store(c.rf_hi, fm[k], c.rf_cell, F[k]);
         }
         const int o = p.base + (j - 1) * p.ss;
         double out[kFA];
@@ -557,6 +576,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt2(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
+                rf_store(c.rf_lo, f, c.rf_cell, Fq);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -567,6 +587,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
                 const double a = c.cache[(j * 3 + 2) * kPencils + t];
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
+                if (j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -643,6 +664,14 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
         F[0] = kt2(a, uL[0], uR[0], fL0, fR0);
         F[1] = kt2(a, uL[1], uR[1], fL1, fR1);
         F[2] = kt2(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
+        if (j == 0 && c.rf_lo != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) rf_store(c.rf_lo, fmo[k], c.rf_cell, F[k]);
+        }
+        if (j == kFaces - 1 && c.rf_hi != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) rf_store(c.rf_hi, fmo[k], c.rf_cell, F[k]);
+        }
         if (NF > kFA && role == 0) {
             c.cache[(j * 3 + 0) * kPencils + pen] = vL;
             c.cache[(j * 3 + 1) * kPencils + pen] = vR;
@@ -690,6 +719,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt2(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
+                rf_store(c.rf_lo, f, c.rf_cell, Fq);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -700,6 +730,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
                 const double a = c.cache[(j * 3 + 2) * kPencils + pen];
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
+                if (j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -1054,6 +1085,13 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         const int nlo = __ldg(A.nbr + 6 * g + 2 * axis);
         const int nhi = __ldg(A.nbr + 6 * g + 2 * axis + 1);
 #endif
+        c.rf_lo = c.rf_hi = nullptr;
+        c.rf_cell = a + N * b;
+        if (A.rf_slot != nullptr) {
+            const int sl = __ldg(A.rf_slot + 6 * g + 2 * axis), sh = __ldg(A.rf_slot + 6 * g + 2 * axis + 1);
+            if (sl >= 0) c.rf_lo = A.rf_flux + (size_t)sl * NF * N * N;
+            if (sh >= 0) c.rf_hi = A.rf_flux + (size_t)sh * NF * N * N;
+        }
         Pencil p;
         p.own = own;
         p.sown = nullptr;

@@ -334,6 +334,9 @@ struct ts_hydro_ctx {
     bool amr_slab_fill = true;             // TS_HYDRO_AMR_FULLFILL=1: fill whole proxies
     tsh::AmrReflux* d_amr_rec = nullptr;
     int32_t* d_amr_level = nullptr;
+    int32_t* d_amr_rf_slot = nullptr;       // [n_leaves][6] flux register slot of a coarse-fine face, -1 = none
+    double* d_amr_rf_flux = nullptr;        // [slots][nf][64] doubled face fluxes stored by the stage kernel
+    bool amr_reflux_reg = true;             // TS_HYDRO_AMR_REFLUX=recompute: reflux reconstructs the fluxes again
 
     // Per-sub-grid drop-in steps (ts_hydro_launch_stage ... ts_hydro_finish_step).
     // Launches are ISSUED in dependency order — a stage-k launch is parked on
@@ -516,6 +519,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_amr_pmask);
     dfree(c, &c->d_amr_rec);
     dfree(c, &c->d_amr_level);
+    dfree(c, &c->d_amr_rf_slot);
+    dfree(c, &c->d_amr_rf_flux);
     c->amr = false;
     c->amr_mr = false;
     c->xfer_cells = kSlab;
@@ -1001,6 +1006,10 @@ int do_step_amr(ts_hydro_ctx* c) {
                                             c->amr_slab_fill ? c->d_amr_pmask : nullptr, c->amr_n_proxy,
                                             stamp, s));
         }
+        if (c->d_amr_rf_slot != nullptr) {
+            a.rf_slot = c->d_amr_rf_slot;
+            a.rf_flux = c->d_amr_rf_flux;
+        }
         if (c->amr_fused && c->amr_max_level < tsh::StageArgs::kMaxLevels) {
             tsh::StageArgs b = a;
             b.lvl_n = c->amr_max_level + 1;
@@ -1034,9 +1043,14 @@ int do_step_amr(ts_hydro_ctx* c) {
         if (c->amr_n_rec > 0) {
             rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrReflux, 0, 0, &stamp);
             if (rc) return rc;
-            TS_CUDA(c, tsh::launch_amr_reflux(a.Uprev, a.Uout, c->nf, c->cfg.recon, c->cfg.gamma, c->cfg.p_floor,
-                                              c->d_nbr, c->d_amr_level, c->amr_max_level, c->cfg.dx, c->d_amr_rec,
-                                              c->amr_n_rec, stage, dt_ptr, stamp, s));
+            if (c->d_amr_rf_slot != nullptr)
+                TS_CUDA(c, tsh::launch_amr_reflux_reg(a.Uout, c->nf, c->d_amr_level, c->amr_max_level, c->cfg.dx,
+                                                      c->d_amr_rec, c->amr_n_rec, c->d_amr_rf_slot, c->d_amr_rf_flux,
+                                                      stage, dt_ptr, stamp, s));
+            else
+                TS_CUDA(c, tsh::launch_amr_reflux(a.Uprev, a.Uout, c->nf, c->cfg.recon, c->cfg.gamma, c->cfg.p_floor,
+                                                  c->d_nbr, c->d_amr_level, c->amr_max_level, c->cfg.dx, c->d_amr_rec,
+                                                  c->amr_n_rec, stage, dt_ptr, stamp, s));
         }
     }
     double* slot = amax_slot(c, c->steps_done + 1);
@@ -1486,6 +1500,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_SCR_RING")) c->scr_ring = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_AMR_REFLUX")) c->amr_reflux_reg = std::strcmp(w, "recompute") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_FULLFILL")) c->amr_slab_fill = std::strcmp(w, "1") != 0;
     if (const char* w = std::getenv("TS_HYDRO_XFER_CHUNKS"))
@@ -2041,6 +2056,25 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
         if (nr > 0)
             TS_CUDA(c, cudaMemcpy(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
         TS_CUDA(c, cudaMemcpy(c->d_amr_level, level, (size_t)nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (nr > 0 && c->amr_reflux_reg) {
+            // flux register: one slot per coarse-fine face side (the coarse
+            // leaf's face, and the facing face of each of its 4 fine leaves)
+            std::vector<int32_t> slot((size_t)nl * 6, -1);
+            int32_t ns = 0;
+            for (int64_t k = 0; k < nr; ++k)
+                for (int f = 0; f < 6; ++f) {
+                    if (rf[k].fine[f][0] < 0) continue;
+                    slot[(size_t)rf[k].coarse * 6 + f] = ns++;
+                    for (int q = 0; q < 4; ++q) {
+                        int32_t& sf = slot[(size_t)rf[k].fine[f][q] * 6 + (f ^ 1)];
+                        if (sf < 0) sf = ns++;
+                    }
+                }
+            rc = dalloc(c, &c->d_amr_rf_slot, slot.size());
+            if (!rc) rc = dalloc(c, &c->d_amr_rf_flux, (size_t)std::max(ns, 1) * c->nf * kN * kN);
+            if (rc) return rc;
+            TS_CUDA(c, cudaMemcpy(c->d_amr_rf_slot, slot.data(), slot.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
     }
     c->amr = true;
     return TS_OK;
