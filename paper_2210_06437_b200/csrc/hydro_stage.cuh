@@ -476,7 +476,7 @@ __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[k
 // Single-lane march, one instantiation per sweep mode (x: init, y:
 // accumulate, z: RK update) so the face loop carries no mode branches; face 0
 // is peeled (it retires nothing) and every prefetch is unconditional.
-template <int NF, int RECON, int STAGE, int MODE>
+template <int NF, int RECON, int STAGE, int MODE, bool RF>
 __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
     const int t = threadIdx.x;
     constexpr bool kUn = STAGE > 1 && MODE == 2;  // U^n needed by the update
@@ -506,7 +506,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             c.cache[(0 * 3 + 1) * kPencils + t] = vR;
             c.cache[(0 * 3 + 2) * kPencils + t] = a;
         }
-        if (c.rf_lo != nullptr) {
+        if (RF && c.rf_lo != nullptr) {
 #pragma unroll
             for (int k = 0; k < kFA; ++k) rf_store(c.rf_lo, fm[k], c.rf_cell, Fp[k]);
         }
@@ -539,7 +539,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             c.cache[(j * 3 + 1) * kPencils + t] = vR;
             c.cache[(j * 3 + 2) * kPencils + t] = a;
         }
-        if (j == kFaces - 1 && c.rf_hi != nullptr) {
+        if (RF && j == kFaces - 1 && c.rf_hi != nullptr) {
 #pragma unroll
             for (int k = 0; k < kFA; ++k) rf_store(c.rf_hi, fm[k], c.rf_cell, F[k]);
         }
@@ -576,7 +576,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt2(c.cache[2 * kPencils + t], uL, uR, uL * c.cache[t], uR * c.cache[kPencils + t]);
-                rf_store(c.rf_lo, f, c.rf_cell, Fq);
+                if (RF) rf_store(c.rf_lo, f, c.rf_cell, Fq);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -587,7 +587,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 const double vR = c.cache[(j * 3 + 1) * kPencils + t];
                 const double a = c.cache[(j * 3 + 2) * kPencils + t];
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
-                if (j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
+                if (RF && j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -606,7 +606,7 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 // arithmetic, operation by operation, as the single-lane march (bitwise).
 __device__ __forceinline__ double xlane(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
 
-template <int NF, int RECON, int STAGE, int MODE>
+template <int NF, int RECON, int STAGE, int MODE, bool RF>
 __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
     const int role = threadIdx.x & 1;
     const int pen = threadIdx.x >> 1;
@@ -664,11 +664,11 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
         F[0] = kt2(a, uL[0], uR[0], fL0, fR0);
         F[1] = kt2(a, uL[1], uR[1], fL1, fR1);
         F[2] = kt2(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
-        if (j == 0 && c.rf_lo != nullptr) {
+        if (RF && j == 0 && c.rf_lo != nullptr) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) rf_store(c.rf_lo, fmo[k], c.rf_cell, F[k]);
         }
-        if (j == kFaces - 1 && c.rf_hi != nullptr) {
+        if (RF && j == kFaces - 1 && c.rf_hi != nullptr) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) rf_store(c.rf_hi, fmo[k], c.rf_cell, F[k]);
         }
@@ -719,7 +719,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 double uL, uR;
                 recon_step<RECON>(next_addr<RECON>(p, 0), fof, q, uL, uR);
                 Fq = kt2(c.cache[2 * kPencils + pen], uL, uR, uL * c.cache[pen], uR * c.cache[kPencils + pen]);
-                rf_store(c.rf_lo, f, c.rf_cell, Fq);
+                if (RF) rf_store(c.rf_lo, f, c.rf_cell, Fq);
             }
 #pragma unroll
             for (int j = 1; j < kFaces; ++j) {
@@ -730,7 +730,7 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
                 const double vR = c.cache[(j * 3 + 1) * kPencils + pen];
                 const double a = c.cache[(j * 3 + 2) * kPencils + pen];
                 const double F = kt2(a, uL, uR, uL * vL, uR * vR);
-                if (j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
+                if (RF && j == kFaces - 1) rf_store(c.rf_hi, f, c.rf_cell, F);
                 retire_species<MODE, STAGE>(c, f, p.base + (j - 1) * p.ss, Fq - F, MODE > 0 ? acc[j - 1] : 0.0, upf,
                                             unf);
                 if (kUn) unf = ld_un(un_row + (j < N ? j : N - 1) * p.ss + fof);
@@ -919,7 +919,10 @@ constexpr size_t stage_smem_bytes() {
     return (size_t)StageSmem<NF>::doubles * sizeof(double) + (TS_TMA ? 1024 + 16 : 0);
 }
 
-template <int NF, int RECON, int STAGE>
+// RF: an AMR launch with a flux register (StageArgs::rf_slot); a separate
+// instantiation so the uniform kernels carry none of its state (measured: the
+// register-pressed nf 11 kernel lost 4.5 % with it).
+template <int NF, int RECON, int STAGE, bool RF>
 __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(const __grid_constant__ StageArgs A) {
     extern __shared__ __align__(16) double smem_raw[];
 #if TS_TMA
@@ -1087,7 +1090,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
 #endif
         c.rf_lo = c.rf_hi = nullptr;
         c.rf_cell = a + N * b;
-        if (A.rf_slot != nullptr) {
+        if (RF && A.rf_slot != nullptr) {
             const int sl = __ldg(A.rf_slot + 6 * g + 2 * axis), sh = __ldg(A.rf_slot + 6 * g + 2 * axis + 1);
             if (sl >= 0) c.rf_lo = A.rf_flux + (size_t)sl * NF * N * N;
             if (sh >= 0) c.rf_hi = A.rf_flux + (size_t)sh * NF * N * N;
@@ -1130,17 +1133,17 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         }
         if (Lanes<NF>::pair) {
             if (axis == 0)
-                sweep_pair<NF, RECON, STAGE, 0>(c, p, fm, amax);
+                sweep_pair<NF, RECON, STAGE, 0, RF>(c, p, fm, amax);
             else if (axis == 1)
-                sweep_pair<NF, RECON, STAGE, 1>(c, p, fm, amax);
+                sweep_pair<NF, RECON, STAGE, 1, RF>(c, p, fm, amax);
             else
-                sweep_pair<NF, RECON, STAGE, 2>(c, p, fm, amax);
+                sweep_pair<NF, RECON, STAGE, 2, RF>(c, p, fm, amax);
         } else if (axis == 0)
-            sweep<NF, RECON, STAGE, 0>(c, p, fm, amax);
+            sweep<NF, RECON, STAGE, 0, RF>(c, p, fm, amax);
         else if (axis == 1)
-            sweep<NF, RECON, STAGE, 1>(c, p, fm, amax);
+            sweep<NF, RECON, STAGE, 1, RF>(c, p, fm, amax);
         else
-            sweep<NF, RECON, STAGE, 2>(c, p, fm, amax);
+            sweep<NF, RECON, STAGE, 2, RF>(c, p, fm, amax);
         if (axis < 2) __syncthreads();
     }
 #if TS_CHECK
@@ -1244,8 +1247,8 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     }
 }
 
-template <int NF, int RECON, int STAGE>
-inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
+template <int NF, int RECON, int STAGE, bool RF>
+inline cudaError_t launch_stage_rf(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
     const size_t smem = stage_smem_bytes<NF>();
     // the dynamic shared-memory limit is a per-device function attribute:
     // set it once on every device this instantiation is launched on
@@ -1255,13 +1258,13 @@ inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s
     if (e != cudaSuccess) return e;
     const unsigned long long bit = 1ull << (dev & 63);
     if ((configured.load(std::memory_order_acquire) & bit) == 0ull) {
-        e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     if (!pdl) {
-        stage_kernel<NF, RECON, STAGE><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);
+        stage_kernel<NF, RECON, STAGE, RF><<<n_ctas, Lanes<NF>::threads, smem, s>>>(a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -1274,7 +1277,13 @@ inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, stage_kernel<NF, RECON, STAGE>, a);
+    return cudaLaunchKernelEx(&cfg, stage_kernel<NF, RECON, STAGE, RF>, a);
+}
+
+template <int NF, int RECON, int STAGE>
+inline cudaError_t launch_stage_t(const StageArgs& a, int n_ctas, cudaStream_t s, bool pdl) {
+    return a.rf_slot != nullptr ? launch_stage_rf<NF, RECON, STAGE, true>(a, n_ctas, s, pdl)
+                                : launch_stage_rf<NF, RECON, STAGE, false>(a, n_ctas, s, pdl);
 }
 
 template <int NF, int RECON>
