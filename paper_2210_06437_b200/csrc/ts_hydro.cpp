@@ -213,7 +213,7 @@ struct ts_hydro_ctx {
     // ts_hydro_step_host_async: chunked copies on their own streams; the
     // previous call's host_out and its per-chunk D2H completion events
     static constexpr int kXferChunksMax = 64;
-    int xfer_chunks = 8;  // TS_HYDRO_XFER_CHUNKS
+    int xfer_chunks = 24;  // TS_HYDRO_XFER_CHUNKS (wavefront e2e, same box: 8 -> 0.82-0.83, 24 -> 0.84-0.87 G)
     bool chunk_overlap = true;  // TS_HYDRO_CHUNK_OVERLAP=0: D2H waits for the whole last stage
     bool amr_fused = true;      // TS_HYDRO_AMR_SPLIT=1: one stage launch per AMR level
     cudaEvent_t ev_d2h[kXferChunksMax] = {};
@@ -228,6 +228,13 @@ struct ts_hydro_ctx {
     uint32_t* d_h2d_flag = nullptr;           // [kXferChunksMax] landed-chunk flags
     uint32_t h2d_seq = 0;
     bool h2d_arm = false;                     // the next stage 1 acquires the chunk flags of h2d_seq
+    // chained pipelined host steps, wavefront form (TS_HYDRO_E2E_WAVE=0: off):
+    // per chunk H2D -> stage 1 -> 2 -> 3 -> D2H launches on the chunk's own
+    // stream, each waiting (events) only for the chunks its halo reaches
+    bool e2e_wave = true;
+    bool wave_ready = false;                  // events + dependency lists built for the bound mesh
+    cudaEvent_t ev_wave[4][kXferChunksMax] = {};  // [h2d, s1, s2, s3][chunk]
+    std::vector<std::vector<int>> wave_dep;   // chunk -> chunks its sub-grids' face neighbours live in
 
     // mesh
     bool have_mesh = false;
@@ -521,6 +528,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_amr_level);
     dfree(c, &c->d_amr_rf_slot);
     dfree(c, &c->d_amr_rf_flux);
+    c->wave_ready = false;
     c->amr = false;
     c->amr_mr = false;
     c->xfer_cells = kSlab;
@@ -1499,6 +1507,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_E2E_WAVE")) c->e2e_wave = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_SCR_RING")) c->scr_ring = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_REFLUX")) c->amr_reflux_reg = std::strcmp(w, "recompute") != 0;
     if (const char* w = std::getenv("TS_HYDRO_AMR_SPLIT")) c->amr_fused = std::strcmp(w, "1") != 0;
@@ -1601,6 +1610,9 @@ int ts_hydro_destroy(ts_hydro_ctx* ctx) {
         if (ctx->h_clock) cudaFreeHost(ctx->h_clock);
         if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
         if (ctx->ev_cal) cudaEventDestroy(ctx->ev_cal);
+        for (auto& row : ctx->ev_wave)
+            for (cudaEvent_t e : row)
+                if (e) cudaEventDestroy(e);
         if (ctx->ev_din) cudaEventDestroy(ctx->ev_din);
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         for (const PendingLaunch& p : ctx->pending) {
@@ -2467,6 +2479,124 @@ int ts_hydro_step_host(ts_hydro_ctx* c, const double* host_in, double* host_out,
 // previous call's D2H of chunk i (or of everything when the call is not
 // chained: that D2H still reads U^n) and for the compute stream's earlier work; the steps wait for
 // the whole H2D (dt needs every sub-grid); the D2H waits for the steps.
+namespace {
+// One chained pipelined step as a wavefront over the transfer chunks: chunk i
+// of the H2D, of each stage and of the D2H is its own operation; stage k of
+// chunk i waits (CUDA events, no spinning) for stage k-1 of the chunks its
+// sub-grids' face neighbours live in, stage 1 additionally for the H2D of
+// those chunks and for every stage-3 chunk of the previous step (its dt), the
+// D2H of chunk i for stage 3 of chunk i.  So the H2D of the next step's chunk
+// i (behind this step's D2H of chunk i) overlaps this step's D2H of later
+// chunks and the two PCIe directions stay busy together.  Hazards: stage k
+// overwrites a buffer only after its readers (stage k+1 of the previous step,
+// stage 1 of the halo chunks for U^n) — all behind the previous step's
+// stage-3 events or this step's neighbour events.
+int step_host_wave(ts_hydro_ctx* c, const double* host_in, double* host_out, ts_done_fn done, void* user) {
+    const int C = c->xfer_chunks;
+    const int64_t n = c->n_owned;
+    const size_t per = (size_t)c->nf * kNC * sizeof(double);
+    auto g0 = [&](int i) { return (n * i + C - 1) / C; };
+    if (!c->wave_ready) {
+        for (auto& row : c->ev_wave)
+            for (int i = 0; i < C; ++i)
+                if (row[i] == nullptr) TS_CUDA(c, cudaEventCreateWithFlags(&row[i], cudaEventDisableTiming));
+        c->wave_dep.assign((size_t)C, {});
+        for (int i = 0; i < C; ++i) {
+            std::vector<char> d((size_t)C, 0);
+            d[(size_t)i] = 1;
+            for (int64_t g = g0(i); g < g0(i + 1); ++g)
+                for (int f = 0; f < 6; ++f) {
+                    const int32_t h = c->nbr_local[(size_t)g * 6 + f];
+                    if (h >= 0 && h < n) d[(size_t)((h * C) / n)] = 1;
+                }
+            for (int j = 0; j < C; ++j)
+                if (d[(size_t)j]) c->wave_dep[(size_t)i].push_back(j);
+        }
+        c->wave_ready = true;
+    }
+    cudaStream_t s0, sh, sd;
+    int rc = ensure_stream(c, 0, &s0);
+    if (!rc) rc = ensure_stream(c, 3, &sh);
+    if (!rc) rc = ensure_stream(c, 4, &sd);
+    if (rc) return rc;
+    std::vector<cudaStream_t> cs((size_t)C);
+    for (int i = 0; i < C; ++i) {
+        rc = ensure_stream(c, 5 + (uint32_t)i, &cs[(size_t)i]);
+        if (rc) return rc;
+    }
+    // earlier stream-0 work (a previous non-wavefront step), every stage-3
+    // chunk of the previous step (this step's dt) and the zeroed max slot:
+    // one event the stage-1 launches wait on
+    for (int j = 0; j < C; ++j) TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_wave[3][j], 0));
+    TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 1), 0, sizeof(double), s0));
+    TS_CUDA(c, cudaEventRecord(c->ev_in, s0));
+    // H2D by chunk, each behind the previous step's D2H of that chunk
+    PendingLaunch* rec = nullptr;
+    rc = begin_event_record(c, TS_ACTIVITY_COPY_H2D, kNameH2D, 3, (size_t)n * per, &rec);
+    if (rc) return rc;
+    cudaEvent_t h2d_e1 = rec != nullptr ? rec->e1 : nullptr;
+    if (rec != nullptr) TS_CUDA(c, cudaEventRecord(rec->e0, sh));
+    const char* in_b = reinterpret_cast<const char*>(host_in);
+    for (int i = 0; i < C; ++i) {
+        TS_CUDA(c, cudaStreamWaitEvent(sh, c->ev_d2h[i], 0));
+        const size_t off = (size_t)g0(i) * per, len = (size_t)(g0(i + 1) - g0(i)) * per;
+        if (len > 0)
+            TS_CUDA(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->U[0]) + off, in_b + off, len, cudaMemcpyHostToDevice,
+                                       sh));
+        TS_CUDA(c, cudaEventRecord(c->ev_wave[0][i], sh));
+    }
+    if (h2d_e1 != nullptr) TS_CUDA(c, cudaEventRecord(h2d_e1, sh));
+    // the three stages by chunk; one activity record per stage
+    for (int stage = 1; stage <= 3; ++stage) {
+        unsigned long long* stamp = nullptr;
+        rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], 5, 0, &stamp);
+        if (rc) return rc;
+        c->launches += (uint64_t)C - 1;
+        for (int i = 0; i < C; ++i) {
+            cudaStream_t st = cs[(size_t)i];
+            if (stage == 1) TS_CUDA(c, cudaStreamWaitEvent(st, c->ev_in, 0));
+            for (int j : c->wave_dep[(size_t)i]) TS_CUDA(c, cudaStreamWaitEvent(st, c->ev_wave[stage - 1][j], 0));
+            tsh::StageArgs a = stage_args(c, stage);
+            a.stamp = stamp;
+            a.first = (int)g0(i);
+            if (stage == 1) a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+            const int cnt = (int)(g0(i + 1) - g0(i));
+            if (cnt > 0) TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, cnt, st, false));
+        }
+        // record after all of this stage's launches: a chunk's next stage waits
+        // for this stage of its neighbours, recorded above in host order
+        for (int i = 0; i < C; ++i) TS_CUDA(c, cudaEventRecord(c->ev_wave[stage][i], cs[(size_t)i]));
+    }
+    // D2H by chunk, each behind stage 3 of its chunk
+    rc = begin_event_record(c, TS_ACTIVITY_COPY_D2H, kNameD2H, 4, (size_t)n * per, &rec);
+    if (rc) return rc;
+    cudaEvent_t d2h_e1 = rec != nullptr ? rec->e1 : nullptr;
+    if (rec != nullptr) TS_CUDA(c, cudaEventRecord(rec->e0, sd));
+    char* out_b = reinterpret_cast<char*>(host_out);
+    for (int i = 0; i < C; ++i) {
+        TS_CUDA(c, cudaStreamWaitEvent(sd, c->ev_wave[3][i], 0));
+        const size_t off = (size_t)g0(i) * per, len = (size_t)(g0(i + 1) - g0(i)) * per;
+        if (len > 0)
+            TS_CUDA(c, cudaMemcpyAsync(out_b + off, reinterpret_cast<const char*>(c->U[0]) + off, len,
+                                       cudaMemcpyDeviceToHost, sd));
+        TS_CUDA(c, cudaEventRecord(c->ev_d2h[i], sd));
+    }
+    if (d2h_e1 != nullptr) TS_CUDA(c, cudaEventRecord(d2h_e1, sd));
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(sd, done_host, new DoneThunk{done, user, nullptr}));
+    // later stream-0 work (downloads, batched steps) follows the whole step
+    for (int i = 0; i < C; ++i) {
+        TS_CUDA(c, cudaEventRecord(c->ev_in, cs[(size_t)i]));
+        TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
+    }
+    c->prev_out = host_out;
+    c->prev_out_bytes = (size_t)n * per;
+    c->steps_done++;
+    c->dt_valid = true;
+    c->amax_src = nullptr;
+    return TS_OK;
+}
+}  // namespace
+
 int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* host_out, uint64_t nsteps,
                              ts_done_fn done, void* user) {
     int rc = check_state(c);
@@ -2499,6 +2629,9 @@ int ts_hydro_step_host_async(ts_hydro_ctx* c, const double* host_in, double* hos
     };
     const char* in_b = reinterpret_cast<const char*>(host_in);
     const bool chained = c->prev_out == host_in && c->prev_out_bytes == bytes;
+    if (chained && c->e2e_wave && c->dt_valid && c->world == 1 && nsteps == 1 &&
+        c->cfg.stream_count >= (uint32_t)(5 + C))
+        return step_host_wave(c, host_in, host_out, done, user);
     // Chained on one rank: dt is the previous call's stage-3 signal speed (its
     // input is this call's input) and stage 1 starts under the H2D, each CTA
     // once the chunks of its sub-grid and neighbours landed.
