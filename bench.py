@@ -359,10 +359,12 @@ def main(argv=None):
         value_e2e = e2e_run(dev.step_host_async)
         e2e = {"value": value_e2e, "unit": unit, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": k_e2e,
-               "path": "ts_hydro_step_host_async: every step pinned host U^n -> H2D (8 chunks, each behind the "
-                       "previous step's D2H of that chunk; stage 1 starts per landed chunk, dt from the previous "
-                       "step) -> 1 step -> D2H (8 chunks, each behind its stage-3 count); step k+1's input is "
-                       "step k's output",
+               "path": "ts_hydro_step_host_async, chained: every step pinned host U^n -> H2D (24 chunks, each "
+                       "behind the previous step's D2H of that chunk) -> stages 1..3 as a wavefront over the chunks "
+                       "(event dependencies on the halo chunks; dt from the previous step) -> D2H (each chunk behind "
+                       "its stage 3); step k+1's input is step k's output",
+               "pcie_ceiling": "both PCIe directions at once move ~49 GB/s each on these boxes: 2 x 100 MB per "
+                               "step caps e2e near 0.98 G cell-updates/s (tools/pcie_probe.py)",
                "sync_value": sync_value,
                "sync_path": "ts_hydro_step_host: H2D -> dt + 1 step -> D2H, one call at a time"}
         dev.host_pinned_free(hin)
