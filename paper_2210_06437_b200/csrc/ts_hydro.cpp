@@ -3282,7 +3282,6 @@ int ts_hydro_save(ts_hydro_ctx* c, const char* path) {
     int rc = check_state(c);
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
-    if (c->amr) return fail(c, TS_ESTATE, "checkpoints of AMR meshes are not supported");
     if (path == nullptr) return fail(c, TS_EINVAL, "null checkpoint path");
     std::vector<double> st((size_t)c->n_owned * c->nf * kNC);
     rc = ts_hydro_download(c, 0, c->n_owned, st.data());
@@ -3298,7 +3297,6 @@ int ts_hydro_restore(ts_hydro_ctx* c, const char* const* paths, int32_t n_paths)
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if ((rc = mutating(c)) != TS_OK) return rc;
-    if (c->amr) return fail(c, TS_ESTATE, "checkpoints of AMR meshes are not supported");
     if (paths == nullptr || n_paths < 1) return fail(c, TS_EINVAL, "no checkpoint files");
     const size_t per = (size_t)c->nf * kNC;
     std::vector<double> st((size_t)c->n_owned * per);
