@@ -250,14 +250,14 @@ int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned
  * joins the step's streams into the compute stream, no host wait. */
 int ts_hydro_finish_step(ts_hydro_ctx* ctx);
 
-/* ---- gravity (first slice) -------------------------- */
+/* ---- gravity ------------------------------------- */
 /* The near-field monopole P2P behind the reference's `p2p_kernel` launches
  * (gravity_kernel_name workload.cpp:365-372; 6 per sub-grid and step,
  * 565-569): for every cell, phi = -G h^2 sum rho_j / |d| and g = G h sum
  * rho_j d / |d|^3 over the same-level cells at offsets 0 < |d|^2 <= radius^2
  * (radius 1..6 cells, across faces, edges and corners; vacuum outside the
- * mesh) — oracle/hydro_oracle.h orc_gravity_p2p, bitwise.  The multipole,
- * p2m and root parts of the FMM are not built.  owned_index == NULL or
+ * mesh) — oracle/hydro_oracle.h orc_gravity_p2p, bitwise.  (The whole
+ * solve, near and far field, is ts_hydro_gravity_fmm below.)  owned_index == NULL or
  * count <= 0: every owned sub-grid.  Runs after everything on the compute
  * stream; single rank, uniform mesh, not while a per-sub-grid step is open.
  * Activity record name "p2p_kernel". */
@@ -265,6 +265,43 @@ int ts_hydro_gravity_p2p(ts_hydro_ctx* ctx, double G, int32_t radius, const int6
                          uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
 /* [count][4][512] = (phi, gx, gy, gz) of owned sub-grids first..first+count-1 (waits). */
 int ts_hydro_download_gravity(ts_hydro_ctx* ctx, int64_t first, int64_t count, double* host);
+
+/* The whole gravity solve: a cell-based fast multipole method over the octree
+ * of 8^3 sub-grids (oracle/hydro_oracle.h orc_gravity_fmm,
+ * bitwise).  The tree is given by the leaves — exactly the owned sub-grids, in
+ * their storage order: level[k] (0 = the coarsest hydro level, cell width
+ * dx0), pos[k][3] at that level inside dims * 2^level; the refined nodes are
+ * their ancestors up to one root (T = ceil(log2 max dims) virtual levels above
+ * level 0), as in the reference's octree (build_mesh, workload.cpp:264-327).
+ * A uniform mesh passes level 0 and ts_hydro_uniform_mesh's positions; an AMR
+ * mesh its leaves' levels and positions.  Rebinding a mesh drops the tree.
+ * Single rank. */
+int ts_hydro_set_gravity_tree(ts_hydro_ctx* ctx, int64_t n_leaves, const int32_t* level, const int32_t* pos,
+                              const int32_t* dims, double dx0);
+/* One solve of the current state's density on stream `stream_id` (after
+ * everything on the compute stream): monopoles about the centre of mass,
+ * first-order local expansions, interaction radius `radius` (1..3 cells: a
+ * cell interacts directly with the cells within `radius`, and with its
+ * parent's near cells' children beyond it).  Output: ts_hydro_download_gravity.
+ * Activity records, one per launch, named as the reference names the kinds
+ * (workload.hpp:45-48): "fmm_moments_kernel" (leaf masses), per refined depth
+ * "multipole_kernel" ("multipole_root_kernel" at the root: restriction, then
+ * expansions), "p2p_kernel" / "p2m_kernel" (leaves, by kind: see
+ * ts_hydro_gravity_tree). */
+int ts_hydro_gravity_fmm(ts_hydro_ctx* ctx, double G, int32_t radius, uint32_t stream_id, uint64_t correlation_guid,
+                         ts_done_fn done, void* user);
+/* The gravity tree of these leaves (ts_hydro_set_gravity_tree's arguments; no
+ * context, no device): n_nodes always, the arrays when cap >= n_nodes — per
+ * node its level (hydro level: negative above level 0), pos[3] at that level,
+ * kind as the reference's gravity_kernel_name picks it (workload.cpp:365-372:
+ * 0 multipole_root_kernel, 1 multipole_kernel, 2 p2m_kernel, 3 p2p_kernel)
+ * and leaf (its index among the leaves, or -1 for a refined node).  Any
+ * output may be NULL.  Nodes: refined ones by level, then the leaves by
+ * level.  On the reference's own octrees the nodes are its grids.
+ * TS_EINVAL for a malformed tree. */
+int ts_hydro_gravity_tree(int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
+                          int64_t cap, int32_t* level_out, int32_t* pos_out, int32_t* kind, int32_t* leaf,
+                          int64_t* n_nodes);
 
 /* ---- ghost exchange --------------------------------------------------------- */
 /* The reference's 1-deep face exchange of field 0 (workload.cpp:487-542):

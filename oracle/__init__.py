@@ -42,9 +42,9 @@ class Params(ctypes.Structure):
 
 
 def build(force: bool = False) -> None:
-    src = os.path.join(HERE, "hydro_oracle.c")
-    stale = os.path.exists(LIB_PATH) and os.path.exists(src) and max(
-        os.path.getmtime(src), os.path.getmtime(os.path.join(HERE, "hydro_oracle.h"))) > os.path.getmtime(LIB_PATH)
+    srcs = [os.path.join(HERE, f) for f in ("hydro_oracle.c", "fmm_oracle.c", "hydro_oracle.h")]
+    stale = os.path.exists(LIB_PATH) and all(os.path.exists(f) for f in srcs) and max(
+        os.path.getmtime(f) for f in srcs) > os.path.getmtime(LIB_PATH)
     if force or stale or not os.path.exists(LIB_PATH):
         subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
 
@@ -98,6 +98,14 @@ def lib():
         L.orc_p2p_stencil.argtypes = [ctypes.c_int, _i32p, _f64p, ctypes.c_int]
         L.orc_gravity_p2p.argtypes = [ctypes.POINTER(Params), ctypes.c_int64, _i64p, _f64p, ctypes.c_int,
                                       ctypes.c_double, _f64p]
+        L.orc_fmm_table.restype = ctypes.c_int
+        L.orc_fmm_table.argtypes = [ctypes.c_int, ctypes.c_int, _i32p, _i32p, ctypes.c_int]
+        for fn in (L.orc_gravity_fmm, L.orc_gravity_direct):
+            fn.restype = ctypes.c_int
+        L.orc_gravity_fmm.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_double, _f64p,
+                                      ctypes.c_int, ctypes.c_double, _f64p]
+        L.orc_gravity_direct.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_double, _f64p,
+                                         ctypes.c_double, _f64p]
         L.orc_amr_fill.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _f64p]
         L.orc_amr_reflux.argtypes = [ctypes.POINTER(Params), _i64p, _i32p, ctypes.c_int, ctypes.c_int64, _i32p,
                                      _f64p, _f64p, ctypes.c_int, ctypes.c_double]
@@ -123,6 +131,8 @@ def ref():
         R.ref_cell_value.argtypes = [ctypes.c_uint64] * 3
         R.ref_face_cell_index.restype = ctypes.c_uint64
         R.ref_face_cell_index.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
+        R.ref_gravity_kinds.restype = ctypes.c_int64
+        R.ref_gravity_kinds.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i32p, ctypes.c_int64]
         R.ref_build_mesh.restype = ctypes.c_int64
         R.ref_build_mesh.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _i32p, _i32p, _i32p,
                                      _i64p, ctypes.c_int64]
@@ -205,6 +215,44 @@ def gravity_p2p(p: Params, nbr, U, radius=4, G=1.0):
     U = np.ascontiguousarray(U, np.float64)
     out = np.zeros((U.shape[0], 4, NC), np.float64)
     lib().orc_gravity_p2p(ctypes.byref(p), U.shape[0], _p(nbr, _i64p), _p(U, _f64p), radius, G, _p(out, _f64p))
+    return out
+
+
+def fmm_table(radius, root=False):
+    """FMM interaction table (octant-0 orientation): offsets [n][3] and near flags [n]."""
+    u = np.zeros((4096, 3), np.int32)
+    near = np.zeros(4096, np.int32)
+    n = lib().orc_fmm_table(radius, int(root), _p(u, _i32p), _p(near, _i32p), 4096)
+    if n < 0:
+        raise ValueError("radius outside 1..3")
+    return u[:n], near[:n].astype(bool)
+
+
+def _leaves(level, pos, dims):
+    level = np.ascontiguousarray(level, np.int32)
+    pos = np.ascontiguousarray(np.asarray(pos).reshape(-1, 3), np.int32)
+    dims = np.ascontiguousarray(dims, np.int32)
+    return level, pos, dims
+
+
+def gravity_fmm(nf, level, pos, dims, dx0, U, radius=2, G=1.0):
+    """Whole gravity solve (FMM, fmm_oracle.c): [n][4][512] = (phi, gx, gy, gz) per leaf."""
+    level, pos, dims = _leaves(level, pos, dims)
+    U = np.ascontiguousarray(U, np.float64)
+    out = np.zeros((len(level), 4, NC), np.float64)
+    if lib().orc_gravity_fmm(nf, len(level), _p(level, _i32p), _p(pos, _i32p), _p(dims, _i32p), dx0,
+                             _p(U, _f64p), radius, G, _p(out, _f64p)) != 0:
+        raise ValueError("malformed gravity tree (overlapping leaves or positions outside the domain)")
+    return out
+
+
+def gravity_direct(nf, level, pos, dims, dx0, U, G=1.0):
+    """Brute-force pair sum over every leaf cell (the FMM's accuracy yardstick)."""
+    level, pos, dims = _leaves(level, pos, dims)
+    U = np.ascontiguousarray(U, np.float64)
+    out = np.zeros((len(level), 4, NC), np.float64)
+    lib().orc_gravity_direct(nf, len(level), _p(level, _i32p), _p(pos, _i32p), _p(dims, _i32p), dx0,
+                             _p(U, _f64p), G, _p(out, _f64p))
     return out
 
 

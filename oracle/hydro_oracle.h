@@ -142,6 +142,27 @@ int orc_p2p_stencil(int radius, int32_t* off, double* coef, int cap);
 void orc_gravity_p2p(const orc_params* p, int64_t ngrids, const int64_t* nbr, const double* U, int radius, double G,
                      double* out);
 
+/* --- gravity, the whole solve: a cell-based FMM over the octree of 8^3
+ * sub-grids (fmm_oracle.c; the reference's
+ * multipole_root / multipole / p2m / p2p launches, workload.cpp:365-372).
+ * Leaves k = 0..n-1: level[k] >= 0 (0 = the coarsest hydro level, whose cell
+ * width is dx0), pos[k][3] at that level, inside dims * 2^level; U = the
+ * leaves' states (nf fields, density = field 0).  Tree: T = ceil(log2
+ * max(dims)) virtual depths above level 0 (depth = level + T, h_d = dx0 2^(T-d)),
+ * nodes = leaves + every ancestor.  Contract in full: DESIGN.md §15.
+ * out[k][4][512] = (phi, gx, gy, gz); returns -1 on a malformed tree. */
+#define ORC_FMM_RMAX 3
+/* Interaction table (octant-0 orientation, (z, y, x) lexicographic over
+ * [-K, K]^3 without 0): depth >= 1 (root = 0): K = 2R+1, parent offset
+ * (u >> 1) within R; depth 0 (root = 1): K = 7, all.  near[k] = |u|^2 <= R^2. */
+int orc_fmm_table(int radius, int root, int32_t* u, int32_t* near, int cap);
+int orc_gravity_fmm(int nf, int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
+                    double dx0, const double* U, int radius, double G, double* out);
+/* Brute force over every pair of leaf cells (monopoles at the centres): the
+ * accuracy yardstick of the FMM, not a parity target. */
+int orc_gravity_direct(int nf, int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
+                       double dx0, const double* U, double G, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,23 @@ std::int64_t ref_build_mesh(int levels, int world, std::uint64_t seed, std::int3
     }
 }
 
+// gravity_kernel_name (workload.cpp:365-372) of every grid of build_mesh's
+// octree: 0 multipole_root_kernel, 1 multipole_kernel, 2 p2m_kernel, 3 p2p_kernel.
+std::int64_t ref_gravity_kinds(int levels, int world, std::uint64_t seed, std::int32_t* kind, std::int64_t cap) {
+    try {
+        Mesh m = build_mesh(levels, world, seed);
+        const auto n = static_cast<std::int64_t>(m.grids.size());
+        if (kind != nullptr && n <= cap)
+            for (std::int64_t i = 0; i < n; ++i) {
+                const std::string k = gravity_kernel_name(m, m.grids[static_cast<std::size_t>(i)]);
+                kind[i] = k == kKernelMultipoleRoot ? 0 : k == kKernelMultipole ? 1 : k == kKernelP2M ? 2 : 3;
+            }
+        return n;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // One reference ghost exchange round at `step` (workload.cpp:572-581) on a
 // hand-built mesh; ghosts out as [g][6][N*N] (0 where no neighbour) and the
 // number of ghost parcels the transport carried.

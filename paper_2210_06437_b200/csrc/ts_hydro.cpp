@@ -34,6 +34,7 @@
 #include <thread>
 #include <vector>
 
+#include "fmm.h"
 #include "hydro_kernels.h"
 
 namespace {
@@ -47,6 +48,10 @@ constexpr const char* kNameStage[4] = {"", "hydro_stage1_kernel", "hydro_stage2_
                                        "hydro_stage3_kernel"};
 constexpr const char* kNameSignal = "signal_speed_kernel";
 constexpr const char* kNameP2P = "p2p_kernel";  // the reference's kKernelP2P (workload.hpp:46)
+constexpr const char* kNameP2M = "p2m_kernel";  // kKernelP2M (workload.hpp:47)
+constexpr const char* kNameMultipole = "multipole_kernel";           // kKernelMultipole (workload.hpp:45)
+constexpr const char* kNameMultipoleRoot = "multipole_root_kernel";  // kKernelMultipoleRoot (workload.hpp:48)
+constexpr const char* kNameFmmMoments = "fmm_moments_kernel";        // the FMM's upward P2M pass
 constexpr const char* kNamePack = "halo_pack_kernel";
 constexpr const char* kNameUnpack = "halo_unpack_kernel";
 constexpr const char* kNameAmrFill = "amr_ghost_fill_kernel";
@@ -249,6 +254,15 @@ struct ts_hydro_ctx {
     double* U[3] = {nullptr, nullptr, nullptr};
     unsigned long long* d_check = nullptr;  // [5] self-check failures (TS_CHECK builds write it)
     double* d_grav = nullptr;               // [n_owned][4][512] gravity P2P output (phi, gx, gy, gz)
+    // gravity FMM (fmm.h): the octree of the owned sub-grids and its device copy
+    bool have_fmm = false;
+    tsh::FmmTree fmm;
+    int* d_fmm_int = nullptr;     // depth, q[3], leaf, parent, child[8], nb27[27] per node (SoA, see fmm_upload)
+    double* d_fmm_M = nullptr;    // [n][4][512]
+    double* d_fmm_L = nullptr;    // [n_internal][10][512]
+    int* d_fmm_lists = nullptr;   // p2p leaves, then p2m leaves
+    tsh::FmmEntry* d_fmm_tab[tsh::kFmmRMax + 1][2] = {};  // [R][far_only]; R = 0: the root's table
+    int n_fmm_tab[tsh::kFmmRMax + 1][2] = {};
     double* d_scr_ring = nullptr;   // nf > 6: species accumulators, kScrK slots per SM id (StageArgs::scr_ring)
     unsigned int* d_scr_mask = nullptr;
     static constexpr int kScrK = 8;
@@ -514,6 +528,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_h2d_flag);
     dfree(c, &c->d_scr_ring);
     dfree(c, &c->d_grav);
+    for (auto& r : c->d_fmm_tab)
+        for (auto& t : r) dfree(c, &t);
     dfree(c, &c->d_scr_mask);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
@@ -528,6 +544,11 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_amr_level);
     dfree(c, &c->d_amr_rf_slot);
     dfree(c, &c->d_amr_rf_flux);
+    dfree(c, &c->d_fmm_int);
+    dfree(c, &c->d_fmm_M);
+    dfree(c, &c->d_fmm_L);
+    dfree(c, &c->d_fmm_lists);
+    c->have_fmm = false;
     c->wave_ready = false;
     c->amr = false;
     c->amr_mr = false;
@@ -2909,6 +2930,183 @@ int ts_hydro_download_gravity(ts_hydro_ctx* c, int64_t first, int64_t count, dou
     if (rc) return rc;
     TS_CUDA(c, cudaMemcpy(host, c->d_grav + (size_t)first * 4 * kNC, (size_t)count * 4 * kNC * sizeof(double),
                           cudaMemcpyDeviceToHost));
+    return TS_OK;
+}
+
+// ---- gravity FMM (fmm.h, fmm_kernels.cu) ----------------------
+
+int ts_hydro_set_gravity_tree(ts_hydro_ctx* c, int64_t n_leaves, const int32_t* level, const int32_t* pos,
+                              const int32_t* dims, double dx0) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (!c->have_mesh) return fail(c, TS_ESTATE, "no mesh bound (call ts_hydro_set_mesh first)");
+    if (c->world > 1) return fail(c, TS_ESTATE, "the gravity FMM is single-rank");
+    if (level == nullptr || pos == nullptr || dims == nullptr) return fail(c, TS_EINVAL, "null tree arrays");
+    if (n_leaves != c->n_owned)
+        return fail(c, TS_EINVAL, "the tree's leaves must be exactly the owned sub-grids (n_leaves != n_owned)");
+    tsh::FmmTree t;
+    const std::string err = tsh::fmm_build_tree(n_leaves, level, pos, dims, dx0, t);
+    if (!err.empty()) return fail(c, TS_EINVAL, "gravity tree: " + err);
+    cudaSetDevice(c->dev);
+    rc = sync_all(c);
+    if (rc) return rc;
+    dfree(c, &c->d_fmm_int);
+    dfree(c, &c->d_fmm_M);
+    dfree(c, &c->d_fmm_L);
+    dfree(c, &c->d_fmm_lists);
+    c->have_fmm = false;
+    const size_t n = (size_t)t.n();
+    std::vector<int> h(n * 41);  // SoA: depth | q (3n) | leaf | parent | child (8n) | nb27 (27n)
+    std::copy(t.depth.begin(), t.depth.end(), h.begin());
+    std::copy(t.q.begin(), t.q.end(), h.begin() + (ptrdiff_t)n);
+    std::copy(t.leaf.begin(), t.leaf.end(), h.begin() + (ptrdiff_t)(4 * n));
+    std::copy(t.parent.begin(), t.parent.end(), h.begin() + (ptrdiff_t)(5 * n));
+    std::copy(t.child.begin(), t.child.end(), h.begin() + (ptrdiff_t)(6 * n));
+    std::copy(t.nb27.begin(), t.nb27.end(), h.begin() + (ptrdiff_t)(14 * n));
+    std::vector<int> lists(t.leaves_p2p);
+    lists.insert(lists.end(), t.leaves_p2p_restr.begin(), t.leaves_p2p_restr.end());
+    lists.insert(lists.end(), t.leaves_p2m.begin(), t.leaves_p2m.end());
+    if ((rc = dalloc(c, &c->d_fmm_int, h.size())) || (rc = dalloc(c, &c->d_fmm_M, n * 4 * kNC)) ||
+        (rc = dalloc(c, &c->d_fmm_L, (size_t)std::max(t.n_internal, 1) * 10 * kNC)) ||
+        (rc = dalloc(c, &c->d_fmm_lists, std::max<size_t>(lists.size(), 1))))
+        return rc;
+    TS_CUDA(c, cudaMemcpy(c->d_fmm_int, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!lists.empty())
+        TS_CUDA(c, cudaMemcpy(c->d_fmm_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->fmm = std::move(t);
+    c->have_fmm = true;
+    return TS_OK;
+}
+
+int ts_hydro_gravity_tree(int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
+                          int64_t cap, int32_t* level_out, int32_t* pos_out, int32_t* kind, int32_t* leaf,
+                          int64_t* n_nodes) {
+    if (level == nullptr || pos == nullptr || dims == nullptr) return TS_EINVAL;
+    tsh::FmmTree t;
+    if (!tsh::fmm_build_tree(n_leaves, level, pos, dims, 1.0, t).empty()) return TS_EINVAL;
+    if (n_nodes != nullptr) *n_nodes = t.n();
+    if (cap < t.n()) return TS_OK;
+    for (int i = 0; i < t.n(); ++i) {
+        if (level_out != nullptr) level_out[i] = t.depth[(size_t)i] - t.T;
+        if (pos_out != nullptr)
+            for (int a = 0; a < 3; ++a) pos_out[3 * i + a] = t.q[3 * (size_t)i + a];
+        if (kind != nullptr) kind[i] = t.kind[(size_t)i];
+        if (leaf != nullptr) leaf[i] = t.leaf[(size_t)i];
+    }
+    return TS_OK;
+}
+
+namespace {
+
+int fmm_table_dev(ts_hydro_ctx* c, int radius, bool root, bool far_only, const tsh::FmmEntry** tab, int* n) {
+    const int r = root ? 0 : radius, f = far_only ? 1 : 0;
+    if (c->d_fmm_tab[r][f] == nullptr) {
+        const std::vector<tsh::FmmEntry> v = tsh::fmm_table(radius, root, far_only);
+        int rc = dalloc(c, &c->d_fmm_tab[r][f], v.size());
+        if (rc) return rc;
+        TS_CUDA(c, cudaMemcpy(c->d_fmm_tab[r][f], v.data(), v.size() * sizeof(tsh::FmmEntry),
+                              cudaMemcpyHostToDevice));
+        c->n_fmm_tab[r][f] = (int)v.size();
+    }
+    *tab = c->d_fmm_tab[r][f];
+    *n = c->n_fmm_tab[r][f];
+    return TS_OK;
+}
+
+}  // namespace
+
+int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t stream_id, uint64_t guid,
+                         ts_done_fn done, void* user) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (radius < 1 || radius > tsh::kFmmRMax) return fail(c, TS_EINVAL, "FMM radius must be 1..3 cells");
+    if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
+    if (!c->have_fmm) return fail(c, TS_ESTATE, "no gravity tree (call ts_hydro_set_gravity_tree first)");
+    if (c->din_open) return fail(c, TS_ESTATE, "gravity reads the state: close the per-sub-grid step first");
+    cudaSetDevice(c->dev);
+    if (c->d_grav == nullptr) {
+        rc = dalloc(c, &c->d_grav, (size_t)c->n_owned * 4 * kNC);
+        if (rc) return rc;
+    }
+    cudaStream_t s, s0;
+    rc = ensure_stream(c, stream_id, &s);
+    if (!rc) rc = ensure_stream(c, 0, &s0);
+    if (rc) return rc;
+    if (s != s0) {
+        TS_CUDA(c, cudaEventRecord(c->ev_in, s0));
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_in, 0));
+    }
+    const tsh::FmmTree& t = c->fmm;
+    const size_t n = (size_t)t.n();
+    tsh::FmmArgs a{};
+    a.U = c->U[0];
+    a.nf = c->nf;
+    a.depth = c->d_fmm_int;
+    a.q = c->d_fmm_int + n;
+    a.leaf = c->d_fmm_int + 4 * n;
+    a.parent = c->d_fmm_int + 5 * n;
+    a.child = c->d_fmm_int + 6 * n;
+    a.nb27 = c->d_fmm_int + 14 * n;
+    a.M = c->d_fmm_M;
+    a.L = c->d_fmm_L;
+    a.out = c->d_grav;
+    a.T = t.T;
+    a.dx0 = t.dx0;
+    a.G = G;
+    auto launch = [&](const char* name, int n_ctas, auto&& fn) -> int {
+        if (n_ctas <= 0) return TS_OK;
+        unsigned long long* stamp = nullptr;
+        int r = begin_launch(c, TS_ACTIVITY_KERNEL, name, (int32_t)stream_id, guid, &stamp);
+        if (r) return r;
+        a.stamp = stamp;
+        TS_CUDA(c, fn(n_ctas));
+        return TS_OK;
+    };
+    // P2M: every leaf's masses (the leaves follow the refined nodes)
+    a.list = nullptr;
+    a.first = t.n_internal;
+    if ((rc = launch(kNameFmmMoments, (int)n - t.n_internal, [&](int k) { return tsh::launch_fmm_moments(a, k, s); })))
+        return rc;
+    // M2M, deepest refined depth first
+    for (int d = t.max_depth - 1; d >= 0; --d) {
+        a.first = t.int_first[(size_t)d];
+        if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, t.n_int[(size_t)d],
+                         [&](int k) { return tsh::launch_fmm_restrict(a, k, s); })))
+            return rc;
+    }
+    // L2L + M2L, root first
+    for (int d = 0; d < t.max_depth; ++d) {
+        if ((rc = fmm_table_dev(c, radius, d == 0, true, &a.table, &a.n_table))) return rc;
+        a.first = t.int_first[(size_t)d];
+        if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, t.n_int[(size_t)d],
+                         [&](int k) { return tsh::launch_fmm_m2l(a, k, s); })))
+            return rc;
+    }
+    // leaves: the root alone, or the p2p / p2m lists
+    if (t.root_leaf >= 0) {
+        if ((rc = fmm_table_dev(c, radius, true, false, &a.table, &a.n_table))) return rc;
+        a.K = tsh::kFmmRootK;
+        a.first = t.root_leaf;
+        if ((rc = launch(kNameMultipoleRoot, 1, [&](int k) { return tsh::launch_fmm_leaf(a, k, false, s); })))
+            return rc;
+    } else {
+        if ((rc = fmm_table_dev(c, radius, false, false, &a.table, &a.n_table))) return rc;
+        a.K = 2 * radius + 1;
+        a.list = c->d_fmm_lists;
+        a.first = 0;
+        if ((rc = launch(kNameP2P, (int)t.leaves_p2p.size(), [&](int k) { return tsh::launch_fmm_leaf(a, k, false, s); })))
+            return rc;
+        a.first = (int)t.leaves_p2p.size();
+        if ((rc = launch(kNameP2P, (int)t.leaves_p2p_restr.size(),
+                         [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); })))
+            return rc;
+        a.first += (int)t.leaves_p2p_restr.size();
+        if ((rc = launch(kNameP2M, (int)t.leaves_p2m.size(), [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); })))
+            return rc;
+    }
+    if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
     return TS_OK;
 }
 

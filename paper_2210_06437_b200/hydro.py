@@ -164,6 +164,11 @@ _SIGNATURES = {
     "ts_hydro_gravity_p2p": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int32, _i64p, ctypes.c_int64,
                                             ctypes.c_uint32, ctypes.c_uint64, DONE_FN, _vp]),
     "ts_hydro_download_gravity": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _f64p]),
+    "ts_hydro_set_gravity_tree": (ctypes.c_int, [_vp, ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_double]),
+    "ts_hydro_gravity_tree": (ctypes.c_int, [ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_int64, _i32p, _i32p,
+                                             _i32p, _i32p, _i64p]),
+    "ts_hydro_gravity_fmm": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
+                                            DONE_FN, _vp]),
     "ts_hydro_debug_check": (ctypes.c_int, [_vp, _u64p, ctypes.c_int32]),
     "ts_hydro_check_build": (ctypes.c_int, []),
     "ts_hydro_flush_activity": (ctypes.c_int, [_vp, ctypes.POINTER(_Record), ctypes.c_uint64, _u64p]),
@@ -382,6 +387,28 @@ class Mesh:
         g = np.repeat(np.arange(self.n), 6).reshape(self.n, 6)
         m = nb >= 0
         return int((self.owner[g[m]] == self.owner[nb[m]]).sum()) // 2
+
+
+GRAVITY_KINDS = ("multipole_root_kernel", "multipole_kernel", "p2m_kernel", "p2p_kernel")
+
+
+def gravity_tree(level, pos, dims):
+    """The gravity octree of these leaves (ts_hydro_gravity_tree; host only):
+    dict of per-node level, pos [n][3], kind (index into GRAVITY_KINDS, the
+    reference's gravity_kernel_name choice) and leaf (leaf index or -1)."""
+    lv = np.ascontiguousarray(level, np.int32)
+    ps = np.ascontiguousarray(np.asarray(pos).reshape(-1, 3), np.int32)
+    dm = np.ascontiguousarray(dims, np.int32)
+    n = ctypes.c_int64()
+    args = (len(lv), _p(lv, _i32p), _p(ps, _i32p), _p(dm, _i32p))
+    if lib().ts_hydro_gravity_tree(*args, 0, None, None, None, None, ctypes.byref(n)) != TS_OK:
+        raise ValueError("malformed gravity tree (overlapping leaves or positions outside the domain)")
+    k = n.value
+    lev, kind, leaf = (np.zeros(k, np.int32) for _ in range(3))
+    pso = np.zeros((k, 3), np.int32)
+    lib().ts_hydro_gravity_tree(*args, k, _p(lev, _i32p), _p(pso, _i32p), _p(kind, _i32p), _p(leaf, _i32p),
+                                ctypes.byref(n))
+    return {"level": lev, "pos": pso, "kind": kind, "leaf": leaf}
 
 
 def uniform_mesh(nx: int, ny: int, nz: int, periodic: str = "", world: int = 1, order: str = "morton") -> Mesh:
@@ -644,6 +671,30 @@ class CudaDevice:
             n = len(idx)
         self._check(lib().ts_hydro_gravity_p2p(self._h, G, radius, None if idx is None else _p(idx, _i64p), n,
                                                stream_id, guid, self._done(done), None), "gravity_p2p")
+
+    def gravity_tree_of_mesh(self):
+        """(level, pos, dims, dx0) of the bound mesh's leaves, for set_gravity_tree."""
+        if getattr(self, "amr_mesh", None) is not None and getattr(self, "mesh", None) is None:
+            m = self.amr_mesh
+            return m.level, m.pos, m.dims, self.config.dx * 2.0 ** m.max_level
+        m = self.mesh
+        return np.zeros(m.n, np.int32), m.pos, m.dims, self.config.dx
+
+    def set_gravity_tree(self, level=None, pos=None, dims=None, dx0: Optional[float] = None) -> None:
+        """Bind the octree of the owned sub-grids for gravity_fmm (default: the bound mesh's own)."""
+        if level is None:
+            level, pos, dims, dx0 = self.gravity_tree_of_mesh()
+        lev = np.ascontiguousarray(level, np.int32)
+        ps = np.ascontiguousarray(np.asarray(pos).reshape(-1, 3), np.int32)
+        dm = np.ascontiguousarray(dims, np.int32)
+        self._check(lib().ts_hydro_set_gravity_tree(self._h, len(lev), _p(lev, _i32p), _p(ps, _i32p), _p(dm, _i32p),
+                                                    float(dx0)), "set_gravity_tree")
+
+    def gravity_fmm(self, G: float = 1.0, radius: int = 2, stream_id: int = 0, guid: int = 0, done=None) -> None:
+        """Whole gravity solve (FMM over the octree; the reference's multipole_root / multipole /
+        p2m / p2p launches, workload.cpp:365-372).  Result: download_gravity()."""
+        self._check(lib().ts_hydro_gravity_fmm(self._h, G, radius, stream_id, guid, self._done(done), None),
+                    "gravity_fmm")
 
     def download_gravity(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
         n = self.local_counts()[0] if count is None else count

@@ -71,8 +71,11 @@ def main() -> int:
         i32p = ctypes.POINTER(ctypes.c_int32)
         R.ref_build_mesh(levels, world, seed, owner.ctypes.data_as(i32p), level.ctypes.data_as(i32p),
                          pos.ctypes.data_as(i32p), nbr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n)
+        kind = np.zeros(n, np.int32)
+        R.ref_gravity_kinds(levels, world, seed, kind.ctypes.data_as(i32p), n)
         meshes.append({"levels": levels, "world": world, "seed": seed, "owner": owner.tolist(),
-                       "level": level.tolist(), "pos": pos.tolist(), "nbr": nbr.tolist()})
+                       "level": level.tolist(), "pos": pos.tolist(), "nbr": nbr.tolist(),
+                       "gravity_kind": kind.tolist()})
     vec["build_mesh"] = meshes
     with open(os.path.join(OUT, "reference_vectors.json"), "w") as f:
         json.dump(vec, f, indent=0)
