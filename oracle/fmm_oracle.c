@@ -301,14 +301,33 @@ int orc_gravity_fmm(int nf, int64_t n_leaves, const int32_t* level, const int32_
                             l2l(Lp, I, h, &phi, g, T);
                         }
                         if (f->leaf < 0) {
+                            /* the far entries in chunks of ORC_FMM_CHUNK (table
+                             * order), each summed from zero and added in order to the
+                             * parent's shifted expansion (the GPU may spread the
+                             * chunks over CTAs) */
+                            double part[10] = {0};
+                            int in_chunk = 0;
                             for (int k = 0; k < nu; ++k) {
                                 if (un[k]) continue;
                                 int J[3];
                                 for (int a = 0; a < 3; ++a) J[a] = I[a] + ((I[a] & 1) ? -uu[3 * k + a] : uu[3 * k + a]);
                                 double rho, m, c[3];
-                                if (source(&t, nf, U, M, d, J, &rho, &m, c) == 0) continue;
-                                m2l(G, m, c, xc, &phi, g, T);
+                                if (source(&t, nf, U, M, d, J, &rho, &m, c) != 0) m2l(G, m, c, xc, &part[0], part + 1, part + 4);
+                                if (++in_chunk == ORC_FMM_CHUNK) {
+                                    phi = phi + part[0];
+                                    for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
+                                    for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
+                                    memset(part, 0, sizeof(part));
+                                    in_chunk = 0;
+                                }
                             }
+                            if (in_chunk > 0) {
+                                phi = phi + part[0];
+                                for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
+                                for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
+                            }
+                        }
+                        if (f->leaf < 0) {
                             double* o = L + (i * 10) * NC + lidx(x, y, z);
                             o[0] = phi;
                             for (int a = 0; a < 3; ++a) o[(1 + a) * NC] = g[a];

@@ -152,6 +152,7 @@ void orc_gravity_p2p(const orc_params* p, int64_t ngrids, const int64_t* nbr, co
  * nodes = leaves + every ancestor.  Contract in full: DESIGN.md §15.
  * out[k][4][512] = (phi, gx, gy, gz); returns -1 on a malformed tree. */
 #define ORC_FMM_RMAX 3
+#define ORC_FMM_CHUNK 64 /* a refined node's far sum: chunks of 64 far entries, chunk sums added in order */
 /* Interaction table (octant-0 orientation, (z, y, x) lexicographic over
  * [-K, K]^3 without 0): depth >= 1 (root = 0): K = 2R+1, parent offset
  * (u >> 1) within R; depth 0 (root = 1): K = 7, all.  near[k] = |u|^2 <= R^2. */

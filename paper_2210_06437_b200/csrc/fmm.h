@@ -17,6 +17,8 @@ namespace tsh {
 
 constexpr int kFmmRMax = 3;         // interaction radius R (cells) 1..3: reach 2R+1 <= 7 < 8
 constexpr int kFmmRootK = 7;        // the root's table spans [-7, 7]^3
+constexpr int kFmmChunk = 64;       // a refined node's far sum: chunk sums of 64 entries (ORC_FMM_CHUNK)
+constexpr int kFmmSplitMax = 2048;  // (node, chunk) partial sums of one split M2L launch (scratch rows)
 constexpr int kFmmNone = -1;        // nb27 code: no source (outside the domain)
 // nb27 code <= -2: the slot lies inside a coarser leaf, node id = -2 - code
 
@@ -70,6 +72,7 @@ struct FmmArgs {
     double* M;           // [n][4][512] moments (m, cx, cy, cz)
     double* L;           // [n_internal][10][512] local expansions (phi, g, T xx yy zz xy xz yz)
     double* out;         // [leaf sub-grid][4][512] (phi, gx, gy, gz)
+    double* part;        // [kFmmSplitMax][10][512] chunk sums of a split M2L launch
     const FmmEntry* table;
     int n_table;
     int K;               // table reach: tile half-width of the leaf kernel
@@ -81,9 +84,13 @@ struct FmmArgs {
     unsigned long long* stamp;
 };
 
+// Constant-bank tables and shared-memory opt-ins on the current device (once).
+cudaError_t fmm_prepare_device();
 cudaError_t launch_fmm_moments(const FmmArgs& a, int n_ctas, cudaStream_t s);   // P2M: leaf masses
 cudaError_t launch_fmm_restrict(const FmmArgs& a, int n_ctas, cudaStream_t s);  // M2M: one depth of refined nodes
 cudaError_t launch_fmm_m2l(const FmmArgs& a, int n_ctas, cudaStream_t s);       // L2L + M2L: one depth of refined nodes
+// the same over (chunk, node) CTAs + an in-order combine: nodes a.first .. + n_nodes - 1
+cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s);
 cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaStream_t s);  // leaves: L2L + near + far
 
 }  // namespace tsh

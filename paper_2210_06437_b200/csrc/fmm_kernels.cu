@@ -75,7 +75,9 @@ __device__ __forceinline__ void m2l(double G, double m, double cx, double cy, do
                                     double xz, double& phi, double (&g)[3], double (&T)[6]) {
     const double rx = xx - cx, ry = xy - cy, rz = xz - cz;
     const double r2 = fma(rz, rz, fma(ry, ry, rx * rx));
-    const double inv = 1.0 / sqrt(r2);
+    // 1.0 / sqrt(r2) with the branch-free IEEE forms (bitwise equal for the
+    // positive normal r2 here: hydro_device.cuh, ts_hydro_selftest_math)
+    const double inv = rcp_rn(sqrt_rn(r2));
     const double inv2 = inv * inv;
     const double a1 = (G * m) * inv;
     const double a3 = a1 * inv2;
@@ -208,12 +210,21 @@ __global__ void __launch_bounds__(NC) fmm_m2l_kernel(const __grid_constant__ Fmm
     double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (d > 0) l2l(A, node, d, I, h, phi, g, T);
     const int sx = (I[0] & 1) ? -1 : 1, sy = (I[1] & 1) ? -1 : 1, sz = (I[2] & 1) ? -1 : 1;
-    for (int k = 0; k < A.n_table; ++k) {
-        const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
-        const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
-        double m, rho, c[3];
-        if (source(A, nb, q, d, h, J, m, rho, c) == 0) continue;
-        m2l<true>(A.G, m, c[0], c[1], c[2], xc[0], xc[1], xc[2], phi, g, T);
+    for (int k0 = 0; k0 < A.n_table; k0 += kFmmChunk) {  // chunk sums added in order (oracle)
+        double pp = 0.0, pg[3] = {0.0, 0.0, 0.0}, pT[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const int k1 = min(k0 + kFmmChunk, A.n_table);
+        for (int k = k0; k < k1; ++k) {
+            const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
+            const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
+            double m, rho, c[3];
+            if (source(A, nb, q, d, h, J, m, rho, c) == 0) continue;
+            m2l<true>(A.G, m, c[0], c[1], c[2], xc[0], xc[1], xc[2], pp, pg, pT);
+        }
+        phi = phi + pp;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[a] = g[a] + pg[a];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) T[j] = T[j] + pT[j];
     }
     double* o = A.L + (size_t)node * 10 * NC + t;
     o[0] = phi;
@@ -222,6 +233,71 @@ __global__ void __launch_bounds__(NC) fmm_m2l_kernel(const __grid_constant__ Fmm
     o[3 * NC] = g[2];
 #pragma unroll
     for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
+    stamp_end(A);
+}
+
+// The same sum spread over CTAs (depths with few refined nodes, the root):
+// CTA (c, n) sums chunk c of node first + n from zero for all 512 cells into
+// part[n][c]; the combine kernel adds the parent's shifted expansion and the
+// chunk sums in order — the bits of fmm_m2l_kernel.
+__global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant__ FmmArgs A) {
+    __shared__ int nb[27];
+    stamp_begin(A);
+    const int node = A.first + (int)blockIdx.y, t = threadIdx.x;
+    if (t < 27) nb[t] = A.nb27[27 * node + t];
+    __syncthreads();
+    const int d = A.depth[node];
+    const double h = hdepth(A, d);
+    const int q[3] = {A.q[3 * node], A.q[3 * node + 1], A.q[3 * node + 2]};
+    const int I[3] = {8 * q[0] + (t & 7), 8 * q[1] + ((t >> 3) & 7), 8 * q[2] + (t >> 6)};
+    const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
+    double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const int sx = (I[0] & 1) ? -1 : 1, sy = (I[1] & 1) ? -1 : 1, sz = (I[2] & 1) ? -1 : 1;
+    const int k0 = (int)blockIdx.x * kFmmChunk, k1 = min(k0 + kFmmChunk, A.n_table);
+    for (int k = k0; k < k1; ++k) {
+        const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
+        const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
+        double m, rho, c[3];
+        if (source(A, nb, q, d, h, J, m, rho, c) == 0) continue;
+        m2l<true>(A.G, m, c[0], c[1], c[2], xc[0], xc[1], xc[2], phi, g, T);
+    }
+    double* o = A.part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 10 * NC + t;
+    o[0] = phi;
+    o[NC] = g[0];
+    o[2 * NC] = g[1];
+    o[3 * NC] = g[2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
+    stamp_end(A);
+}
+
+// grid (n_nodes, 10): CTA (n, j) writes expansion component j of node
+// first + n (the shift is recomputed per component: cheap); the chunk sums are
+// loaded eight at a time and added in order.
+__global__ void __launch_bounds__(NC) fmm_m2l_combine_kernel(const __grid_constant__ FmmArgs A, int n_chunks) {
+    stamp_begin(A);
+    const int node = A.first + (int)blockIdx.x, j = (int)blockIdx.y, t = threadIdx.x;
+    const int d = A.depth[node];
+    double acc = 0.0;
+    if (d > 0) {
+        const double h = hdepth(A, d);
+        const int I[3] = {8 * A.q[3 * node] + (t & 7), 8 * A.q[3 * node + 1] + ((t >> 3) & 7),
+                          8 * A.q[3 * node + 2] + (t >> 6)};
+        double phi, g[3], T[6];
+        l2l(A, node, d, I, h, phi, g, T);
+        acc = j == 0 ? phi : (j < 4 ? g[j - 1] : T[j - 4]);
+    }
+    const double* p = A.part + ((size_t)blockIdx.x * n_chunks * 10 + j) * NC + t;
+    int c = 0;
+    for (; c + 8 <= n_chunks; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = p[(size_t)(c + k) * 10 * NC];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = acc + v[k];
+    }
+    for (; c < n_chunks; ++c) acc = acc + p[(size_t)c * 10 * NC];
+    A.L[((size_t)node * 10 + j) * NC + t] = acc;
     stamp_end(A);
 }
 
@@ -334,6 +410,14 @@ __global__ void __launch_bounds__(NC) fmm_leaf_kernel(const __grid_constant__ Fm
 
 constexpr size_t tile_bytes(int K) { return (size_t)(N + 2 * K) * (N + 2 * K) * kPitch * sizeof(double); }
 
+cudaError_t ensure_device_setup();
+
+}  // namespace
+
+cudaError_t fmm_prepare_device() { return ensure_device_setup(); }
+
+namespace {
+
 cudaError_t ensure_device_setup() {
     static std::atomic<unsigned long long> ready{0ull};
     int dev = 0;
@@ -352,6 +436,7 @@ cudaError_t ensure_device_setup() {
     }
     e = cudaMemcpyToSymbol(c_fmm_coef1, c1.data(), c1.size() * sizeof(double));
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_fmm_coef2, c2.data(), c2.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the symbol copies land before any launch
     const int smem = (int)tile_bytes(kFmmRootK);
     for (auto fn : {fmm_leaf_kernel<0, false>, fmm_leaf_kernel<0, true>, fmm_leaf_kernel<1, false>,
                     fmm_leaf_kernel<1, true>, fmm_leaf_kernel<2, false>, fmm_leaf_kernel<2, true>})
@@ -378,6 +463,14 @@ cudaError_t launch_fmm_restrict(const FmmArgs& a, int n_ctas, cudaStream_t s) {
 cudaError_t launch_fmm_m2l(const FmmArgs& a, int n_ctas, cudaStream_t s) {
     if (n_ctas <= 0) return cudaSuccess;
     fmm_m2l_kernel<<<n_ctas, NC, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s) {
+    const int n_chunks = (a.n_table + kFmmChunk - 1) / kFmmChunk;
+    if (n_nodes <= 0 || n_chunks <= 0) return cudaSuccess;
+    fmm_m2l_part_kernel<<<dim3(n_chunks, n_nodes), NC, 0, s>>>(a);
+    fmm_m2l_combine_kernel<<<dim3(n_nodes, 10), NC, 0, s>>>(a, n_chunks);
     return cudaGetLastError();
 }
 

@@ -175,6 +175,7 @@ cudaError_t launch_p2p(const P2PArgs& a, int n_ctas, cudaStream_t s) {
         for (int k = 0; k < n; ++k) lin[k] = (off3[3 * k + 2] * kTile + off3[3 * k + 1]) * kPitch + off3[3 * k];
         e = cudaMemcpyToSymbol(c_p2p_coef, coef, sizeof(coef));
         if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_p2p_off, lin, sizeof(lin));
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the symbol copies land before any launch
         const int smem = (int)(kTileDoubles * sizeof(double));
         for (auto fn : {p2p_kernel<0>, p2p_kernel<2>, p2p_kernel<4>, p2p_kernel<6>})
             if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -260,9 +260,10 @@ struct ts_hydro_ctx {
     int* d_fmm_int = nullptr;     // depth, q[3], leaf, parent, child[8], nb27[27] per node (SoA, see fmm_upload)
     double* d_fmm_M = nullptr;    // [n][4][512]
     double* d_fmm_L = nullptr;    // [n_internal][10][512]
+    double* d_fmm_part = nullptr;  // the root's chunk sums
     int* d_fmm_lists = nullptr;   // p2p leaves, then p2m leaves
-    tsh::FmmEntry* d_fmm_tab[tsh::kFmmRMax + 1][2] = {};  // [R][far_only]; R = 0: the root's table
-    int n_fmm_tab[tsh::kFmmRMax + 1][2] = {};
+    tsh::FmmEntry* d_fmm_tab[tsh::kFmmRMax + 1][2][2] = {};  // [R][root][far_only]
+    int n_fmm_tab[tsh::kFmmRMax + 1][2][2] = {};
     double* d_scr_ring = nullptr;   // nf > 6: species accumulators, kScrK slots per SM id (StageArgs::scr_ring)
     unsigned int* d_scr_mask = nullptr;
     static constexpr int kScrK = 8;
@@ -529,7 +530,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_scr_ring);
     dfree(c, &c->d_grav);
     for (auto& r : c->d_fmm_tab)
-        for (auto& t : r) dfree(c, &t);
+        for (auto& q : r)
+            for (auto& t : q) dfree(c, &t);
     dfree(c, &c->d_scr_mask);
     dfree(c, &c->d_cta_bnd);
     dfree(c, &c->d_push_tbl);
@@ -548,6 +550,7 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_fmm_M);
     dfree(c, &c->d_fmm_L);
     dfree(c, &c->d_fmm_lists);
+    dfree(c, &c->d_fmm_part);
     c->have_fmm = false;
     c->wave_ready = false;
     c->amr = false;
@@ -615,6 +618,15 @@ int harvest(ts_hydro_ctx* c) {
     // legacy-stream work does not order against our non-blocking streams
     TS_CUDA(c, cudaDeviceSynchronize());
     return TS_OK;
+}
+
+// Host -> device copy of set-up data that kernels on the context's
+// (non-blocking) streams read next: a pageable cudaMemcpy may return before its
+// DMA lands, and nothing orders those streams behind the legacy stream — so
+// wait for it.
+cudaError_t h2d_sync(void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? cudaStreamSynchronize(0) : e;
 }
 
 int sync_all(ts_hydro_ctx* c) {
@@ -1850,14 +1862,11 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
     if (!rc) rc = dalloc(c, &c->d_cta_bnd, (size_t)c->n_owned);
     if (!rc) rc = dalloc(c, &c->d_gid, (size_t)c->n_owned);
     if (rc) return rc;
-    TS_CUDA(c, cudaMemcpy(c->d_nbr, c->nbr_local.data(), c->nbr_local.size() * sizeof(int32_t),
-                          cudaMemcpyHostToDevice));
+    TS_CUDA(c, h2d_sync(c->d_nbr, c->nbr_local.data(), c->nbr_local.size() * sizeof(int32_t)));
     if (!c->interior.empty())
-        TS_CUDA(c, cudaMemcpy(c->d_interior, c->interior.data(), c->interior.size() * sizeof(int32_t),
-                              cudaMemcpyHostToDevice));
+        TS_CUDA(c, h2d_sync(c->d_interior, c->interior.data(), c->interior.size() * sizeof(int32_t)));
     if (!c->boundary.empty())
-        TS_CUDA(c, cudaMemcpy(c->d_boundary, c->boundary.data(), c->boundary.size() * sizeof(int32_t),
-                              cudaMemcpyHostToDevice));
+        TS_CUDA(c, h2d_sync(c->d_boundary, c->boundary.data(), c->boundary.size() * sizeof(int32_t)));
     {
         // fused P2P launch order: boundary sub-grid b at position b * stride
         // (while interior ones remain).  Measured on 4 B200s (Sedov 16^3 per
@@ -1915,13 +1924,13 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
                 order.push_back(interior_order[ii++]);
             }
         }
-        TS_CUDA(c, cudaMemcpy(c->d_order, order.data(), order.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_cta_bnd, bnd.data(), bnd.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        TS_CUDA(c, h2d_sync(c->d_order, order.data(), order.size() * sizeof(int32_t)));
+        TS_CUDA(c, h2d_sync(c->d_cta_bnd, bnd.data(), bnd.size() * sizeof(int32_t)));
     }
     {
         std::vector<long long> gid(c->owned_gid.begin(), c->owned_gid.end());
         if (!gid.empty())
-            TS_CUDA(c, cudaMemcpy(c->d_gid, gid.data(), gid.size() * sizeof(long long), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_gid, gid.data(), gid.size() * sizeof(long long)));
     }
     if (world > 1) {
         std::vector<int2> se((size_t)c->n_send_total), re((size_t)c->n_recv_total);
@@ -1962,14 +1971,14 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         if (!tbl.empty()) {
             rc = dalloc(c, &c->d_push_tbl, tbl.size());
             if (rc) return rc;
-            TS_CUDA(c, cudaMemcpy(c->d_push_tbl, tbl.data(), tbl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_push_tbl, tbl.data(), tbl.size() * sizeof(int2)));
         }
         TS_CUDA(c, cudaMemset(c->d_flags, 0, 2 * (size_t)world * sizeof(int32_t)));
         TS_CUDA(c, cudaMemset(c->d_gather, 0, 2 * (size_t)world * sizeof(double)));
         if (!se.empty())
-            TS_CUDA(c, cudaMemcpy(c->d_send_entries, se.data(), se.size() * sizeof(int2), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_send_entries, se.data(), se.size() * sizeof(int2)));
         if (!re.empty())
-            TS_CUDA(c, cudaMemcpy(c->d_recv_entries, re.data(), re.size() * sizeof(int2), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_recv_entries, re.data(), re.size() * sizeof(int2)));
     }
     // set-up copies ran on the legacy stream: fence them before any kernel
     TS_CUDA(c, cudaDeviceSynchronize());
@@ -2076,7 +2085,7 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
         if (!rc) rc = dalloc(c, &c->d_amr_level, (size_t)nl);
         if (rc) return rc;
         if (np > 0) {
-            TS_CUDA(c, cudaMemcpy(c->d_amr_proxy, px, (size_t)np * sizeof(tsh::AmrProxy), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_proxy, px, (size_t)np * sizeof(tsh::AmrProxy)));
             // leaf g reads proxy p = nbr[g][f] through p's face f ^ 1
             std::vector<unsigned char> pm((size_t)np, 0);
             for (int64_t g = 0; g < nl; ++g)
@@ -2084,11 +2093,11 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
                     const int64_t h = nbr[6 * g + f];
                     if (h >= nl) pm[(size_t)(h - nl)] |= (unsigned char)(1u << (f ^ 1));
                 }
-            TS_CUDA(c, cudaMemcpy(c->d_amr_pmask, pm.data(), (size_t)np, cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_pmask, pm.data(), (size_t)np));
         }
         if (nr > 0)
-            TS_CUDA(c, cudaMemcpy(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_amr_level, level, (size_t)nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_rec, rf, (size_t)nr * sizeof(tsh::AmrReflux)));
+        TS_CUDA(c, h2d_sync(c->d_amr_level, level, (size_t)nl * sizeof(int32_t)));
         if (nr > 0 && c->amr_reflux_reg) {
             // flux register: one slot per coarse-fine face side (the coarse
             // leaf's face, and the facing face of each of its 4 fine leaves)
@@ -2106,7 +2115,7 @@ int ts_hydro_set_amr_mesh(ts_hydro_ctx* c, int64_t nl, const int64_t* nbr, const
             rc = dalloc(c, &c->d_amr_rf_slot, slot.size());
             if (!rc) rc = dalloc(c, &c->d_amr_rf_flux, (size_t)std::max(ns, 1) * c->nf * kN * kN);
             if (rc) return rc;
-            TS_CUDA(c, cudaMemcpy(c->d_amr_rf_slot, slot.data(), slot.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_rf_slot, slot.data(), slot.size() * sizeof(int32_t)));
         }
     }
     c->amr = true;
@@ -2292,7 +2301,7 @@ int ts_hydro_set_amr_mesh_partitioned(ts_hydro_ctx* c, int64_t nl, const int64_t
         if (!rc) rc = dalloc(c, &c->d_amr_level, (size_t)n_leaf_local);
         if (rc) return rc;
         if (npl > 0) {
-            TS_CUDA(c, cudaMemcpy(c->d_amr_proxy, lpx.data(), (size_t)npl * sizeof(tsh::AmrProxy), cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_proxy, lpx.data(), (size_t)npl * sizeof(tsh::AmrProxy)));
             // local leaf i reads proxy p = nbr_local[i][f] through p's face f ^ 1
             std::vector<unsigned char> pm((size_t)npl, 0);
             for (int64_t i = 0; i < n_leaf_local; ++i)
@@ -2300,12 +2309,11 @@ int ts_hydro_set_amr_mesh_partitioned(ts_hydro_ctx* c, int64_t nl, const int64_t
                     const int32_t h = c->nbr_local[(size_t)i * 6 + f];
                     if (h >= n_leaf_local) pm[(size_t)(h - n_leaf_local)] |= (unsigned char)(1u << (f ^ 1));
                 }
-            TS_CUDA(c, cudaMemcpy(c->d_amr_pmask, pm.data(), (size_t)npl, cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_pmask, pm.data(), (size_t)npl));
         }
         if (nrl > 0)
-            TS_CUDA(c, cudaMemcpy(c->d_amr_rec, lrf.data(), (size_t)nrl * sizeof(tsh::AmrReflux), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_amr_level, llev.data(), (size_t)n_leaf_local * sizeof(int32_t),
-                              cudaMemcpyHostToDevice));
+            TS_CUDA(c, h2d_sync(c->d_amr_rec, lrf.data(), (size_t)nrl * sizeof(tsh::AmrReflux)));
+        TS_CUDA(c, h2d_sync(c->d_amr_level, llev.data(), (size_t)n_leaf_local * sizeof(int32_t)));
     }
     c->amr = true;
     return TS_OK;
@@ -2935,6 +2943,10 @@ int ts_hydro_download_gravity(ts_hydro_ctx* c, int64_t first, int64_t count, dou
 
 // ---- gravity FMM (fmm.h, fmm_kernels.cu) ----------------------
 
+namespace {
+int fmm_table_dev(ts_hydro_ctx* c, int radius, bool root, bool far_only, const tsh::FmmEntry** tab, int* n);
+}  // namespace
+
 int ts_hydro_set_gravity_tree(ts_hydro_ctx* c, int64_t n_leaves, const int32_t* level, const int32_t* pos,
                               const int32_t* dims, double dx0) {
     int rc = check_state(c);
@@ -2971,9 +2983,23 @@ int ts_hydro_set_gravity_tree(ts_hydro_ctx* c, int64_t n_leaves, const int32_t* 
         (rc = dalloc(c, &c->d_fmm_L, (size_t)std::max(t.n_internal, 1) * 10 * kNC)) ||
         (rc = dalloc(c, &c->d_fmm_lists, std::max<size_t>(lists.size(), 1))))
         return rc;
-    TS_CUDA(c, cudaMemcpy(c->d_fmm_int, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (c->d_fmm_part == nullptr && (rc = dalloc(c, &c->d_fmm_part, (size_t)tsh::kFmmSplitMax * 10 * kNC)))
+        return rc;
+    TS_CUDA(c, h2d_sync(c->d_fmm_int, h.data(), h.size() * sizeof(int)));
     if (!lists.empty())
-        TS_CUDA(c, cudaMemcpy(c->d_fmm_lists, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice));
+        TS_CUDA(c, h2d_sync(c->d_fmm_lists, lists.data(), lists.size() * sizeof(int)));
+    // every interaction table and the constant-bank coefficients now, then
+    // wait: a pageable cudaMemcpy may return before its DMA lands, and the
+    // solve's streams do not order behind the legacy stream
+    for (int r = 1; r <= tsh::kFmmRMax; ++r)
+        for (int o = 0; o < 2; ++o)
+            for (int f = 0; f < 2; ++f) {
+                const tsh::FmmEntry* tab;
+                int nt;
+                if ((rc = fmm_table_dev(c, r, o != 0, f != 0, &tab, &nt))) return rc;
+            }
+    TS_CUDA(c, tsh::fmm_prepare_device());
+    TS_CUDA(c, cudaDeviceSynchronize());
     c->fmm = std::move(t);
     c->have_fmm = true;
     return TS_OK;
@@ -3000,17 +3026,17 @@ int ts_hydro_gravity_tree(int64_t n_leaves, const int32_t* level, const int32_t*
 namespace {
 
 int fmm_table_dev(ts_hydro_ctx* c, int radius, bool root, bool far_only, const tsh::FmmEntry** tab, int* n) {
-    const int r = root ? 0 : radius, f = far_only ? 1 : 0;
-    if (c->d_fmm_tab[r][f] == nullptr) {
+    const int o = root ? 1 : 0, f = far_only ? 1 : 0;
+    tsh::FmmEntry*& slot = c->d_fmm_tab[radius][o][f];
+    if (slot == nullptr) {
         const std::vector<tsh::FmmEntry> v = tsh::fmm_table(radius, root, far_only);
-        int rc = dalloc(c, &c->d_fmm_tab[r][f], v.size());
+        int rc = dalloc(c, &slot, v.size());
         if (rc) return rc;
-        TS_CUDA(c, cudaMemcpy(c->d_fmm_tab[r][f], v.data(), v.size() * sizeof(tsh::FmmEntry),
-                              cudaMemcpyHostToDevice));
-        c->n_fmm_tab[r][f] = (int)v.size();
+        TS_CUDA(c, h2d_sync(slot, v.data(), v.size() * sizeof(tsh::FmmEntry)));
+        c->n_fmm_tab[radius][o][f] = (int)v.size();
     }
-    *tab = c->d_fmm_tab[r][f];
-    *n = c->n_fmm_tab[r][f];
+    *tab = slot;
+    *n = c->n_fmm_tab[radius][o][f];
     return TS_OK;
 }
 
@@ -3051,6 +3077,7 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
     a.nb27 = c->d_fmm_int + 14 * n;
     a.M = c->d_fmm_M;
     a.L = c->d_fmm_L;
+    a.part = c->d_fmm_part;
     a.out = c->d_grav;
     a.T = t.T;
     a.dx0 = t.dx0;
@@ -3080,8 +3107,14 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
     for (int d = 0; d < t.max_depth; ++d) {
         if ((rc = fmm_table_dev(c, radius, d == 0, true, &a.table, &a.n_table))) return rc;
         a.first = t.int_first[(size_t)d];
-        if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, t.n_int[(size_t)d],
-                         [&](int k) { return tsh::launch_fmm_m2l(a, k, s); })))
+        // few nodes (the root, the shallow depths): spread each node's chunks
+        // over CTAs; otherwise one CTA per node walks its chunks
+        const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
+        const int nn = t.n_int[(size_t)d];
+        const bool split = nn * n_chunks <= tsh::kFmmSplitMax && !getenv("TS_HYDRO_FMM_NOSPLIT");
+        if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, nn, [&](int k) {
+                 return split ? tsh::launch_fmm_m2l_split(a, k, s) : tsh::launch_fmm_m2l(a, k, s);
+             })))
             return rc;
     }
     // leaves: the root alone, or the p2p / p2m lists
@@ -3336,10 +3369,10 @@ int ts_hydro_p2p_import(ts_hydro_ctx* c, const void* blobs, int32_t world) {
         if (!rc) rc = dalloc(c, &c->d_push_out, po.size());
         if (!rc) rc = dalloc(c, &c->d_halo_flag, hf.size());
         if (rc) return rc;
-        TS_CUDA(c, cudaMemcpy(c->d_push_out, po.data(), po.size() * sizeof(double*), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_halo_flag, hf.data(), hf.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_push_gather, pg.data(), pg.size() * sizeof(double*), cudaMemcpyHostToDevice));
-        TS_CUDA(c, cudaMemcpy(c->d_push_flag, pf.data(), pf.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice));
+        TS_CUDA(c, h2d_sync(c->d_push_out, po.data(), po.size() * sizeof(double*)));
+        TS_CUDA(c, h2d_sync(c->d_halo_flag, hf.data(), hf.size() * sizeof(unsigned int*)));
+        TS_CUDA(c, h2d_sync(c->d_push_gather, pg.data(), pg.size() * sizeof(double*)));
+        TS_CUDA(c, h2d_sync(c->d_push_flag, pf.data(), pf.size() * sizeof(unsigned int*)));
         TS_CUDA(c, cudaDeviceSynchronize());
     }
     c->p2p = true;

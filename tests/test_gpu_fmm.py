@@ -127,3 +127,22 @@ def test_fmm_refusals(hydro):
     with pytest.raises(ValueError):
         d.gravity_fmm(radius=4)
     d.close()
+
+
+def test_fmm_one_context_every_radius_twice(hydro, oracle_lib):
+    """One context, radii 3, 1, 2, 3 back to back (the tables of every radius
+    live side by side; the set-up copies have landed before the first solve)."""
+    m = hydro.uniform_mesh(4, 4, 2)
+    dx = 1.0 / 32
+    lev = np.zeros(m.n, np.int32)
+    U = blob(lev, m.pos, dx, 6, seed=5)
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=dx))
+    d.set_mesh(m)
+    d.upload(U)
+    d.set_gravity_tree()
+    for R in (3, 1, 2, 3):
+        d.gravity_fmm(G=0.7, radius=R)
+        got = d.download_gravity()
+        want = oracle_lib.gravity_fmm(6, lev, m.pos, m.dims, dx, U, radius=R, G=0.7)
+        assert np.array_equal(got, want), R
+    d.close()

@@ -52,6 +52,17 @@ def run(name, d, leaves, reps=20):
 def main():
     import torch
     torch.cuda.init()
+    if "--ncu" in sys.argv:  # one solve per radius on the uniform mesh, for a profiler
+        m = H.uniform_mesh(16, 16, 16, order="row")
+        d = H.CudaDevice(H.HydroConfig(dx=1.0 / 128))
+        d.set_mesh(m)
+        d.upload(H.ic_fill(d.config, "sedov", m, np.arange(m.n)))
+        d.set_gravity_tree()
+        for R in (2, 3):
+            d.gravity_fmm(radius=R)
+        d.synchronize()
+        d.close()
+        return
     m = H.uniform_mesh(16, 16, 16, order="row")
     d = H.CudaDevice(H.HydroConfig(dx=1.0 / 128))
     d.set_mesh(m)
