@@ -290,6 +290,17 @@ int ts_hydro_set_gravity_tree(ts_hydro_ctx* ctx, int64_t n_leaves, const int32_t
  * ts_hydro_gravity_tree). */
 int ts_hydro_gravity_fmm(ts_hydro_ctx* ctx, double G, int32_t radius, uint32_t stream_id, uint64_t correlation_guid,
                          ts_done_fn done, void* user);
+/* The gravity source over dt on the owned sub-grids from the last gravity
+ * solve (ts_hydro_gravity_fmm or _p2p): S += dt rho g, E += dt/2 (S + S').g
+ * (oracle orc_gravity_kick, bitwise).  dt < 0: the last step's dt, read on
+ * the device.  The next step recomputes its dt from the kicked state. */
+int ts_hydro_gravity_kick(ts_hydro_ctx* ctx, double dt);
+/* Hydro with self-gravity (un-freezing gravity in config 4): per step one
+ * SSP-RK3 hydro step, the FMM on its result, the kick over that step's dt —
+ * the reference's per-step order (3 hydro rounds, then the gravity launches,
+ * workload.cpp:559-569) — all on the compute stream, no host round trip.
+ * Needs ts_hydro_set_gravity_tree; single rank. */
+int ts_hydro_step_gravity(ts_hydro_ctx* ctx, uint64_t nsteps, double G, int32_t radius);
 /* The gravity tree of these leaves (ts_hydro_set_gravity_tree's arguments; no
  * context, no device): n_nodes always, the arrays when cap >= n_nodes — per
  * node its level (hydro level: negative above level 0), pos[3] at that level,

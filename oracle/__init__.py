@@ -106,6 +106,7 @@ def lib():
                                       ctypes.c_int, ctypes.c_double, _f64p]
         L.orc_gravity_direct.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_double, _f64p,
                                          ctypes.c_double, _f64p]
+        L.orc_gravity_kick.argtypes = [ctypes.c_int, ctypes.c_int64, _f64p, _f64p, ctypes.c_double]
         L.orc_amr_fill.argtypes = [ctypes.c_int, ctypes.c_int64, _i32p, _f64p]
         L.orc_amr_reflux.argtypes = [ctypes.POINTER(Params), _i64p, _i32p, ctypes.c_int, ctypes.c_int64, _i32p,
                                      _f64p, _f64p, ctypes.c_int, ctypes.c_double]
@@ -244,6 +245,36 @@ def gravity_fmm(nf, level, pos, dims, dx0, U, radius=2, G=1.0):
                              _p(U, _f64p), radius, G, _p(out, _f64p)) != 0:
         raise ValueError("malformed gravity tree (overlapping leaves or positions outside the domain)")
     return out
+
+
+def gravity_kick(U, grav, dt):
+    """Gravity source over dt (orc_gravity_kick) on a copy of U."""
+    U = np.array(U, np.float64, copy=True, order="C")
+    grav = np.ascontiguousarray(grav, np.float64)
+    assert grav.shape[0] >= U.shape[0]
+    lib().orc_gravity_kick(U.shape[1], U.shape[0], _p(U, _f64p), _p(grav, _f64p), dt)
+    return U
+
+
+def run_self_gravity(p: Params, nbr, U, nsteps, level, pos, dims, dx0, radius=2, G=1.0, mesh=None):
+    """Hydro with self-gravity, the order ts_hydro_step_gravity follows: per
+    step one SSP-RK3 hydro step (dt from the state), the FMM on the result, the
+    kick over that dt.  mesh: an AmrMesh (then nbr is ignored and U holds the
+    leaves).  Returns (U, dts)."""
+    U = np.array(U, np.float64, copy=True, order="C")
+    dts = []
+    for _ in range(nsteps):
+        if mesh is None:
+            U, dt = run(p, nbr, U, 1)
+        else:
+            full = np.zeros((mesh.n_total,) + U.shape[1:])
+            full[:mesh.n_leaves] = U
+            full, dt = run_amr(p, mesh, full, 1)
+            U = full[:mesh.n_leaves].copy()
+        g = gravity_fmm(U.shape[1], level, pos, dims, dx0, U, radius=radius, G=G)
+        U = gravity_kick(U, g, dt[0])
+        dts.append(dt[0])
+    return U, np.array(dts)
 
 
 def gravity_direct(nf, level, pos, dims, dx0, U, G=1.0):

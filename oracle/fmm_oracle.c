@@ -418,3 +418,23 @@ int orc_gravity_direct(int nf, int64_t n_leaves, const int32_t* level, const int
     free(own);
     return 0;
 }
+
+void orc_gravity_kick(int nf, int64_t n, double* U, const double* grav, double dt) {
+    const double hdt = 0.5 * dt;
+    for (int64_t k = 0; k < n; ++k)
+        for (int i = 0; i < NC; ++i) {
+            double* u = U + (k * nf) * NC + i;
+            const double* g = grav + (k * 4) * NC + i;
+            const double rho = u[0];
+            const double gx = g[NC], gy = g[2 * NC], gz = g[3 * NC];
+            const double sx = u[NC], sy = u[2 * NC], sz = u[3 * NC];
+            const double nx = fma(dt, rho * gx, sx), ny = fma(dt, rho * gy, sy), nz = fma(dt, rho * gz, sz);
+            double w = (sx + nx) * gx;
+            w = fma(sy + ny, gy, w);
+            w = fma(sz + nz, gz, w);
+            u[NC] = nx;
+            u[2 * NC] = ny;
+            u[3 * NC] = nz;
+            u[4 * NC] = fma(hdt, w, u[4 * NC]);
+        }
+}

@@ -159,6 +159,12 @@ void orc_gravity_p2p(const orc_params* p, int64_t ngrids, const int64_t* nbr, co
 int orc_fmm_table(int radius, int root, int32_t* u, int32_t* near, int cap);
 int orc_gravity_fmm(int nf, int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
                     double dx0, const double* U, int radius, double G, double* out);
+/* The gravity source over dt (operator split after the hydro step, the
+ * reference's order: 3 hydro rounds, then the gravity launches,
+ * workload.cpp:559-569): per cell S' = fma(dt, rho g, S) per component and
+ * E' = fma(dt/2, (S + S') . g, E) (the work of the mean momentum; the dot
+ * product as (Sx+Sx')gx, then fma y, fma z).  grav = [n][4][512]. */
+void orc_gravity_kick(int nf, int64_t n, double* U, const double* grav, double dt);
 /* Brute force over every pair of leaf cells (monopoles at the centres): the
  * accuracy yardstick of the FMM, not a parity target. */
 int orc_gravity_direct(int nf, int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,

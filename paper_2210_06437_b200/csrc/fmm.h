@@ -93,4 +93,9 @@ cudaError_t launch_fmm_m2l(const FmmArgs& a, int n_ctas, cudaStream_t s);       
 cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s);
 cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaStream_t s);  // leaves: L2L + near + far
 
+// Gravity source over dt on the first n sub-grids (dt_dev: the device's
+// last-step dt, else dt).
+cudaError_t launch_gravity_kick(double* U, int nf, long long n, const double* grav, const double* dt_dev, double dt,
+                                unsigned long long* stamp, int sms, cudaStream_t s);
+
 }  // namespace tsh

@@ -11,6 +11,7 @@
 // an interaction is one LDS + four DFMA against constant-bank coefficients
 // (the octant-0 table; a cell of another octant reads the mirrored offset and
 // flips the sign of the summed components, which is exact).
+#include <algorithm>
 #include <atomic>
 #include <utility>
 
@@ -408,6 +409,36 @@ __global__ void __launch_bounds__(NC) fmm_leaf_kernel(const __grid_constant__ Fm
     stamp_end(A);
 }
 
+// Gravity source over dt (oracle orc_gravity_kick): S += dt rho g, E +=
+// dt/2 (S + S').g; dt from the device (the last step's) when dt_dev is set.
+__global__ void gravity_kick_kernel(double* __restrict__ U, int nf, long long n, const double* __restrict__ grav,
+                                    const double* dt_dev, double dt_val, unsigned long long* stamp) {
+    if (stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) atomicMax(stamp, ~globaltimer());
+    const double dt = dt_dev != nullptr ? *dt_dev : dt_val;
+    const double hdt = 0.5 * dt;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n * NC; c += (long long)gridDim.x * blockDim.x) {
+        const long long k = c / NC;
+        const int i = (int)(c % NC);
+        double* u = U + (size_t)k * nf * NC + i;
+        const double* g = grav + (size_t)k * 4 * NC + i;
+        const double rho = u[0];
+        const double gx = g[NC], gy = g[2 * NC], gz = g[3 * NC];
+        const double sx = u[NC], sy = u[2 * NC], sz = u[3 * NC];
+        const double nx = fma(dt, rho * gx, sx), ny = fma(dt, rho * gy, sy), nz = fma(dt, rho * gz, sz);
+        double w = (sx + nx) * gx;
+        w = fma(sy + ny, gy, w);
+        w = fma(sz + nz, gz, w);
+        u[NC] = nx;
+        u[2 * NC] = ny;
+        u[3 * NC] = nz;
+        u[4 * NC] = fma(hdt, w, u[4 * NC]);
+    }
+    if (stamp != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(stamp + 1, globaltimer());
+    }
+}
+
 constexpr size_t tile_bytes(int K) { return (size_t)(N + 2 * K) * (N + 2 * K) * kPitch * sizeof(double); }
 
 cudaError_t ensure_device_setup();
@@ -488,6 +519,15 @@ cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaS
                                   : fmm_leaf_kernel<2, false><<<n_ctas, NC, smem, s>>>(a);
     else restricted ? fmm_leaf_kernel<0, true><<<n_ctas, NC, smem, s>>>(a)
                     : fmm_leaf_kernel<0, false><<<n_ctas, NC, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gravity_kick(double* U, int nf, long long n, const double* grav, const double* dt_dev, double dt,
+                                unsigned long long* stamp, int sms, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const long long cells = n * NC;
+    const int blocks = (int)std::min<long long>((cells + 255) / 256, 8LL * sms);
+    gravity_kick_kernel<<<blocks, 256, 0, s>>>(U, nf, n, grav, dt_dev, dt, stamp);
     return cudaGetLastError();
 }
 

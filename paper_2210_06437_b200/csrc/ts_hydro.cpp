@@ -52,6 +52,7 @@ constexpr const char* kNameP2M = "p2m_kernel";  // kKernelP2M (workload.hpp:47)
 constexpr const char* kNameMultipole = "multipole_kernel";           // kKernelMultipole (workload.hpp:45)
 constexpr const char* kNameMultipoleRoot = "multipole_root_kernel";  // kKernelMultipoleRoot (workload.hpp:48)
 constexpr const char* kNameFmmMoments = "fmm_moments_kernel";        // the FMM's upward P2M pass
+constexpr const char* kNameGravityKick = "gravity_kick_kernel";      // the gravity source term
 constexpr const char* kNamePack = "halo_pack_kernel";
 constexpr const char* kNameUnpack = "halo_unpack_kernel";
 constexpr const char* kNameAmrFill = "amr_ghost_fill_kernel";
@@ -3140,6 +3141,54 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
             return rc;
     }
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    return TS_OK;
+}
+
+namespace {
+
+// The kick on the compute stream after everything before it; dt_dev: use the
+// last step's dt from the device.  The state changed: the next step recomputes
+// its signal speed (no stage-3 chaining across the kick).
+int do_gravity_kick(ts_hydro_ctx* c, double dt, bool last_dt) {
+    cudaStream_t s;
+    int rc = ensure_stream(c, 0, &s);
+    if (rc) return rc;
+    unsigned long long* stamp = nullptr;
+    rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameGravityKick, 0, 0, &stamp);
+    if (rc) return rc;
+    const double* dt_dev = last_dt ? c->d_dt_hist + ((c->steps_done - 1) % ts_hydro_ctx::kDtHist) : nullptr;
+    TS_CUDA(c, tsh::launch_gravity_kick(c->U[0], c->nf, c->n_owned, c->d_grav, dt_dev, dt, stamp, c->sms, s));
+    c->dt_valid = false;
+    c->flow_chain = false;
+    return TS_OK;
+}
+
+}  // namespace
+
+int ts_hydro_gravity_kick(ts_hydro_ctx* c, double dt) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
+    if (c->d_grav == nullptr) return fail(c, TS_ESTATE, "no gravity computed yet (ts_hydro_gravity_fmm / _p2p)");
+    if (!(dt >= 0.0) && c->steps_done == 0) return fail(c, TS_ESTATE, "dt < 0 means the last step's dt: no step taken yet");
+    cudaSetDevice(c->dev);
+    return do_gravity_kick(c, dt, !(dt >= 0.0));
+}
+
+int ts_hydro_step_gravity(ts_hydro_ctx* c, uint64_t nsteps, double G, int32_t radius) {
+    int rc = check_state(c);
+    if (rc) return rc;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if ((rc = mutating(c)) != TS_OK) return rc;
+    if (!c->have_fmm) return fail(c, TS_ESTATE, "no gravity tree (call ts_hydro_set_gravity_tree first)");
+    if (radius < 1 || radius > tsh::kFmmRMax) return fail(c, TS_EINVAL, "FMM radius must be 1..3 cells");
+    cudaSetDevice(c->dev);
+    for (uint64_t k = 0; k < nsteps; ++k) {
+        if ((rc = ts_hydro_step(c, 1)) != TS_OK) return rc;
+        if ((rc = ts_hydro_gravity_fmm(c, G, radius, 0, 0, nullptr, nullptr)) != TS_OK) return rc;
+        if ((rc = do_gravity_kick(c, 0.0, true)) != TS_OK) return rc;
+    }
     return TS_OK;
 }
 

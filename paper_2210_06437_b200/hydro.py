@@ -167,6 +167,8 @@ _SIGNATURES = {
     "ts_hydro_set_gravity_tree": (ctypes.c_int, [_vp, ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_double]),
     "ts_hydro_gravity_tree": (ctypes.c_int, [ctypes.c_int64, _i32p, _i32p, _i32p, ctypes.c_int64, _i32p, _i32p,
                                              _i32p, _i32p, _i64p]),
+    "ts_hydro_gravity_kick": (ctypes.c_int, [_vp, ctypes.c_double]),
+    "ts_hydro_step_gravity": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_double, ctypes.c_int32]),
     "ts_hydro_gravity_fmm": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
                                             DONE_FN, _vp]),
     "ts_hydro_debug_check": (ctypes.c_int, [_vp, _u64p, ctypes.c_int32]),
@@ -695,6 +697,14 @@ class CudaDevice:
         p2m / p2p launches, workload.cpp:365-372).  Result: download_gravity()."""
         self._check(lib().ts_hydro_gravity_fmm(self._h, G, radius, stream_id, guid, self._done(done), None),
                     "gravity_fmm")
+
+    def gravity_kick(self, dt: float = -1.0) -> None:
+        """Gravity source over dt from the last solve (dt < 0: the last step's dt)."""
+        self._check(lib().ts_hydro_gravity_kick(self._h, dt), "gravity_kick")
+
+    def step_gravity(self, nsteps: int = 1, G: float = 1.0, radius: int = 2) -> None:
+        """nsteps of hydro + self-gravity (step, FMM, kick), all on the device."""
+        self._check(lib().ts_hydro_step_gravity(self._h, nsteps, G, radius), "step_gravity")
 
     def download_gravity(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
         n = self.local_counts()[0] if count is None else count

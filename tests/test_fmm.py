@@ -146,3 +146,35 @@ def test_gravity_tree_uniform_and_refusals(hydro):
     assert set(t["kind"][t["leaf"] >= 0]) == {3}
     with pytest.raises(ValueError):
         hydro.gravity_tree([0, 0], [[0, 0, 0], [0, 0, 0]], (1, 1, 1))
+
+
+def test_self_gravity_cold_sphere_starts_homologous_collapse(oracle_lib):
+    """A cold uniform sphere at rest: after one hydro + self-gravity step
+    (oracle loop, the contract the GPU is held to bitwise) the momentum inside
+    is the kick of g = -(4 pi / 3) G rho0 r: radial, linear in r."""
+    nbr, pos, _ = oracle_lib.uniform_mesh(4, 4, 4)
+    dx0 = 1.0 / 32
+    i = np.arange(512)
+    loc = np.stack([i & 7, (i >> 3) & 7, i >> 6]).astype(float)
+    U = np.zeros((64, 6, 512))
+    rho0, a = 1.0, 0.3
+    for k in range(64):
+        xc = (pos[k][:, None] * 8 + loc + 0.5) * dx0 - 0.5
+        r = np.sqrt((xc ** 2).sum(0))
+        U[k, 0] = np.where(r < a, rho0, 1e-3)
+        U[k, 4] = 1e-6  # cold
+    p = oracle_lib.params(nf=6, dx=dx0)
+    U1, dts = oracle_lib.run_self_gravity(p, nbr, U, 1, np.zeros(64, np.int32),
+                                          pos, (4, 4, 4), dx0, radius=2, G=1.0)
+    dt = dts[0]
+    want = -(4 * np.pi / 3) * rho0
+    ratios = []
+    for k in range(64):
+        xc = (pos[k][:, None] * 8 + loc + 0.5) * dx0 - 0.5
+        r = np.sqrt((xc ** 2).sum(0))
+        inside = (r > 0.05) & (r < 0.5 * a)
+        vr = (U1[k, 1:4] * xc).sum(0) / r / U1[k, 0]
+        ratios.extend((vr[inside] / (r[inside] * dt)).tolist())
+    ratios = np.array(ratios)
+    assert len(ratios) > 100
+    assert np.abs(ratios / want - 1).max() < 0.05, (ratios.min() / want, ratios.max() / want)
