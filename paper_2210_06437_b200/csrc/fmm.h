@@ -88,8 +88,8 @@ struct FmmArgs {
 cudaError_t fmm_prepare_device();
 cudaError_t launch_fmm_moments(const FmmArgs& a, int n_ctas, cudaStream_t s);   // P2M: leaf masses
 cudaError_t launch_fmm_restrict(const FmmArgs& a, int n_ctas, cudaStream_t s);  // M2M: one depth of refined nodes
-cudaError_t launch_fmm_m2l(const FmmArgs& a, int n_ctas, cudaStream_t s);       // L2L + M2L: one depth of refined nodes
-// the same over (chunk, node) CTAs + an in-order combine: nodes a.first .. + n_nodes - 1
+// L2L + M2L of refined nodes a.first .. + n_nodes - 1 (one depth): (chunk,
+// node) CTAs + an in-order combine; n_nodes * chunks <= kFmmSplitMax
 cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s);
 cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaStream_t s);  // leaves: L2L + near + far
 

@@ -196,51 +196,11 @@ __global__ void __launch_bounds__(NC) fmm_restrict_kernel(const __grid_constant_
     stamp_end(A);
 }
 
-// L2L + M2L of a refined node (the root: no L2L, the root table).
-__global__ void __launch_bounds__(NC) fmm_m2l_kernel(const __grid_constant__ FmmArgs A) {
-    __shared__ int nb[27];
-    stamp_begin(A);
-    const int node = node_of(A), t = threadIdx.x;
-    if (t < 27) nb[t] = A.nb27[27 * node + t];
-    __syncthreads();
-    const int d = A.depth[node];
-    const double h = hdepth(A, d);
-    const int q[3] = {A.q[3 * node], A.q[3 * node + 1], A.q[3 * node + 2]};
-    const int I[3] = {8 * q[0] + (t & 7), 8 * q[1] + ((t >> 3) & 7), 8 * q[2] + (t >> 6)};
-    const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
-    double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (d > 0) l2l(A, node, d, I, h, phi, g, T);
-    const int sx = (I[0] & 1) ? -1 : 1, sy = (I[1] & 1) ? -1 : 1, sz = (I[2] & 1) ? -1 : 1;
-    for (int k0 = 0; k0 < A.n_table; k0 += kFmmChunk) {  // chunk sums added in order (oracle)
-        double pp = 0.0, pg[3] = {0.0, 0.0, 0.0}, pT[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        const int k1 = min(k0 + kFmmChunk, A.n_table);
-        for (int k = k0; k < k1; ++k) {
-            const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
-            const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
-            double m, rho, c[3];
-            if (source(A, nb, q, d, h, J, m, rho, c) == 0) continue;
-            m2l<true>(A.G, m, c[0], c[1], c[2], xc[0], xc[1], xc[2], pp, pg, pT);
-        }
-        phi = phi + pp;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) g[a] = g[a] + pg[a];
-#pragma unroll
-        for (int j = 0; j < 6; ++j) T[j] = T[j] + pT[j];
-    }
-    double* o = A.L + (size_t)node * 10 * NC + t;
-    o[0] = phi;
-    o[NC] = g[0];
-    o[2 * NC] = g[1];
-    o[3 * NC] = g[2];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
-    stamp_end(A);
-}
-
-// The same sum spread over CTAs (depths with few refined nodes, the root):
-// CTA (c, n) sums chunk c of node first + n from zero for all 512 cells into
-// part[n][c]; the combine kernel adds the parent's shifted expansion and the
-// chunk sums in order — the bits of fmm_m2l_kernel.
+// L2L + M2L of refined nodes (the root: no L2L, the root table).  The far
+// sum runs in chunks of kFmmChunk table entries, each summed from zero, added
+// in order (the oracle's contract), spread over CTAs: CTA (c, n) sums chunk c
+// of node first + n for all 512 cells into part[n][c]; the combine kernel
+// adds the parent's shifted expansion and the chunk sums in order.
 __global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant__ FmmArgs A) {
     __shared__ int nb[27];
     stamp_begin(A);
@@ -302,32 +262,40 @@ __global__ void __launch_bounds__(NC) fmm_m2l_combine_kernel(const __grid_consta
     stamp_end(A);
 }
 
+// Two cells per thread, (x, y, z) and (x, y, z + 4): the same octant, so
+// the same mirrored offset — one address, two LDS (the second at an
+// immediate S * pitch * 4 further), and each coefficient serves both cells.
 template <int R, int K>
-__device__ __forceinline__ void leaf_term(const double* base, int mx, int my, int mz, double& s0, double& s1,
-                                          double& s2, double& s3) {
+__device__ __forceinline__ void leaf_term(const double* base, int mx, int my, int mz, double (&a)[4],
+                                          double (&b)[4]) {
     constexpr int ux = R == 1 ? kU1.x[K] : kU2.x[K];
     constexpr int uy = R == 1 ? kU1.y[K] : kU2.y[K];
     constexpr int uz = R == 1 ? kU1.z[K] : kU2.z[K];
+    constexpr int S = N + 2 * (2 * R + 1);
     const double* coef = R == 1 ? c_fmm_coef1 : c_fmm_coef2;
-    const double rho = base[ux * mx + uy * my + uz * mz];
-    s0 = fma(rho, coef[4 * K], s0);
-    s1 = fma(rho, coef[4 * K + 1], s1);
-    s2 = fma(rho, coef[4 * K + 2], s2);
-    s3 = fma(rho, coef[4 * K + 3], s3);
+    const double* p = base + (ux * mx + uy * my + uz * mz);
+    const double ra = p[0], rb = p[4 * S * kPitch];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        a[j] = fma(ra, coef[4 * K + j], a[j]);
+        b[j] = fma(rb, coef[4 * K + j], b[j]);
+    }
 }
 template <int R, int... K>
-__device__ __forceinline__ void leaf_terms(const double* base, int mx, int my, int mz, double& s0, double& s1,
-                                           double& s2, double& s3, std::integer_sequence<int, K...>) {
-    (leaf_term<R, K>(base, mx, my, mz, s0, s1, s2, s3), ...);  // in table order
+__device__ __forceinline__ void leaf_terms(const double* base, int mx, int my, int mz, double (&a)[4], double (&b)[4],
+                                           std::integer_sequence<int, K...>) {
+    (leaf_term<R, K>(base, mx, my, mz, a, b), ...);  // in table order
 }
 
 // Leaves: L2L from the parent + every table entry (near and this depth's far
 // field).  Centred sources (leaf cells, pieces of coarser leaves) come from
-// the density tile; RESTR (p2m leaves): moments of refined same-depth nodes
-// through the general formula.  RS = 1, 2: unrolled constant tables; 0: the
-// runtime table (R = 3, and the root when it is the only leaf).
+// the density tile; RESTR (leaves with a refined neighbour): moments of
+// refined same-depth nodes through the general formula.  RS = 1, 2: unrolled
+// constant tables; 0: the run-time table (R = 3, and the root when it is the
+// only leaf).  256 threads, two cells each.
+constexpr int kLeafThreads = NC / 2;
 template <int RS, bool RESTR>
-__global__ void __launch_bounds__(NC) fmm_leaf_kernel(const __grid_constant__ FmmArgs A) {
+__global__ void __launch_bounds__(kLeafThreads) fmm_leaf_kernel(const __grid_constant__ FmmArgs A) {
     extern __shared__ __align__(16) double tile[];
     __shared__ int nb[27];
     stamp_begin(A);
@@ -338,7 +306,7 @@ __global__ void __launch_bounds__(NC) fmm_leaf_kernel(const __grid_constant__ Fm
     const double h = hdepth(A, d);
     const int q[3] = {A.q[3 * node], A.q[3 * node + 1], A.q[3 * node + 2]};
     const int K = A.K, S = N + 2 * K;
-    for (int i = t; i < S * S * S; i += NC) {
+    for (int i = t; i < S * S * S; i += kLeafThreads) {
         const int x = i % S - K, y = (i / S) % S - K, z = i / (S * S) - K;
         const int code = nb[(((z + 8) >> 3) * 3 + ((y + 8) >> 3)) * 3 + ((x + 8) >> 3)];
         double rho = 0.0;
@@ -355,57 +323,81 @@ __global__ void __launch_bounds__(NC) fmm_leaf_kernel(const __grid_constant__ Fm
         tile[((z + K) * S + (y + K)) * kPitch + (x + K)] = rho;
     }
     __syncthreads();
-    const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-    const int I[3] = {8 * q[0] + x, 8 * q[1] + y, 8 * q[2] + z};
-    double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6];
-    if (d > 0) l2l(A, node, d, I, h, phi, g, T);
-    const int sx = (x & 1) ? -1 : 1, sy = (y & 1) ? -1 : 1, sz = (z & 1) ? -1 : 1;
+    const int x = t & 7, y = (t >> 3) & 7, z0 = t >> 6;  // cells z0 and z0 + 4
+    const int sx = (x & 1) ? -1 : 1, sy = (y & 1) ? -1 : 1, sz = (z0 & 1) ? -1 : 1;
     const int mx = sx, my = sy * kPitch, mz = sz * kPitch * S;
-    const double* base = tile + ((z + K) * S + (y + K)) * kPitch + (x + K);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const double* base = tile + ((z0 + K) * S + (y + K)) * kPitch + (x + K);
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
     if constexpr (RS == 1) {
-        leaf_terms<1>(base, mx, my, mz, s0, s1, s2, s3, std::make_integer_sequence<int, kTabMax1>{});
+        leaf_terms<1>(base, mx, my, mz, sa, sb, std::make_integer_sequence<int, kTabMax1>{});
     } else if constexpr (RS == 2) {
-        leaf_terms<2>(base, mx, my, mz, s0, s1, s2, s3, std::make_integer_sequence<int, kTabMax2>{});
+        leaf_terms<2>(base, mx, my, mz, sa, sb, std::make_integer_sequence<int, kTabMax2>{});
     } else {
+        const int off2 = 4 * S * kPitch;
 #pragma unroll 4
         for (int k = 0; k < A.n_table; ++k) {
             const FmmEntry* e = A.table + k;
             const int4 u = __ldg(reinterpret_cast<const int4*>(e));
             const double2 c01 = __ldg(reinterpret_cast<const double2*>(e->c));
             const double2 c23 = __ldg(reinterpret_cast<const double2*>(e->c + 2));
-            const double rho = base[u.x * mx + u.y * my + u.z * mz];
-            s0 = fma(rho, c01.x, s0);
-            s1 = fma(rho, c01.y, s1);
-            s2 = fma(rho, c23.x, s2);
-            s3 = fma(rho, c23.y, s3);
+            const double* p = base + (u.x * mx + u.y * my + u.z * mz);
+            const double ra = p[0], rb = p[off2];
+            sa[0] = fma(ra, c01.x, sa[0]);
+            sa[1] = fma(ra, c01.y, sa[1]);
+            sa[2] = fma(ra, c23.x, sa[2]);
+            sa[3] = fma(ra, c23.y, sa[3]);
+            sb[0] = fma(rb, c01.x, sb[0]);
+            sb[1] = fma(rb, c01.y, sb[1]);
+            sb[2] = fma(rb, c23.x, sb[2]);
+            sb[3] = fma(rb, c23.y, sb[3]);
         }
     }
     // the octant's mirror: e = sigma u, so the summed components flip sign
     // (0 - s: a +0 sum stays +0, as the oracle's sum of mirrored terms does)
-    if (sx < 0) s1 = 0.0 - s1;
-    if (sy < 0) s2 = 0.0 - s2;
-    if (sz < 0) s3 = 0.0 - s3;
-    double rphi = 0.0, rg[3] = {0.0, 0.0, 0.0};
+    if (sx < 0) sa[1] = 0.0 - sa[1], sb[1] = 0.0 - sb[1];
+    if (sy < 0) sa[2] = 0.0 - sa[2], sb[2] = 0.0 - sb[2];
+    if (sz < 0) sa[3] = 0.0 - sa[3], sb[3] = 0.0 - sb[3];
+    const int Ia[3] = {8 * q[0] + x, 8 * q[1] + y, 8 * q[2] + z0};
+    const int Ib[3] = {Ia[0], Ia[1], Ia[2] + 4};
+    double ra[4] = {0.0, 0.0, 0.0, 0.0}, rb[4] = {0.0, 0.0, 0.0, 0.0};  // restricted sources: phi, g
     if constexpr (RESTR) {
-        const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
+        // both cells per table entry (two independent chains)
+        const double xa[3] = {centre(Ia[0], h), centre(Ia[1], h), centre(Ia[2], h)};
+        const double zb = centre(Ib[2], h);
         double Tn[6];
         for (int k = 0; k < A.n_table; ++k) {
             const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
-            const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
-            const int slot = (((J[2] >> 3) - q[2] + 1) * 3 + ((J[1] >> 3) - q[1] + 1)) * 3 + ((J[0] >> 3) - q[0] + 1);
-            const int code = nb[slot];
-            if (code < 0 || A.leaf[code] >= 0) continue;
-            const double* Ms = A.M + (size_t)code * 4 * NC + lidx(J[0] & 7, J[1] & 7, J[2] & 7);
-            m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], xc[0], xc[1], xc[2], rphi, rg, Tn);
+            const int Jx = Ia[0] + sx * u.x, Jy = Ia[1] + sy * u.y, Jza = Ia[2] + sz * u.z, Jzb = Jza + 4;
+            const int sxy = ((Jy >> 3) - q[1] + 1) * 3 + ((Jx >> 3) - q[0] + 1);
+            const int ca = nb[((Jza >> 3) - q[2] + 1) * 9 + sxy], cb = nb[((Jzb >> 3) - q[2] + 1) * 9 + sxy];
+            if (ca >= 0 && A.leaf[ca] < 0) {
+                const double* Ms = A.M + (size_t)ca * 4 * NC + lidx(Jx & 7, Jy & 7, Jza & 7);
+                double g3[3] = {ra[1], ra[2], ra[3]};
+                m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], xa[0], xa[1], xa[2], ra[0], g3, Tn);
+                ra[1] = g3[0], ra[2] = g3[1], ra[3] = g3[2];
+            }
+            if (cb >= 0 && A.leaf[cb] < 0) {
+                const double* Ms = A.M + (size_t)cb * 4 * NC + lidx(Jx & 7, Jy & 7, Jzb & 7);
+                double g3[3] = {rb[1], rb[2], rb[3]};
+                m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], xa[0], xa[1], zb, rb[0], g3, Tn);
+                rb[1] = g3[0], rb[2] = g3[1], rb[3] = g3[2];
+            }
         }
     }
     const double kphi = -A.G * (h * h), kg = A.G * h;
-    double* o = A.out + (size_t)A.leaf[node] * 4 * NC + t;
-    o[0] = (phi + kphi * s0) + rphi;
-    o[NC] = (g[0] + kg * s1) + rg[0];
-    o[2 * NC] = (g[1] + kg * s2) + rg[1];
-    o[3 * NC] = (g[2] + kg * s3) + rg[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const double* sc = c == 0 ? sa : sb;
+        const double* rc = c == 0 ? ra : rb;
+        const int* I = c == 0 ? Ia : Ib;
+        double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6];
+        if (d > 0) l2l(A, node, d, c == 0 ? Ia : Ib, h, phi, g, T);
+        double* o = A.out + (size_t)A.leaf[node] * 4 * NC + lidx(x, y, I[2] - 8 * q[2]);
+        o[0] = (phi + kphi * sc[0]) + rc[0];
+        o[NC] = (g[0] + kg * sc[1]) + rc[1];
+        o[2 * NC] = (g[1] + kg * sc[2]) + rc[2];
+        o[3 * NC] = (g[2] + kg * sc[3]) + rc[3];
+    }
     stamp_end(A);
 }
 
@@ -491,12 +483,6 @@ cudaError_t launch_fmm_restrict(const FmmArgs& a, int n_ctas, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_fmm_m2l(const FmmArgs& a, int n_ctas, cudaStream_t s) {
-    if (n_ctas <= 0) return cudaSuccess;
-    fmm_m2l_kernel<<<n_ctas, NC, 0, s>>>(a);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s) {
     const int n_chunks = (a.n_table + kFmmChunk - 1) / kFmmChunk;
     if (n_nodes <= 0 || n_chunks <= 0) return cudaSuccess;
@@ -513,12 +499,12 @@ cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaS
     const size_t smem = tile_bytes(a.K);
     // the R = 1, 2 depth >= 1 tables unrolled; R = 3 and the root's table at run time
     const int sel = a.n_table == kTabMax1 ? 1 : (a.n_table == kTabMax2 ? 2 : 0);
-    if (sel == 1) restricted ? fmm_leaf_kernel<1, true><<<n_ctas, NC, smem, s>>>(a)
-                             : fmm_leaf_kernel<1, false><<<n_ctas, NC, smem, s>>>(a);
-    else if (sel == 2) restricted ? fmm_leaf_kernel<2, true><<<n_ctas, NC, smem, s>>>(a)
-                                  : fmm_leaf_kernel<2, false><<<n_ctas, NC, smem, s>>>(a);
-    else restricted ? fmm_leaf_kernel<0, true><<<n_ctas, NC, smem, s>>>(a)
-                    : fmm_leaf_kernel<0, false><<<n_ctas, NC, smem, s>>>(a);
+    if (sel == 1) restricted ? fmm_leaf_kernel<1, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
+                             : fmm_leaf_kernel<1, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
+    else if (sel == 2) restricted ? fmm_leaf_kernel<2, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
+                                  : fmm_leaf_kernel<2, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
+    else restricted ? fmm_leaf_kernel<0, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
+                    : fmm_leaf_kernel<0, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

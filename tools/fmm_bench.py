@@ -81,5 +81,42 @@ def main():
     d.close()
 
 
+def coupled():
+    """Hydro with self-gravity (ts_hydro_step_gravity: step, FMM R = 2, kick)
+    against the hydro step alone: the polytrope (config 3: 32^3 sub-grids,
+    nf 11) and Sedov 16^3; device time per step from CUDA events around
+    back-to-back calls."""
+    import torch
+    for name, dims, prob, species, dx in (("sedov 16^3", (16, 16, 16), "sedov", 0, 1.0 / 128),
+                                          ("polytrope 32^3 nf 11", (32, 32, 32), "polytrope", 5, 1.0 / 256)):
+        m = H.uniform_mesh(*dims, order="row")
+        d = H.CudaDevice(H.HydroConfig(dx=dx, n_species=species))
+        d.set_mesh(m)
+        d.upload(H.ic_fill(d.config, prob, m, np.arange(m.n)))
+        d.set_gravity_tree()
+        out = {"mesh": name, "sub_grids": m.n}
+        for what, fn in (("hydro_only", lambda: d.step(1)), ("hydro_plus_gravity", lambda: d.step_gravity(1, 1.0, 2))):
+            for _ in range(3):
+                fn()
+            d.synchronize()
+            reps = 10
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            d.synchronize()
+            e1.record()
+            torch.cuda.synchronize()
+            out[what + "_ms_per_step"] = e0.elapsed_time(e1) / reps
+        out["gravity_share"] = 1 - out["hydro_only_ms_per_step"] / out["hydro_plus_gravity_ms_per_step"]
+        d.close()
+        print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--coupled" in sys.argv:
+        import torch
+        torch.cuda.init()
+        coupled()
+    else:
+        main()
