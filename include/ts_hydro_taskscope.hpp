@@ -86,6 +86,37 @@ public:
         return token;
     }
 
+    // The whole gravity solve of a step (the FMM over the octree: every
+    // sub-grid's multipole_root / multipole / p2m / p2p work of
+    // workload.cpp:565-569 in one call, records named by kind), after the
+    // step's hydro of every sub-grid; then, with kick = true, the source term
+    // over the last step's dt.  Needs set_gravity_tree.
+    CompletionToken launch_gravity_fmm(std::uint32_t stream_id, Guid guid, double G = 1.0, int radius = 2,
+                                       bool kick = false) {
+        auto* promise = new PromiseHandle();
+        CompletionToken token = promise->token();
+        int rc = ts_hydro_gravity_fmm(ctx_, G, radius, stream_id, guid, kick ? nullptr : &fulfil, kick ? nullptr : promise);
+        if (rc == TS_OK && kick) {
+            rc = ts_hydro_gravity_kick(ctx_, -1.0);
+            if (rc == TS_OK) rc = ts_hydro_synchronize(ctx_);  // the kick takes no callback: ready on return
+            if (rc == TS_OK) {
+                promise->set_value();
+                delete promise;
+                return token;
+            }
+        }
+        if (rc != TS_OK) {
+            delete promise;
+            check(rc, "launch_gravity_fmm");
+        }
+        return token;
+    }
+    void set_gravity_tree(const std::vector<std::int32_t>& level, const std::vector<std::int32_t>& pos,
+                          const std::int32_t dims[3], double dx0) {
+        check(ts_hydro_set_gravity_tree(ctx_, (std::int64_t)level.size(), level.data(), pos.data(), dims, dx0),
+              "set_gravity_tree");
+    }
+
     // The rest of SimDevice's public surface (device.hpp:57-64) on the GPU, so
     // a CudaHydroDevice stands in for the SimDevice a Locality owns: named
     // launches occupy their stream for the requested time (the gravity

@@ -70,12 +70,22 @@ int main(int argc, char** argv) {
     for (std::int64_t g = 0; g < 8; ++g) tokens.push_back(dev.launch_kernel("multipole_kernel", g % 4, 20000, 100 + g));
     tokens.push_back(dev.enqueue_copy(ActivityKind::copy_device_to_host, 1 << 20, 5, 99));
     for (auto& t : tokens) t->wait_blocking();
+    tokens.clear();
+    // the whole gravity solve of a step (FMM; records named by kind) and its kick
+    const std::vector<std::int32_t> lev(64, 0), posv(pos.begin(), pos.end());
+    const std::int32_t dims[3] = {4, 4, 4};
+    dev.set_gravity_tree(lev, posv, dims, cfg.dx);
+    tokens.push_back(dev.launch_gravity_fmm(3, 500, 1.0, 2, false));
+    tokens.push_back(dev.launch_gravity_fmm(4, 501, 1.0, 2, true));
+    for (auto& t : tokens) t->wait_blocking();
     const std::uint64_t h = dev.device_alloc(4096);
     dev.device_free(h);
     const auto n = dev.flush_activity(profiler);
     const Snapshot s = profiler.snapshot();
     const auto it = s.profile.find("hydro_stage1_kernel");
     const auto grav = s.profile.find("multipole_kernel");
+    const auto p2p = s.profile.find("p2p_kernel");
+    const auto root = s.profile.find("multipole_root_kernel");
 #ifdef TS_HAVE_EXPORT
     // the reference's own exporters over the real GPU activity: Google trace
     // events (device lanes 10000 + device*1000 + stream) and the profile CSV
@@ -86,9 +96,11 @@ int main(int argc, char** argv) {
         std::printf("trace events %llu, csv rows %llu\n", (unsigned long long)events, (unsigned long long)rows);
     }
 #endif
-    std::printf("records %llu, hydro_stage1_kernel calls %llu, multipole_kernel calls %llu\n", (unsigned long long)n,
-                (unsigned long long)(it == s.profile.end() ? 0 : it->second.calls),
-                (unsigned long long)(grav == s.profile.end() ? 0 : grav->second.calls));
-    return (it != s.profile.end() && it->second.calls == 4 * 64 && grav != s.profile.end() && grav->second.calls == 8) ? 0
-                                                                                                                : 1;
+    auto calls = [&](decltype(it) e) { return (unsigned long long)(e == s.profile.end() ? 0 : e->second.calls); };
+    std::printf("records %llu, hydro_stage1_kernel calls %llu, multipole_kernel calls %llu (8 named + 2 x 2 FMM), "
+                "multipole_root_kernel %llu, p2p_kernel %llu\n",
+                (unsigned long long)n, calls(it), calls(grav), calls(root), calls(p2p));
+    // 4^3 sub-grids: a root, 8 refined nodes, 64 leaves -> per solve 2 multipole (M2M + M2L of depth 1),
+    // 2 multipole_root (M2M + M2L of the root), 1 p2p (the leaves)
+    return (calls(it) == 4 * 64 && calls(grav) == 8 + 4 && calls(root) == 4 && calls(p2p) == 2) ? 0 : 1;
 }
