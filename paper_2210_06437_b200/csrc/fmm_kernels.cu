@@ -262,29 +262,33 @@ __global__ void __launch_bounds__(NC) fmm_m2l_combine_kernel(const __grid_consta
     stamp_end(A);
 }
 
-// Two cells per thread, (x, y, z) and (x, y, z + 4): the same octant, so
-// the same mirrored offset — one address, two LDS (the second at an
-// immediate S * pitch * 4 further), and each coefficient serves both cells.
-template <int R, int K>
-__device__ __forceinline__ void leaf_term(const double* base, int mx, int my, int mz, double (&a)[4],
-                                          double (&b)[4]) {
+// CPT cells per thread: (x, y, z), (x, y, z + 4) and, for CPT = 4, the same
+// at y + 4 — one octant, so one mirrored offset: one address, CPT LDS at
+// immediate distances, and each coefficient load serves every cell.
+template <int CPT>
+__device__ __forceinline__ constexpr int cell_off(int c, int S) {
+    return (c & 1) * 4 * S * kPitch + (c >> 1) * 4 * kPitch;
+}
+template <int R, int CPT, int K>
+__device__ __forceinline__ void leaf_term(const double* base, int mx, int my, int mz, double (&a)[CPT][4]) {
     constexpr int ux = R == 1 ? kU1.x[K] : kU2.x[K];
     constexpr int uy = R == 1 ? kU1.y[K] : kU2.y[K];
     constexpr int uz = R == 1 ? kU1.z[K] : kU2.z[K];
     constexpr int S = N + 2 * (2 * R + 1);
     const double* coef = R == 1 ? c_fmm_coef1 : c_fmm_coef2;
     const double* p = base + (ux * mx + uy * my + uz * mz);
-    const double ra = p[0], rb = p[4 * S * kPitch];
+    double rho[CPT];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        a[j] = fma(ra, coef[4 * K + j], a[j]);
-        b[j] = fma(rb, coef[4 * K + j], b[j]);
-    }
+    for (int c = 0; c < CPT; ++c) rho[c] = p[cell_off<CPT>(c, S)];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) a[c][j] = fma(rho[c], coef[4 * K + j], a[c][j]);
 }
-template <int R, int... K>
-__device__ __forceinline__ void leaf_terms(const double* base, int mx, int my, int mz, double (&a)[4], double (&b)[4],
+template <int R, int CPT, int... K>
+__device__ __forceinline__ void leaf_terms(const double* base, int mx, int my, int mz, double (&a)[CPT][4],
                                            std::integer_sequence<int, K...>) {
-    (leaf_term<R, K>(base, mx, my, mz, a, b), ...);  // in table order
+    (leaf_term<R, CPT, K>(base, mx, my, mz, a), ...);  // in table order
 }
 
 // Leaves: L2L from the parent + every table entry (near and this depth's far
@@ -292,10 +296,10 @@ __device__ __forceinline__ void leaf_terms(const double* base, int mx, int my, i
 // the density tile; RESTR (leaves with a refined neighbour): moments of
 // refined same-depth nodes through the general formula.  RS = 1, 2: unrolled
 // constant tables; 0: the run-time table (R = 3, and the root when it is the
-// only leaf).  256 threads, two cells each.
-constexpr int kLeafThreads = NC / 2;
-template <int RS, bool RESTR>
-__global__ void __launch_bounds__(kLeafThreads) fmm_leaf_kernel(const __grid_constant__ FmmArgs A) {
+// only leaf).  512 / CPT threads, CPT cells each.
+template <int RS, bool RESTR, int CPT>
+__global__ void __launch_bounds__(NC / CPT) fmm_leaf_kernel(const __grid_constant__ FmmArgs A) {
+    constexpr int NT = NC / CPT;
     extern __shared__ __align__(16) double tile[];
     __shared__ int nb[27];
     stamp_begin(A);
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(kLeafThreads) fmm_leaf_kernel(const __grid_con
     const double h = hdepth(A, d);
     const int q[3] = {A.q[3 * node], A.q[3 * node + 1], A.q[3 * node + 2]};
     const int K = A.K, S = N + 2 * K;
-    for (int i = t; i < S * S * S; i += kLeafThreads) {
+    for (int i = t; i < S * S * S; i += NT) {
         const int x = i % S - K, y = (i / S) % S - K, z = i / (S * S) - K;
         const int code = nb[(((z + 8) >> 3) * 3 + ((y + 8) >> 3)) * 3 + ((x + 8) >> 3)];
         double rho = 0.0;
@@ -323,17 +327,23 @@ __global__ void __launch_bounds__(kLeafThreads) fmm_leaf_kernel(const __grid_con
         tile[((z + K) * S + (y + K)) * kPitch + (x + K)] = rho;
     }
     __syncthreads();
-    const int x = t & 7, y = (t >> 3) & 7, z0 = t >> 6;  // cells z0 and z0 + 4
-    const int sx = (x & 1) ? -1 : 1, sy = (y & 1) ? -1 : 1, sz = (z0 & 1) ? -1 : 1;
+    // cell c of this thread: (x, y0 + 4 (c >> 1), z0 + 4 (c & 1))
+    const int x = t & 7;
+    const int y0 = CPT == 4 ? (t >> 3) & 3 : (t >> 3) & 7;
+    const int z0 = CPT == 4 ? t >> 5 : t >> 6;
+    const int sx = (x & 1) ? -1 : 1, sy = (y0 & 1) ? -1 : 1, sz = (z0 & 1) ? -1 : 1;
     const int mx = sx, my = sy * kPitch, mz = sz * kPitch * S;
-    const double* base = tile + ((z0 + K) * S + (y + K)) * kPitch + (x + K);
-    double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* base = tile + ((z0 + K) * S + (y0 + K)) * kPitch + (x + K);
+    double acc[CPT][4];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[c][j] = 0.0;
     if constexpr (RS == 1) {
-        leaf_terms<1>(base, mx, my, mz, sa, sb, std::make_integer_sequence<int, kTabMax1>{});
+        leaf_terms<1, CPT>(base, mx, my, mz, acc, std::make_integer_sequence<int, kTabMax1>{});
     } else if constexpr (RS == 2) {
-        leaf_terms<2>(base, mx, my, mz, sa, sb, std::make_integer_sequence<int, kTabMax2>{});
+        leaf_terms<2, CPT>(base, mx, my, mz, acc, std::make_integer_sequence<int, kTabMax2>{});
     } else {
-        const int off2 = 4 * S * kPitch;
 #pragma unroll 4
         for (int k = 0; k < A.n_table; ++k) {
             const FmmEntry* e = A.table + k;
@@ -341,62 +351,60 @@ __global__ void __launch_bounds__(kLeafThreads) fmm_leaf_kernel(const __grid_con
             const double2 c01 = __ldg(reinterpret_cast<const double2*>(e->c));
             const double2 c23 = __ldg(reinterpret_cast<const double2*>(e->c + 2));
             const double* p = base + (u.x * mx + u.y * my + u.z * mz);
-            const double ra = p[0], rb = p[off2];
-            sa[0] = fma(ra, c01.x, sa[0]);
-            sa[1] = fma(ra, c01.y, sa[1]);
-            sa[2] = fma(ra, c23.x, sa[2]);
-            sa[3] = fma(ra, c23.y, sa[3]);
-            sb[0] = fma(rb, c01.x, sb[0]);
-            sb[1] = fma(rb, c01.y, sb[1]);
-            sb[2] = fma(rb, c23.x, sb[2]);
-            sb[3] = fma(rb, c23.y, sb[3]);
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const double rho = p[cell_off<CPT>(c, S)];
+                acc[c][0] = fma(rho, c01.x, acc[c][0]);
+                acc[c][1] = fma(rho, c01.y, acc[c][1]);
+                acc[c][2] = fma(rho, c23.x, acc[c][2]);
+                acc[c][3] = fma(rho, c23.y, acc[c][3]);
+            }
         }
     }
     // the octant's mirror: e = sigma u, so the summed components flip sign
     // (0 - s: a +0 sum stays +0, as the oracle's sum of mirrored terms does)
-    if (sx < 0) sa[1] = 0.0 - sa[1], sb[1] = 0.0 - sb[1];
-    if (sy < 0) sa[2] = 0.0 - sa[2], sb[2] = 0.0 - sb[2];
-    if (sz < 0) sa[3] = 0.0 - sa[3], sb[3] = 0.0 - sb[3];
-    const int Ia[3] = {8 * q[0] + x, 8 * q[1] + y, 8 * q[2] + z0};
-    const int Ib[3] = {Ia[0], Ia[1], Ia[2] + 4};
-    double ra[4] = {0.0, 0.0, 0.0, 0.0}, rb[4] = {0.0, 0.0, 0.0, 0.0};  // restricted sources: phi, g
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (sx < 0) acc[c][1] = 0.0 - acc[c][1];
+        if (sy < 0) acc[c][2] = 0.0 - acc[c][2];
+        if (sz < 0) acc[c][3] = 0.0 - acc[c][3];
+    }
+    double racc[CPT][4];  // restricted sources: phi, g
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) racc[c][j] = 0.0;
     if constexpr (RESTR) {
-        // both cells per table entry (two independent chains)
-        const double xa[3] = {centre(Ia[0], h), centre(Ia[1], h), centre(Ia[2], h)};
-        const double zb = centre(Ib[2], h);
-        double Tn[6];
+        // every cell per table entry (independent chains)
         for (int k = 0; k < A.n_table; ++k) {
             const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
-            const int Jx = Ia[0] + sx * u.x, Jy = Ia[1] + sy * u.y, Jza = Ia[2] + sz * u.z, Jzb = Jza + 4;
-            const int sxy = ((Jy >> 3) - q[1] + 1) * 3 + ((Jx >> 3) - q[0] + 1);
-            const int ca = nb[((Jza >> 3) - q[2] + 1) * 9 + sxy], cb = nb[((Jzb >> 3) - q[2] + 1) * 9 + sxy];
-            if (ca >= 0 && A.leaf[ca] < 0) {
-                const double* Ms = A.M + (size_t)ca * 4 * NC + lidx(Jx & 7, Jy & 7, Jza & 7);
-                double g3[3] = {ra[1], ra[2], ra[3]};
-                m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], xa[0], xa[1], xa[2], ra[0], g3, Tn);
-                ra[1] = g3[0], ra[2] = g3[1], ra[3] = g3[2];
-            }
-            if (cb >= 0 && A.leaf[cb] < 0) {
-                const double* Ms = A.M + (size_t)cb * 4 * NC + lidx(Jx & 7, Jy & 7, Jzb & 7);
-                double g3[3] = {rb[1], rb[2], rb[3]};
-                m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], xa[0], xa[1], zb, rb[0], g3, Tn);
-                rb[1] = g3[0], rb[2] = g3[1], rb[3] = g3[2];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int I[3] = {8 * q[0] + x, 8 * q[1] + y0 + 4 * (c >> 1), 8 * q[2] + z0 + 4 * (c & 1)};
+                const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
+                const int code =
+                    nb[(((J[2] >> 3) - q[2] + 1) * 3 + ((J[1] >> 3) - q[1] + 1)) * 3 + ((J[0] >> 3) - q[0] + 1)];
+                if (code < 0 || A.leaf[code] >= 0) continue;
+                const double* Ms = A.M + (size_t)code * 4 * NC + lidx(J[0] & 7, J[1] & 7, J[2] & 7);
+                double g3[3] = {racc[c][1], racc[c][2], racc[c][3]}, Tn[6];
+                m2l<false>(A.G, Ms[0], Ms[NC], Ms[2 * NC], Ms[3 * NC], centre(I[0], h), centre(I[1], h),
+                           centre(I[2], h), racc[c][0], g3, Tn);
+                racc[c][1] = g3[0], racc[c][2] = g3[1], racc[c][3] = g3[2];
             }
         }
     }
     const double kphi = -A.G * (h * h), kg = A.G * h;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const double* sc = c == 0 ? sa : sb;
-        const double* rc = c == 0 ? ra : rb;
-        const int* I = c == 0 ? Ia : Ib;
+    for (int c = 0; c < CPT; ++c) {
+        const int yc = y0 + 4 * (c >> 1), zc = z0 + 4 * (c & 1);
+        const int I[3] = {8 * q[0] + x, 8 * q[1] + yc, 8 * q[2] + zc};
         double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6];
-        if (d > 0) l2l(A, node, d, c == 0 ? Ia : Ib, h, phi, g, T);
-        double* o = A.out + (size_t)A.leaf[node] * 4 * NC + lidx(x, y, I[2] - 8 * q[2]);
-        o[0] = (phi + kphi * sc[0]) + rc[0];
-        o[NC] = (g[0] + kg * sc[1]) + rc[1];
-        o[2 * NC] = (g[1] + kg * sc[2]) + rc[2];
-        o[3 * NC] = (g[2] + kg * sc[3]) + rc[3];
+        if (d > 0) l2l(A, node, d, I, h, phi, g, T);
+        double* o = A.out + (size_t)A.leaf[node] * 4 * NC + lidx(x, yc, zc);
+        o[0] = (phi + kphi * acc[c][0]) + racc[c][0];
+        o[NC] = (g[0] + kg * acc[c][1]) + racc[c][1];
+        o[2 * NC] = (g[1] + kg * acc[c][2]) + racc[c][2];
+        o[3 * NC] = (g[2] + kg * acc[c][3]) + racc[c][3];
     }
     stamp_end(A);
 }
@@ -461,9 +469,12 @@ cudaError_t ensure_device_setup() {
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_fmm_coef2, c2.data(), c2.size() * sizeof(double));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the symbol copies land before any launch
     const int smem = (int)tile_bytes(kFmmRootK);
-    for (auto fn : {fmm_leaf_kernel<0, false>, fmm_leaf_kernel<0, true>, fmm_leaf_kernel<1, false>,
-                    fmm_leaf_kernel<1, true>, fmm_leaf_kernel<2, false>, fmm_leaf_kernel<2, true>})
+#define TS_FMM_LEAF_ATTR(CPT)                                                                              \
+    for (auto fn : {fmm_leaf_kernel<0, false, CPT>, fmm_leaf_kernel<0, true, CPT>, fmm_leaf_kernel<1, false, CPT>, \
+                    fmm_leaf_kernel<1, true, CPT>, fmm_leaf_kernel<2, false, CPT>, fmm_leaf_kernel<2, true, CPT>})   \
         if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    TS_FMM_LEAF_ATTR(2)
+#undef TS_FMM_LEAF_ATTR
     if (e != cudaSuccess) return e;
     ready.fetch_or(bit, std::memory_order_acq_rel);
     return cudaSuccess;
@@ -499,12 +510,13 @@ cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaS
     const size_t smem = tile_bytes(a.K);
     // the R = 1, 2 depth >= 1 tables unrolled; R = 3 and the root's table at run time
     const int sel = a.n_table == kTabMax1 ? 1 : (a.n_table == kTabMax2 ? 2 : 0);
-    if (sel == 1) restricted ? fmm_leaf_kernel<1, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
-                             : fmm_leaf_kernel<1, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
-    else if (sel == 2) restricted ? fmm_leaf_kernel<2, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
-                                  : fmm_leaf_kernel<2, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
-    else restricted ? fmm_leaf_kernel<0, true><<<n_ctas, kLeafThreads, smem, s>>>(a)
-                    : fmm_leaf_kernel<0, false><<<n_ctas, kLeafThreads, smem, s>>>(a);
+    // two cells per thread: 0.262 ms for the 16^3 Sedov leaves at R = 2,
+    // against 0.277 for one and 0.388 for four (128 threads: 12 warps/SM)
+#define TS_FMM_LEAF_LAUNCH(RS, RESTR) fmm_leaf_kernel<RS, RESTR, 2><<<n_ctas, NC / 2, smem, s>>>(a)
+    if (sel == 1) restricted ? TS_FMM_LEAF_LAUNCH(1, true) : TS_FMM_LEAF_LAUNCH(1, false);
+    else if (sel == 2) restricted ? TS_FMM_LEAF_LAUNCH(2, true) : TS_FMM_LEAF_LAUNCH(2, false);
+    else restricted ? TS_FMM_LEAF_LAUNCH(0, true) : TS_FMM_LEAF_LAUNCH(0, false);
+#undef TS_FMM_LEAF_LAUNCH
     return cudaGetLastError();
 }
 
