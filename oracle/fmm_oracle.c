@@ -20,6 +20,8 @@
 #include "hydro_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -227,6 +229,116 @@ int orc_fmm_table(int radius, int root, int32_t* u, int32_t* near, int cap) {
     return n;
 }
 
+typedef struct {
+    const ftree* t;
+    int nf;
+    const double* U;
+    const double* M;
+    double* L;
+    double* out;
+    double G;
+    const int32_t *tu, *tn, *ru, *rn;
+    int nt, nr;
+    int d, tid, nth;
+} down_job;
+
+/* One node of the downward pass (refined: its expansions; leaf: its field). */
+static void down_node(const down_job* j, int64_t i) {
+    const ftree t = *j->t;
+    const int nf = j->nf, d = j->d;
+    const double* U = j->U;
+    const double* M = j->M;
+    double* L = j->L;
+    double* out = j->out;
+    const double G = j->G;
+    const int32_t *tu = j->tu, *tn = j->tn, *ru = j->ru, *rn = j->rn;
+    const int nt = j->nt, nr = j->nr;
+    const fnode* f = &t.nodes[i];
+    const double h = hdepth(&t, d);
+    const int32_t* uu = d == 0 ? ru : tu;
+    const int32_t* un = d == 0 ? rn : tn;
+    const int nu = d == 0 ? nr : nt;
+    for (int z = 0; z < N; ++z)
+        for (int y = 0; y < N; ++y)
+            for (int x = 0; x < N; ++x) {
+                const int I[3] = {8 * f->q[0] + x, 8 * f->q[1] + y, 8 * f->q[2] + z};
+                const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
+                double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0, 0, 0, 0, 0, 0};
+                if (d > 0) {
+                    const fnode* pf = &t.nodes[f->parent];
+                    const int64_t lp = lidx((I[0] >> 1) - 8 * pf->q[0], (I[1] >> 1) - 8 * pf->q[1],
+                                            (I[2] >> 1) - 8 * pf->q[2]);
+                    double Lp[10];
+                    for (int k = 0; k < 10; ++k) Lp[k] = L[(f->parent * 10 + k) * NC + lp];
+                    l2l(Lp, I, h, &phi, g, T);
+                }
+                if (f->leaf < 0) {
+                    /* the far entries in chunks of ORC_FMM_CHUNK (table
+                     * order), each summed from zero and added in order to the
+                     * parent's shifted expansion (the GPU may spread the
+                     * chunks over CTAs) */
+                    double part[10] = {0};
+                    int in_chunk = 0;
+                    for (int k = 0; k < nu; ++k) {
+                        if (un[k]) continue;
+                        int J[3];
+                        for (int a = 0; a < 3; ++a) J[a] = I[a] + ((I[a] & 1) ? -uu[3 * k + a] : uu[3 * k + a]);
+                        double rho, m, c[3];
+                        if (source(&t, nf, U, M, d, J, &rho, &m, c) != 0) m2l(G, m, c, xc, &part[0], part + 1, part + 4);
+                        if (++in_chunk == ORC_FMM_CHUNK) {
+                            phi = phi + part[0];
+                            for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
+                            for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
+                            memset(part, 0, sizeof(part));
+                            in_chunk = 0;
+                        }
+                    }
+                    if (in_chunk > 0) {
+                        phi = phi + part[0];
+                        for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
+                        for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
+                    }
+                }
+                if (f->leaf < 0) {
+                    double* o = L + (i * 10) * NC + lidx(x, y, z);
+                    o[0] = phi;
+                    for (int a = 0; a < 3; ++a) o[(1 + a) * NC] = g[a];
+                    for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
+                    continue;
+                }
+                double s0 = 0.0, s[3] = {0.0, 0.0, 0.0}, rphi = 0.0, rg[3] = {0.0, 0.0, 0.0};
+                for (int k = 0; k < nu; ++k) {
+                    int e[3], J[3];
+                    for (int a = 0; a < 3; ++a) {
+                        e[a] = (I[a] & 1) ? -uu[3 * k + a] : uu[3 * k + a];
+                        J[a] = I[a] + e[a];
+                    }
+                    double rho, m, c[3];
+                    const int kind = source(&t, nf, U, M, d, J, &rho, &m, c);
+                    if (kind == 1) {
+                        const int r2 = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+                        const double c0 = 1.0 / sqrt((double)r2);
+                        const double c3 = c0 / (double)r2;
+                        s0 = fma(rho, c0, s0);
+                        for (int a = 0; a < 3; ++a) s[a] = fma(rho, (double)e[a] * c3, s[a]);
+                    } else if (kind == 2) {
+                        m2l(G, m, c, xc, &rphi, rg, NULL);
+                    }
+                }
+                const double kphi = -G * (h * h), kg = G * h;
+                double* o = out + (f->leaf * 4) * NC + lidx(x, y, z);
+                o[0] = (phi + kphi * s0) + rphi;
+                for (int a = 0; a < 3; ++a) o[(1 + a) * NC] = (g[a] + kg * s[a]) + rg[a];
+            }
+}
+
+static void* down_worker(void* arg) {
+    const down_job* j = (const down_job*)arg;
+    for (int64_t i = j->tid; i < j->t->n; i += j->nth)
+        if (j->t->nodes[i].depth == j->d) down_node(j, i);
+    return NULL;
+}
+
 int orc_gravity_fmm(int nf, int64_t n_leaves, const int32_t* level, const int32_t* pos, const int32_t* dims,
                     double dx0, const double* U, int radius, double G, double* out) {
     if (radius < 1 || radius > ORC_FMM_RMAX || n_leaves <= 0) return -1;
@@ -278,87 +390,21 @@ int orc_gravity_fmm(int nf, int64_t n_leaves, const int32_t* level, const int32_
     int32_t* rn = (int32_t*)malloc(sizeof(int32_t) * 4096);
     const int nt = orc_fmm_table(radius, 0, tu, tn, 4096);
     const int nr = orc_fmm_table(radius, 1, ru, rn, 4096);
-    for (int d = 0; d <= maxd; ++d)
-        for (int64_t i = 0; i < nn; ++i) {
-            const fnode* f = &t.nodes[i];
-            if (f->depth != d) continue;
-            const double h = hdepth(&t, d);
-            const int32_t* uu = d == 0 ? ru : tu;
-            const int32_t* un = d == 0 ? rn : tn;
-            const int nu = d == 0 ? nr : nt;
-            for (int z = 0; z < N; ++z)
-                for (int y = 0; y < N; ++y)
-                    for (int x = 0; x < N; ++x) {
-                        const int I[3] = {8 * f->q[0] + x, 8 * f->q[1] + y, 8 * f->q[2] + z};
-                        const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
-                        double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0, 0, 0, 0, 0, 0};
-                        if (d > 0) {
-                            const fnode* pf = &t.nodes[f->parent];
-                            const int64_t lp = lidx((I[0] >> 1) - 8 * pf->q[0], (I[1] >> 1) - 8 * pf->q[1],
-                                                    (I[2] >> 1) - 8 * pf->q[2]);
-                            double Lp[10];
-                            for (int k = 0; k < 10; ++k) Lp[k] = L[(f->parent * 10 + k) * NC + lp];
-                            l2l(Lp, I, h, &phi, g, T);
-                        }
-                        if (f->leaf < 0) {
-                            /* the far entries in chunks of ORC_FMM_CHUNK (table
-                             * order), each summed from zero and added in order to the
-                             * parent's shifted expansion (the GPU may spread the
-                             * chunks over CTAs) */
-                            double part[10] = {0};
-                            int in_chunk = 0;
-                            for (int k = 0; k < nu; ++k) {
-                                if (un[k]) continue;
-                                int J[3];
-                                for (int a = 0; a < 3; ++a) J[a] = I[a] + ((I[a] & 1) ? -uu[3 * k + a] : uu[3 * k + a]);
-                                double rho, m, c[3];
-                                if (source(&t, nf, U, M, d, J, &rho, &m, c) != 0) m2l(G, m, c, xc, &part[0], part + 1, part + 4);
-                                if (++in_chunk == ORC_FMM_CHUNK) {
-                                    phi = phi + part[0];
-                                    for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
-                                    for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
-                                    memset(part, 0, sizeof(part));
-                                    in_chunk = 0;
-                                }
-                            }
-                            if (in_chunk > 0) {
-                                phi = phi + part[0];
-                                for (int a = 0; a < 3; ++a) g[a] = g[a] + part[1 + a];
-                                for (int q = 0; q < 6; ++q) T[q] = T[q] + part[4 + q];
-                            }
-                        }
-                        if (f->leaf < 0) {
-                            double* o = L + (i * 10) * NC + lidx(x, y, z);
-                            o[0] = phi;
-                            for (int a = 0; a < 3; ++a) o[(1 + a) * NC] = g[a];
-                            for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
-                            continue;
-                        }
-                        double s0 = 0.0, s[3] = {0.0, 0.0, 0.0}, rphi = 0.0, rg[3] = {0.0, 0.0, 0.0};
-                        for (int k = 0; k < nu; ++k) {
-                            int e[3], J[3];
-                            for (int a = 0; a < 3; ++a) {
-                                e[a] = (I[a] & 1) ? -uu[3 * k + a] : uu[3 * k + a];
-                                J[a] = I[a] + e[a];
-                            }
-                            double rho, m, c[3];
-                            const int kind = source(&t, nf, U, M, d, J, &rho, &m, c);
-                            if (kind == 1) {
-                                const int r2 = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
-                                const double c0 = 1.0 / sqrt((double)r2);
-                                const double c3 = c0 / (double)r2;
-                                s0 = fma(rho, c0, s0);
-                                for (int a = 0; a < 3; ++a) s[a] = fma(rho, (double)e[a] * c3, s[a]);
-                            } else if (kind == 2) {
-                                m2l(G, m, c, xc, &rphi, rg, NULL);
-                            }
-                        }
-                        const double kphi = -G * (h * h), kg = G * h;
-                        double* o = out + (f->leaf * 4) * NC + lidx(x, y, z);
-                        o[0] = (phi + kphi * s0) + rphi;
-                        for (int a = 0; a < 3; ++a) o[(1 + a) * NC] = (g[a] + kg * s[a]) + rg[a];
-                    }
+    /* nodes of one depth are independent: spread them over host threads */
+    long nth = sysconf(_SC_NPROCESSORS_ONLN);
+    if (getenv("ORC_THREADS") != NULL) nth = atol(getenv("ORC_THREADS"));
+    if (nth < 1) nth = 1;
+    if (nth > 64) nth = 64;
+    for (int d = 0; d <= maxd; ++d) {
+        down_job jobs[64];
+        pthread_t th[64];
+        for (int k = 0; k < nth; ++k) {
+            jobs[k] = (down_job){&t, nf, U, M, L, out, G, tu, tn, ru, rn, nt, nr, d, k, (int)nth};
+            if (k > 0) pthread_create(&th[k], NULL, down_worker, &jobs[k]);
         }
+        down_worker(&jobs[0]);
+        for (int k = 1; k < nth; ++k) pthread_join(th[k], NULL);
+    }
     free(tu);
     free(tn);
     free(ru);

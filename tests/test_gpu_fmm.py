@@ -199,3 +199,28 @@ def test_step_gravity_matches_oracle(hydro, oracle_lib, case):
                                             radius=2, G=3.0, mesh=mesh)
     assert dt == dts[-1]
     assert np.array_equal(got, want), f"max abs diff {np.abs(got - want).max():.3e}"
+
+
+def test_fmm_full_size_sedov_and_amr_match_oracle(hydro, oracle_lib):
+    """BASELINE config 2's mesh (16^3 sub-grids, 2 M cells) after two Sedov
+    steps, and a 16^3 AMR mesh with a refined centre (4544 leaves): bitwise."""
+    m = hydro.uniform_mesh(16, 16, 16, order="row")
+    dx = 1.0 / 128
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=dx))
+    d.set_mesh(m)
+    d.upload(hydro.ic_fill(d.config, "sedov", m, np.arange(m.n)))
+    d.step(2)
+    d.set_gravity_tree()
+    d.gravity_fmm(G=1.0, radius=2)
+    got = d.download_gravity()
+    U = d.download()
+    d.close()
+    want = oracle_lib.gravity_fmm(6, np.zeros(m.n, np.int32), m.pos, m.dims, dx, U, radius=2, G=1.0)
+    assert np.array_equal(got, want)
+    a = amr.amr_mesh(16, 16, 16, lambda L, p: all(6 <= v < 10 for v in p))
+    dx = 1.0 / 256
+    U0 = blob(a.level, a.pos, 2 * dx, 6, centre=(0.5, 0.5, 0.5), width=0.1)
+    got, recs = fmm_gpu(hydro, lambda d: d.set_amr_mesh(a), U0, 2, dx=dx)
+    want = oracle_lib.gravity_fmm(6, a.level, a.pos, a.dims, 2 * dx, U0, radius=2, G=1.3)
+    assert np.array_equal(got, want)
+    assert {"p2p_kernel", "p2m_kernel", "multipole_kernel", "multipole_root_kernel"} <= {r.name for r in recs}
