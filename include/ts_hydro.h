@@ -242,12 +242,19 @@ int ts_hydro_launch_count(const ts_hydro_ctx* ctx, uint64_t* launches);
  * and its face neighbours' previous stage (and stage 1 for the previous
  * step's stage-3 count, which carries dt); a launch whose producers were not
  * issued yet is parked and issued once they are.  dt: ts_hydro_compute_dt
- * before the first step, then from the device.  Single rank (TS_ESTATE
- * otherwise); state-changing calls fail with TS_ESTATE while a step is open. */
+ * before the first step, then from the device.  On N ranks (fused P2P
+ * transport: ts_hydro_p2p_import; TS_ESTATE otherwise) a boundary sub-grid's
+ * launch also acquires the peers' halo slabs of its input and pushes its
+ * output's slabs into the peers' proxies, as the batched step does; a stage-k
+ * launch holding a boundary sub-grid is issued once every boundary sub-grid
+ * has issued stage k-1; the step's dt is reduced over the ranks when the step
+ * closes.  Drop-in steps are collective like ts_hydro_step.  State-changing
+ * calls fail with TS_ESTATE while a step is open. */
 int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned_index, int64_t count,
                           uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
 /* Close the open per-sub-grid step (every owned sub-grid launched stage 3):
- * joins the step's streams into the compute stream, no host wait. */
+ * joins the step's streams into the compute stream, no host wait (N ranks:
+ * then the dt exchange kernel gathers the step's max signal speeds). */
 int ts_hydro_finish_step(ts_hydro_ctx* ctx);
 
 /* ---- gravity ------------------------------------- */

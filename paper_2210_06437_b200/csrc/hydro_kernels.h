@@ -78,8 +78,9 @@ struct StageArgs {
     const double* gather_own;            // own gather half [push_n]
     double* amax_global;
     // P2P transport, fused halo exchange.  The n_boundary sub-grids with a
-    // foreign face neighbour are spread through the front of the launch
-    // (cta_bnd[cta] = their boundary slot b, -1 for interior CTAs).  Each
+    // foreign face neighbour (bnd_of[g] = their boundary slot b, -1 for
+    // interior sub-grids) are spread through the front of a batched launch,
+    // or come in any per-sub-grid launch of a drop-in step.  Each
     // stores its 3-deep output slabs straight into the proxy slots of the
     // peers' U^(k) buffers over NVLink (push_tbl[6 b + face] = {peer rank,
     // peer-local sub-grid} or {-1, -1}); the last one (halo_ctr) releases
@@ -88,7 +89,7 @@ struct StageArgs {
     // halo_wait_mask, >= halo_wait_seq) before reading proxies; interior CTAs
     // run meanwhile, so the wait is off the critical path.
     int n_boundary;
-    const int* cta_bnd;
+    const int* bnd_of;                   // [n_owned]
     const int2* push_tbl;                // nullptr: no push
     double* const* push_out;             // [world] peer's buffer of this stage's U^(k)
     // halo_ctr: one monotonic counter per stage slot (halo_seq % 3), never

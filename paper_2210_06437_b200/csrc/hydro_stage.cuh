@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     }
     __syncthreads();
 #endif
-    if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0) {
+    if (A.halo_wait_mask != 0ull && __ldg(A.bnd_of + g) >= 0) {
         // proxies of U^(k-1): pushed by the peers' previous-stage boundary CTAs
         // (released in their first wave, so this rarely spins)
         // one source rank per thread, in parallel
@@ -1158,7 +1158,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
             if (v != A.flow_wait_seq) chk_fail(A.check, 10u, h, (long long)(int)(v - A.flow_wait_seq));
         }
     }
-    if (A.halo_wait_mask != 0ull && __ldg(A.cta_bnd + blockIdx.x) >= 0 && t < 64 &&
+    if (A.halo_wait_mask != 0ull && __ldg(A.bnd_of + g) >= 0 && t < 64 &&
         ((A.halo_wait_mask >> t) & 1ull)) {
         // a peer may already have pushed its NEXT stage (into the other buffer
         // of the rotation: +1), never the one after (it needs this CTA's push)
@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     }
 #endif
     if (A.push_tbl != nullptr) {
-        const int b = __ldg(A.cta_bnd + blockIdx.x);
+        const int b = __ldg(A.bnd_of + g);
         if (b >= 0) halo_push<NF>(A, c.own, b);
     }
 

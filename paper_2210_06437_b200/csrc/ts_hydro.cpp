@@ -279,7 +279,7 @@ struct ts_hydro_ctx {
     int32_t* d_order = nullptr;       // launch order of the fused P2P stage: boundary spread through the front
     uint32_t* d_flow = nullptr;       // [3][n_owned] dataflow: last step seq that finished stage 1 / 2 / 3
     unsigned long long* d_cta_log = nullptr;  // [3][n_owned][4] diagnostic per-CTA timeline of the last step
-    int32_t* d_cta_bnd = nullptr;     // [n_owned] launch position -> boundary slot (-1: interior)
+    int32_t* d_bnd_of = nullptr;      // [n_owned] sub-grid -> boundary slot (-1: interior)
     int2* d_push_tbl = nullptr;       // [n_boundary][6] fused halo push targets
     long long* d_gid = nullptr;
     int2* d_send_entries = nullptr;
@@ -385,6 +385,14 @@ struct ts_hydro_ctx {
     std::vector<DropinLaunch> din_parked;
     std::vector<uint8_t> din_streams; // streams used by the open step
     cudaEvent_t ev_din = nullptr;     // stream-0 work before the step (upload, compute_dt, batched steps)
+    // N ranks (fused P2P halos): the step's halo seqs are din_xbase + stage;
+    // a boundary sub-grid's stage k is issued only after every boundary
+    // sub-grid's stage k-1 (its peers' stage k-1 waits for all of those)
+    uint32_t din_xbase = 0;
+    bool din_wait1 = false;           // stage 1 acquires the peers' pushes of U^n (else a copy-engine refresh ran)
+    uint32_t din_halo_target[4] = {0, 0, 0, 0};
+    int64_t din_bnd_issued[4] = {0, 0, 0, 0};
+    std::vector<int32_t> bnd_host;    // [n_owned] boundary slot (-1: interior)
 
     // stepping
     uint64_t steps_done = 0;
@@ -534,7 +542,7 @@ void free_mesh(ts_hydro_ctx* c) {
         for (auto& q : r)
             for (auto& t : q) dfree(c, &t);
     dfree(c, &c->d_scr_mask);
-    dfree(c, &c->d_cta_bnd);
+    dfree(c, &c->d_bnd_of);
     dfree(c, &c->d_push_tbl);
     dfree(c, &c->d_gid);
     dfree(c, &c->d_send_entries);
@@ -1235,7 +1243,7 @@ int do_step(ts_hydro_ctx* c) {
             }
             const int out_idx = stage == 1 ? 1 : (stage == 2 ? 2 : 0);
             a.n_boundary = (int)c->boundary.size();
-            a.cta_bnd = c->d_cta_bnd;
+            a.bnd_of = c->d_bnd_of;
             a.push_tbl = c->d_push_tbl;
             a.push_out = c->d_push_out + (size_t)out_idx * c->world;
             a.halo_flag = c->d_halo_flag;
@@ -1324,6 +1332,31 @@ int dropin_open(ts_hydro_ctx* c) {
     int rc = ensure_stream(c, 0, &s0);
     if (rc) return rc;
     if (c->ev_din == nullptr) TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_din, cudaEventDisableTiming));
+    if (c->world > 1) {
+        // the proxies of U^n: the peers' stage-3 pushes of the previous step,
+        // or (state replaced / first step) a copy-engine refresh behind
+        // everything on the compute stream
+        c->din_chained = false;
+        c->din_wait1 = c->halo_pushed;
+        if (!c->halo_pushed) {
+            cudaStream_t cs;
+            if ((rc = ensure_stream(c, 1, &cs))) return rc;
+            TS_CUDA(c, cudaEventRecord(c->ev_in, s0));
+            TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
+            if ((rc = exchange_on_comm(c, c->U[0]))) return rc;
+            TS_CUDA(c, cudaEventRecord(c->ev_halo, cs));
+            TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_halo, 0));
+        }
+        c->din_xbase = c->xseq;
+        for (int k = 1; k <= 3; ++k) {
+            const int slot = (int)((c->din_xbase + (uint32_t)k) % 3u);
+            c->halo_cnt[slot] += (uint32_t)c->boundary.size();
+            c->din_halo_target[k] = c->halo_cnt[slot];
+            c->din_bnd_issued[k] = 0;
+        }
+        c->bnd_host.assign((size_t)c->n_owned, -1);
+        for (size_t b = 0; b < c->boundary.size(); ++b) c->bnd_host[(size_t)c->boundary[b]] = (int32_t)b;
+    }
     if (!c->din_chained) {
         TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 1), 0, sizeof(double), s0));
         TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 2), 0, sizeof(double), s0));
@@ -1342,6 +1375,10 @@ int dropin_open(ts_hydro_ctx* c) {
 bool dropin_ready(const ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     if (L.stage == 1) return true;
     const uint8_t need = (uint8_t)(L.stage - 1);
+    if (c->world > 1 && c->din_bnd_issued[L.stage - 1] < (int64_t)c->boundary.size()) {
+        for (int32_t g : L.list)
+            if (c->bnd_host[(size_t)g] >= 0) return false;
+    }
     for (int32_t g : L.list) {
         if (c->din_issued[(size_t)g] < need) return false;
         for (int f = 0; f < 6; ++f) {
@@ -1359,9 +1396,28 @@ int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     const int stage = L.stage;
     const size_t n = (size_t)c->n_owned;
     tsh::StageArgs a = stage_args(c, stage);
-    a.amax_in = amax_slot(c, c->steps_done);
-    a.amax_n = 1;
+    a.amax_in = c->amax_src != nullptr ? c->amax_src : amax_slot(c, c->steps_done);
+    a.amax_n = c->amax_src != nullptr ? c->amax_n : 1;
     a.amax_out = amax_slot(c, c->steps_done + 1);
+    if (c->world > 1) {
+        // fused P2P halos, as the batched step (do_step): boundary sub-grids
+        // acquire the peers' slabs of U^(k-1) and push their own U^(k)
+        const int out_idx = stage == 1 ? 1 : (stage == 2 ? 2 : 0);
+        a.n_boundary = (int)c->boundary.size();
+        a.bnd_of = c->d_bnd_of;
+        a.push_tbl = c->d_push_tbl;
+        a.push_out = c->d_push_out + (size_t)out_idx * c->world;
+        a.halo_flag = c->d_halo_flag;
+        a.halo_flag_n = c->world;
+        a.halo_seq = c->din_xbase + (uint32_t)stage;
+        a.halo_ctr = c->d_ctr + 1 + (int)(a.halo_seq % 3u);
+        a.halo_target = c->din_halo_target[stage];
+        if (stage > 1 || c->din_wait1) {
+            a.halo_wait = reinterpret_cast<const unsigned int*>(c->d_flags);
+            a.halo_wait_mask = c->halo_recv_mask;
+            a.halo_wait_seq = a.halo_seq - 1u;
+        }
+    }
     a.flow_n = (int)c->n_owned;
     a.flow_seq = c->din_seq;
     a.flow_wait_seq = c->din_seq;
@@ -1408,7 +1464,10 @@ int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
         }
     }
     if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
-    for (int32_t g : L.list) c->din_issued[(size_t)g] = (uint8_t)stage;
+    for (int32_t g : L.list) {
+        c->din_issued[(size_t)g] = (uint8_t)stage;
+        if (c->world > 1 && c->bnd_host[(size_t)g] >= 0) ++c->din_bnd_issued[stage];
+    }
     if (stage == 3) c->din_done3 += (int64_t)m;
     if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
     c->din_streams[L.stream_id] = 1;
@@ -1443,6 +1502,7 @@ int mutating(ts_hydro_ctx* c) {
     if (c->din_open)
         return fail(c, TS_ESTATE, "a per-sub-grid step is open (launch stage 3 of every sub-grid, then ts_hydro_finish_step)");
     c->din_chained = false;
+    c->halo_pushed = false;  // the proxies no longer hold the peers' last push of this state
     return TS_OK;
 }
 
@@ -1860,7 +1920,7 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
         TS_CUDA(c, cudaMemset(c->d_flow, 0, 3 * (size_t)c->n_owned * sizeof(uint32_t)));
         TS_CUDA(c, cudaMemset(c->d_cnt3, 0, sizeof(uint32_t)));
     }
-    if (!rc) rc = dalloc(c, &c->d_cta_bnd, (size_t)c->n_owned);
+    if (!rc) rc = dalloc(c, &c->d_bnd_of, (size_t)c->n_owned);
     if (!rc) rc = dalloc(c, &c->d_gid, (size_t)c->n_owned);
     if (rc) return rc;
     TS_CUDA(c, h2d_sync(c->d_nbr, c->nbr_local.data(), c->nbr_local.size() * sizeof(int32_t)));
@@ -1913,20 +1973,19 @@ static int bind_mesh(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner, 
                 return la < lb;
             });
         }
-        std::vector<int32_t> order, bnd;
+        std::vector<int32_t> order, bnd((size_t)c->n_owned, -1);
         size_t bi = 0, ii = 0;
         while (bi < c->boundary.size() || ii < c->interior.size()) {
             const bool take_b = bi < c->boundary.size() && (ii >= c->interior.size() || order.size() % stride == 0);
             if (take_b) {
-                bnd.push_back((int32_t)bi);
+                bnd[(size_t)c->boundary[bi]] = (int32_t)bi;
                 order.push_back(c->boundary[bi++]);
             } else {
-                bnd.push_back(-1);
                 order.push_back(interior_order[ii++]);
             }
         }
         TS_CUDA(c, h2d_sync(c->d_order, order.data(), order.size() * sizeof(int32_t)));
-        TS_CUDA(c, h2d_sync(c->d_cta_bnd, bnd.data(), bnd.size() * sizeof(int32_t)));
+        TS_CUDA(c, h2d_sync(c->d_bnd_of, bnd.data(), bnd.size() * sizeof(int32_t)));
     }
     {
         std::vector<long long> gid(c->owned_gid.begin(), c->owned_gid.end());
@@ -2834,7 +2893,8 @@ int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_i
     if (stage < 1 || stage > 3) return fail(c, TS_EINVAL, "stage must be 1, 2 or 3");
     if (count <= 0 || owned_index == nullptr) return fail(c, TS_EINVAL, "empty sub-grid list");
     if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
-    if (c->world > 1) return fail(c, TS_ESTATE, "per-sub-grid launches are single-rank (use ts_hydro_step)");
+    if (c->world > 1 && !(c->p2p && c->halo_fused && c->d_push_tbl != nullptr))
+        return fail(c, TS_ESTATE, "per-sub-grid launches on N ranks need the fused P2P transport (ts_hydro_p2p_import)");
     if (c->amr) return fail(c, TS_ESTATE, "per-sub-grid launches are not available on an AMR mesh (use ts_hydro_step)");
     cudaSetDevice(c->dev);
     if (!c->din_open) {
@@ -3221,11 +3281,28 @@ int ts_hydro_finish_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
     }
     c->din_open = false;
-    c->din_chained = true;
+    c->din_chained = c->world == 1;
     c->cnt3_expect += (uint32_t)c->n_owned;  // every stage-3 CTA of the step counted into d_cnt3
+    c->amax_src = nullptr;
+    if (c->world > 1) {
+        // the next dt: every rank's stage-3 max, gathered by the dt kernel
+        // behind the step on the compute stream (as the batched step's)
+        const uint32_t push_seq = c->aseq + 1;
+        TS_CUDA(c, tsh::launch_dt_exchange(amax_slot(c, c->steps_done + 1),
+                                           c->d_push_gather + (size_t)(push_seq & 1) * c->world, c->d_push_flag,
+                                           c->world, c->rank, push_seq,
+                                           reinterpret_cast<const unsigned int*>(c->d_flags + c->world),
+                                           c->d_gather + (size_t)(push_seq & 1) * c->world, c->d_scal + 4,
+                                           c->h_clock + 1, c->wait_ns, s0));
+        c->launches++;
+        c->aseq = push_seq;
+        c->amax_src = c->d_scal + 4;
+        c->amax_n = 1;
+        c->xseq = c->din_xbase + 3u;
+        c->halo_pushed = true;
+    }
     c->steps_done++;
     c->dt_valid = true;  // the step's stage 3 reduced the next dt's signal speed on the device
-    c->amax_src = nullptr;
     return TS_OK;
 }
 

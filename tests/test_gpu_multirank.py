@@ -79,6 +79,19 @@ def test_two_ranks_on_one_gpu_bitwise_equal_to_single_rank(args, transport):
     assert "MULTIGPU OK" in r.stdout
 
 
+@pytest.mark.parametrize("order", ["stage", "grid"])
+@pytest.mark.parametrize("args", [["--dims", "4", "4", "4"], ["--dims", "3", "2", "4", "--periodic", "xyz", "--species", "2"]])
+def test_dropin_steps_across_ranks_bitwise_equal_to_single_rank(args, order):
+    """The per-sub-grid drop-in (ts_hydro_launch_stage) on two ranks: every
+    sub-grid's stage launched alone on a rotating stream, scrambled, no host
+    barrier; the boundary sub-grids' halos move by the fused in-kernel push;
+    batched steps before and after.  Bitwise equal to one rank, equal dt."""
+    extra = ["--same-device"] if _gpus() < 2 else []
+    r = _torchrun([*args, "--transport", "p2p", "--dropin", order, "--steps", "4", *extra], 600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout
+
+
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
 def test_mismatch_on_one_gpu_fails_instead_of_hanging(transport):
     if _gpus() < 1:

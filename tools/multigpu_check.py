@@ -37,6 +37,10 @@ def main():
     ap.add_argument("--amr", default="", choices=["", "lshape", "ref4"],
                     help="multi-rank coarse-fine AMR: an L-shaped refinement of a 4^3 box, or the reference's own "
                          "levels-4 build_mesh octree (tests/golden), dealt along the Morton curve")
+    ap.add_argument("--dropin", default="", choices=["", "stage", "grid"],
+                    help="per-sub-grid drop-in steps (ts_hydro_launch_stage) between batched ones: every "
+                         "sub-grid's launch on a rotating stream, scrambled, stage by stage (stage) or "
+                         "sub-grid by sub-grid (grid: the host parks what is not ready)")
     ap.add_argument("--mismatch", action="store_true",
                     help="rank 1 makes one stepping call too many: it must fail with TS_ECOMM, not hang")
     a = ap.parse_args()
@@ -84,11 +88,26 @@ def main():
                   flush=True)
         dist.destroy_process_group()
         return 0 if res.item() == H.TS_ECOMM else 1
-    # two calls: the first stage of each call refreshes the halos by a copy, the
-    # other stages take the slabs the peers' stage kernels pushed
-    dev.step(1)
-    if a.steps > 1:
-        dev.step(a.steps - 1)
+    if a.dropin:
+        # a batched step, then drop-in steps (the first takes the batched
+        # stage 3's pushes; the next ones each other's), then a batched one
+        dev.step(1)
+        n = n_owned
+        for step in range(max(a.steps - 2, 1)):
+            perm = [(k * 37 + step * 11 + 5) % n for k in range(n)] if n % 37 else list(range(n))[::-1]
+            order = ([(st, g) for st in (1, 2, 3) for g in perm] if a.dropin == "stage"
+                     else [(st, g) for g in perm for st in (1, 2, 3)])
+            for i, (st, g) in enumerate(order):
+                dev.launch_stage(st, [g], stream_id=1 + i % 12, guid=g)
+            dev.finish_step()
+        dev.step(1)
+        a.steps = max(a.steps - 2, 1) + 2
+    else:
+        # two calls: the first stage of each call refreshes the halos by a copy, the
+        # other stages take the slabs the peers' stage kernels pushed
+        dev.step(1)
+        if a.steps > 1:
+            dev.step(a.steps - 1)
     got = dev.download()
     dt = dev.last_dt()
     recs = [r for r in dev.flush_activity() if r.kind == "kernel"]
@@ -115,7 +134,7 @@ def main():
     if rank == 0:
         print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
               f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}"
-              + (" same-device" if a.same_device else ""), flush=True)
+              + (" same-device" if a.same_device else "") + (f" dropin={a.dropin}" if a.dropin else ""), flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 1 else 1
 
