@@ -282,7 +282,11 @@ int ts_hydro_download_gravity(ts_hydro_ctx* ctx, int64_t first, int64_t count, d
  * level 0), as in the reference's octree (build_mesh, workload.cpp:264-327).
  * A uniform mesh passes level 0 and ts_hydro_uniform_mesh's positions; an AMR
  * mesh its leaves' levels and positions.  Rebinding a mesh drops the tree.
- * Single rank. */
+ * N ranks: the leaves are every rank's sub-grids by global id (the mesh's own
+ * numbering); each solve all-gathers the densities over NCCL
+ * (ts_hydro_comm_init, next to a P2P transport if that carries the halos) and
+ * each rank evaluates its own sub-grids and the expansions of their
+ * ancestors — bitwise equal to one rank. */
 int ts_hydro_set_gravity_tree(ts_hydro_ctx* ctx, int64_t n_leaves, const int32_t* level, const int32_t* pos,
                               const int32_t* dims, double dx0);
 /* One solve of the current state's density on stream `stream_id` (after
@@ -306,7 +310,7 @@ int ts_hydro_gravity_kick(ts_hydro_ctx* ctx, double dt);
  * SSP-RK3 hydro step, the FMM on its result, the kick over that step's dt —
  * the reference's per-step order (3 hydro rounds, then the gravity launches,
  * workload.cpp:559-569) — all on the compute stream, no host round trip.
- * Needs ts_hydro_set_gravity_tree; single rank. */
+ * Needs ts_hydro_set_gravity_tree; collective on N ranks. */
 int ts_hydro_step_gravity(ts_hydro_ctx* ctx, uint64_t nsteps, double G, int32_t radius);
 /* The gravity tree of these leaves (ts_hydro_set_gravity_tree's arguments; no
  * context, no device): n_nodes always, the arrays when cap >= n_nodes — per

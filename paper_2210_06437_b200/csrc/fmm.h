@@ -61,7 +61,8 @@ std::string fmm_build_tree(int64_t n_leaves, const int32_t* level, const int32_t
 std::vector<FmmEntry> fmm_table(int radius, bool root, bool far_only);
 
 struct FmmArgs {
-    const double* U;     // state (field 0 = density), leaf sub-grid k at U + k nf 512
+    const double* U;     // densities: field 0 of row leaf[node] at U + leaf nf 512 (the state, or the
+                         // ranks' gathered densities with nf = 1)
     int nf;
     const int* depth;    // device copies of FmmTree's arrays
     const int* q;
@@ -69,6 +70,7 @@ struct FmmArgs {
     const int* parent;
     const int* child;
     const int* nb27;
+    const int* leaf_out;  // a leaf node's output row (owned index), -1 for a leaf another rank owns
     double* M;           // [n][4][512] moments (m, cx, cy, cz)
     double* L;           // [n_internal][10][512] local expansions (phi, g, T xx yy zz xy xz yz)
     double* out;         // [leaf sub-grid][4][512] (phi, gx, gy, gz)
@@ -76,7 +78,7 @@ struct FmmArgs {
     const FmmEntry* table;
     int n_table;
     int K;               // table reach: tile half-width of the leaf kernel
-    const int* list;     // node ids of the launch (blockIdx.x -> list[blockIdx.x]); nullptr: first + blockIdx.x
+    const int* list;     // node ids of the launch (list[first + block]); nullptr: first + block
     int first;
     int T;
     double dx0;

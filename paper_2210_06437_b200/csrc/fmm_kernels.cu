@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(NC) fmm_restrict_kernel(const __grid_constant_
 __global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant__ FmmArgs A) {
     __shared__ int nb[27];
     stamp_begin(A);
-    const int node = A.first + (int)blockIdx.y, t = threadIdx.x;
+    const int node = A.list != nullptr ? A.list[A.first + (int)blockIdx.y] : A.first + (int)blockIdx.y;
+    const int t = threadIdx.x;
     if (t < 27) nb[t] = A.nb27[27 * node + t];
     __syncthreads();
     const int d = A.depth[node];
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant_
 // loaded eight at a time and added in order.
 __global__ void __launch_bounds__(NC) fmm_m2l_combine_kernel(const __grid_constant__ FmmArgs A, int n_chunks) {
     stamp_begin(A);
-    const int node = A.first + (int)blockIdx.x, j = (int)blockIdx.y, t = threadIdx.x;
+    const int node = A.list != nullptr ? A.list[A.first + (int)blockIdx.x] : A.first + (int)blockIdx.x;
+    const int j = (int)blockIdx.y, t = threadIdx.x;
     const int d = A.depth[node];
     double acc = 0.0;
     if (d > 0) {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(NC / CPT) fmm_leaf_kernel(const __grid_constan
         const int I[3] = {8 * q[0] + x, 8 * q[1] + yc, 8 * q[2] + zc};
         double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6];
         if (d > 0) l2l(A, node, d, I, h, phi, g, T);
-        double* o = A.out + (size_t)A.leaf[node] * 4 * NC + lidx(x, yc, zc);
+        double* o = A.out + (size_t)A.leaf_out[node] * 4 * NC + lidx(x, yc, zc);
         o[0] = (phi + kphi * acc[c][0]) + racc[c][0];
         o[NC] = (g[0] + kg * acc[c][1]) + racc[c][1];
         o[2 * NC] = (g[1] + kg * acc[c][2]) + racc[c][2];

@@ -81,6 +81,7 @@ struct Nccl {
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -109,6 +110,7 @@ Nccl& nccl() {
         TS_SYM(Send, "ncclSend");
         TS_SYM(Recv, "ncclRecv");
         TS_SYM(AllReduce, "ncclAllReduce");
+        TS_SYM(AllGather, "ncclAllGather");
         TS_SYM(GroupStart, "ncclGroupStart");
         TS_SYM(GroupEnd, "ncclGroupEnd");
         TS_SYM(GetErrorString, "ncclGetErrorString");
@@ -262,7 +264,15 @@ struct ts_hydro_ctx {
     double* d_fmm_M = nullptr;    // [n][4][512]
     double* d_fmm_L = nullptr;    // [n_internal][10][512]
     double* d_fmm_part = nullptr;  // the root's chunk sums
-    int* d_fmm_lists = nullptr;   // p2p leaves, then p2m leaves
+    int* d_fmm_lists = nullptr;   // leaves to evaluate (p2p, p2p with refined edge / corner slots, p2m), then
+                                  // the refined nodes whose expansions they need, by depth
+    std::vector<int> fmm_m2l_first, fmm_m2l_count;  // per depth: the M2L nodes' range in the list buffer
+    int fmm_leaf_lists[3] = {0, 0, 0};               // counts of the three leaf lists
+    // N ranks: every rank gathers every leaf's density (NCCL all-gather) and
+    // evaluates its own leaves; leaf rows = owner * fmm_max_owned + owned index
+    int64_t fmm_max_owned = 0;
+    double* d_fmm_send = nullptr;  // [max_owned][512] own densities, packed
+    double* d_fmm_rho = nullptr;   // [world * max_owned][512] every rank's
     tsh::FmmEntry* d_fmm_tab[tsh::kFmmRMax + 1][2][2] = {};  // [R][root][far_only]
     int n_fmm_tab[tsh::kFmmRMax + 1][2][2] = {};
     double* d_scr_ring = nullptr;   // nf > 6: species accumulators, kScrK slots per SM id (StageArgs::scr_ring)
@@ -560,6 +570,8 @@ void free_mesh(ts_hydro_ctx* c) {
     dfree(c, &c->d_fmm_L);
     dfree(c, &c->d_fmm_lists);
     dfree(c, &c->d_fmm_part);
+    dfree(c, &c->d_fmm_send);
+    dfree(c, &c->d_fmm_rho);
     c->have_fmm = false;
     c->wave_ready = false;
     c->amr = false;
@@ -3014,13 +3026,37 @@ int ts_hydro_set_gravity_tree(ts_hydro_ctx* c, int64_t n_leaves, const int32_t* 
     if (rc) return rc;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     if (!c->have_mesh) return fail(c, TS_ESTATE, "no mesh bound (call ts_hydro_set_mesh first)");
-    if (c->world > 1) return fail(c, TS_ESTATE, "the gravity FMM is single-rank");
     if (level == nullptr || pos == nullptr || dims == nullptr) return fail(c, TS_EINVAL, "null tree arrays");
-    if (n_leaves != c->n_owned)
+    const bool multi = c->world > 1;
+    if (multi) {
+        if (c->comm == nullptr) return fail(c, TS_ESTATE, "gravity on N ranks gathers the densities over NCCL (ts_hydro_comm_init)");
+        if (n_leaves != (int64_t)c->mesh_owner.size())
+            return fail(c, TS_EINVAL, "on N ranks the tree's leaves are every rank's sub-grids, by global id");
+    } else if (n_leaves != c->n_owned) {
         return fail(c, TS_EINVAL, "the tree's leaves must be exactly the owned sub-grids (n_leaves != n_owned)");
+    }
     tsh::FmmTree t;
     const std::string err = tsh::fmm_build_tree(n_leaves, level, pos, dims, dx0, t);
     if (!err.empty()) return fail(c, TS_EINVAL, "gravity tree: " + err);
+    // density row and output row of every leaf
+    std::vector<int> row((size_t)n_leaves), out((size_t)n_leaves, -1);
+    int64_t max_owned = c->n_owned;
+    if (multi) {
+        std::vector<int64_t> cnt((size_t)c->world, 0);
+        std::vector<int64_t> idx((size_t)n_leaves);
+        for (int64_t k = 0; k < n_leaves; ++k) idx[(size_t)k] = cnt[(size_t)c->mesh_owner[(size_t)k]]++;
+        max_owned = *std::max_element(cnt.begin(), cnt.end());
+        for (int64_t k = 0; k < n_leaves; ++k) {
+            row[(size_t)k] = (int)(c->mesh_owner[(size_t)k] * max_owned + idx[(size_t)k]);
+            if (c->mesh_owner[(size_t)k] == c->rank) {
+                // owned sub-grids are stored in ascending global id: the owned index
+                if (c->owned_gid[(size_t)idx[(size_t)k]] != k) return fail(c, TS_ESTATE, "owned ids out of order");
+                out[(size_t)k] = (int)idx[(size_t)k];
+            }
+        }
+    } else {
+        for (int64_t k = 0; k < n_leaves; ++k) row[(size_t)k] = out[(size_t)k] = (int)k;
+    }
     cudaSetDevice(c->dev);
     rc = sync_all(c);
     if (rc) return rc;
@@ -3028,22 +3064,50 @@ int ts_hydro_set_gravity_tree(ts_hydro_ctx* c, int64_t n_leaves, const int32_t* 
     dfree(c, &c->d_fmm_M);
     dfree(c, &c->d_fmm_L);
     dfree(c, &c->d_fmm_lists);
+    dfree(c, &c->d_fmm_send);
+    dfree(c, &c->d_fmm_rho);
     c->have_fmm = false;
     const size_t n = (size_t)t.n();
-    std::vector<int> h(n * 41);  // SoA: depth | q (3n) | leaf | parent | child (8n) | nb27 (27n)
+    // SoA: depth | q (3n) | leaf row | parent | child (8n) | nb27 (27n) | leaf output row
+    std::vector<int> h(n * 42);
     std::copy(t.depth.begin(), t.depth.end(), h.begin());
     std::copy(t.q.begin(), t.q.end(), h.begin() + (ptrdiff_t)n);
-    std::copy(t.leaf.begin(), t.leaf.end(), h.begin() + (ptrdiff_t)(4 * n));
+    for (size_t i = 0; i < n; ++i) {
+        h[4 * n + i] = t.leaf[i] >= 0 ? row[(size_t)t.leaf[i]] : -1;
+        h[41 * n + i] = t.leaf[i] >= 0 ? out[(size_t)t.leaf[i]] : -1;
+    }
     std::copy(t.parent.begin(), t.parent.end(), h.begin() + (ptrdiff_t)(5 * n));
     std::copy(t.child.begin(), t.child.end(), h.begin() + (ptrdiff_t)(6 * n));
     std::copy(t.nb27.begin(), t.nb27.end(), h.begin() + (ptrdiff_t)(14 * n));
-    std::vector<int> lists(t.leaves_p2p);
-    lists.insert(lists.end(), t.leaves_p2p_restr.begin(), t.leaves_p2p_restr.end());
-    lists.insert(lists.end(), t.leaves_p2m.begin(), t.leaves_p2m.end());
+    // the leaves this rank evaluates, and the refined nodes on their paths to the root
+    std::vector<int> lists;
+    const std::vector<int>* ll[3] = {&t.leaves_p2p, &t.leaves_p2p_restr, &t.leaves_p2m};
+    std::vector<uint8_t> need(n, multi ? 0 : 1);
+    for (int k = 0; k < 3; ++k) {
+        c->fmm_leaf_lists[k] = 0;
+        for (int node : *ll[k]) {
+            if (out[(size_t)t.leaf[(size_t)node]] < 0) continue;
+            lists.push_back(node);
+            ++c->fmm_leaf_lists[k];
+            for (int p = t.parent[(size_t)node]; p >= 0 && !need[(size_t)p]; p = t.parent[(size_t)p]) need[(size_t)p] = 1;
+        }
+    }
+    c->fmm_m2l_first.assign((size_t)t.max_depth + 1, 0);
+    c->fmm_m2l_count.assign((size_t)t.max_depth + 1, 0);
+    for (int d = 0; d < t.max_depth; ++d) {
+        c->fmm_m2l_first[(size_t)d] = (int)lists.size();
+        for (int i = t.int_first[(size_t)d]; i < t.int_first[(size_t)d] + t.n_int[(size_t)d]; ++i)
+            if (need[(size_t)i]) lists.push_back(i);
+        c->fmm_m2l_count[(size_t)d] = (int)lists.size() - c->fmm_m2l_first[(size_t)d];
+    }
     if ((rc = dalloc(c, &c->d_fmm_int, h.size())) || (rc = dalloc(c, &c->d_fmm_M, n * 4 * kNC)) ||
         (rc = dalloc(c, &c->d_fmm_L, (size_t)std::max(t.n_internal, 1) * 10 * kNC)) ||
         (rc = dalloc(c, &c->d_fmm_lists, std::max<size_t>(lists.size(), 1))))
         return rc;
+    if (multi && ((rc = dalloc(c, &c->d_fmm_send, (size_t)max_owned * kNC)) ||
+                  (rc = dalloc(c, &c->d_fmm_rho, (size_t)c->world * max_owned * kNC))))
+        return rc;
+    c->fmm_max_owned = max_owned;
     if (c->d_fmm_part == nullptr && (rc = dalloc(c, &c->d_fmm_part, (size_t)tsh::kFmmSplitMax * 10 * kNC)))
         return rc;
     TS_CUDA(c, h2d_sync(c->d_fmm_int, h.data(), h.size() * sizeof(int)));
@@ -3130,12 +3194,25 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
     tsh::FmmArgs a{};
     a.U = c->U[0];
     a.nf = c->nf;
+    if (c->world > 1) {
+        // every rank's densities: field 0 of the owned sub-grids packed (a
+        // strided 2-D copy), then an all-gather; rows owner * max_owned + i
+        const size_t row_b = (size_t)kNC * sizeof(double);
+        if (c->n_owned > 0)
+            TS_CUDA(c, cudaMemcpy2DAsync(c->d_fmm_send, row_b, c->U[0], (size_t)c->nf * row_b, row_b,
+                                         (size_t)c->n_owned, cudaMemcpyDeviceToDevice, s));
+        TS_NCCL(c, nccl().AllGather(c->d_fmm_send, c->d_fmm_rho, (size_t)c->fmm_max_owned * kNC, ncclFloat64,
+                                    c->comm, s));
+        a.U = c->d_fmm_rho;
+        a.nf = 1;
+    }
     a.depth = c->d_fmm_int;
     a.q = c->d_fmm_int + n;
     a.leaf = c->d_fmm_int + 4 * n;
     a.parent = c->d_fmm_int + 5 * n;
     a.child = c->d_fmm_int + 6 * n;
     a.nb27 = c->d_fmm_int + 14 * n;
+    a.leaf_out = c->d_fmm_int + 41 * n;
     a.M = c->d_fmm_M;
     a.L = c->d_fmm_L;
     a.part = c->d_fmm_part;
@@ -3172,10 +3249,13 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
         // (Sedov 16^3, R = 2, depth 3's 512 nodes): 0.27 ms, against 0.37 for
         // one CTA per node walking its chunks and 0.35 for that with the
         // sources staged in 187 KB of shared memory
+        // (the refined nodes on this rank's leaves' paths to the root: all of
+        // them on one rank)
         const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
-        const int nn = t.n_int[(size_t)d];
+        const int nn = c->fmm_m2l_count[(size_t)d];
         const int batch = std::max(1, tsh::kFmmSplitMax / n_chunks);
-        const int first = t.int_first[(size_t)d];
+        const int first = c->fmm_m2l_first[(size_t)d];
+        a.list = c->d_fmm_lists;
         if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, nn, [&](int k) {
                  cudaError_t e = cudaSuccess;
                  for (int b = 0; b < k && e == cudaSuccess; b += batch) {
@@ -3185,6 +3265,7 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
                  return e;
              })))
             return rc;
+        a.list = nullptr;
     }
     // leaves: the root alone, or the p2p / p2m lists
     if (t.root_leaf >= 0) {
@@ -3198,15 +3279,12 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
         a.K = 2 * radius + 1;
         a.list = c->d_fmm_lists;
         a.first = 0;
-        if ((rc = launch(kNameP2P, (int)t.leaves_p2p.size(), [&](int k) { return tsh::launch_fmm_leaf(a, k, false, s); })))
-            return rc;
-        a.first = (int)t.leaves_p2p.size();
-        if ((rc = launch(kNameP2P, (int)t.leaves_p2p_restr.size(),
-                         [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); })))
-            return rc;
-        a.first += (int)t.leaves_p2p_restr.size();
-        if ((rc = launch(kNameP2M, (int)t.leaves_p2m.size(), [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); })))
-            return rc;
+        const int* nl = c->fmm_leaf_lists;
+        if ((rc = launch(kNameP2P, nl[0], [&](int k) { return tsh::launch_fmm_leaf(a, k, false, s); }))) return rc;
+        a.first = nl[0];
+        if ((rc = launch(kNameP2P, nl[1], [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); }))) return rc;
+        a.first += nl[1];
+        if ((rc = launch(kNameP2M, nl[2], [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); }))) return rc;
     }
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
     return TS_OK;
@@ -3228,6 +3306,7 @@ int do_gravity_kick(ts_hydro_ctx* c, double dt, bool last_dt) {
     TS_CUDA(c, tsh::launch_gravity_kick(c->U[0], c->nf, c->n_owned, c->d_grav, dt_dev, dt, stamp, c->sms, s));
     c->dt_valid = false;
     c->flow_chain = false;
+    c->halo_pushed = false;
     return TS_OK;
 }
 

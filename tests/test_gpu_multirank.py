@@ -92,6 +92,19 @@ def test_dropin_steps_across_ranks_bitwise_equal_to_single_rank(args, order):
     assert "MULTIGPU OK" in r.stdout
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("args", [["--dims", "4", "4", "4"], ["--dims", "3", "5", "2"]])
+def test_self_gravity_across_ranks_bitwise_equal_to_single_rank(args, transport):
+    """The FMM over the global tree on two GPUs (densities all-gathered over
+    NCCL, each rank evaluating its own leaves and their ancestors'
+    expansions), and hydro + self-gravity steps: bitwise equal to one rank."""
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs (NCCL refuses two ranks on one device)")
+    r = _torchrun([*args, "--transport", transport, "--gravity"], 600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout
+
+
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
 def test_mismatch_on_one_gpu_fails_instead_of_hanging(transport):
     if _gpus() < 1:

@@ -41,6 +41,9 @@ def main():
                     help="per-sub-grid drop-in steps (ts_hydro_launch_stage) between batched ones: every "
                          "sub-grid's launch on a rotating stream, scrambled, stage by stage (stage) or "
                          "sub-grid by sub-grid (grid: the host parks what is not ready)")
+    ap.add_argument("--gravity", action="store_true",
+                    help="self-gravity across the ranks (FMM over the global tree, densities all-gathered over "
+                         "NCCL): a solve and two hydro + gravity steps, against one rank")
     ap.add_argument("--mismatch", action="store_true",
                     help="rank 1 makes one stepping call too many: it must fail with TS_ECOMM, not hang")
     a = ap.parse_args()
@@ -67,7 +70,13 @@ def main():
         blobs = [None] * world
         dist.all_gather_object(blobs, dev.p2p_export())
         dev.p2p_import(blobs)
+        if a.gravity:  # the gravity gather runs over NCCL next to the P2P halos
+            uid = [H.CudaDevice.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            dev.comm_init(uid[0], world, rank)
     dev.init_random(2210)
+    if a.gravity:
+        return gravity_check(a, dev, cfg, rank, world)
     owned = dev.owned_ids()
     n_owned, n_proxy, n_interior = dev.local_counts()
     if a.mismatch:
@@ -135,6 +144,42 @@ def main():
         print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
               f" world={world} dims={a.dims} steps={a.steps} species={a.species} transport={a.transport}"
               + (" same-device" if a.same_device else "") + (f" dropin={a.dropin}" if a.dropin else ""), flush=True)
+    dist.destroy_process_group()
+    return 0 if flag.item() == 1 else 1
+
+
+def gravity_check(a, dev, cfg, rank, world):
+    """Self-gravity on N ranks: one FMM solve of the random state, then two
+    hydro + gravity steps; each rank's sub-grids bitwise equal to one rank."""
+    owned = dev.owned_ids()
+    dev.set_gravity_tree()
+    dev.gravity_fmm(G=1.0, radius=2)
+    g = dev.download_gravity()
+    dev.step_gravity(2, G=1.0, radius=2)
+    got = dev.download()
+    dt = dev.last_dt()
+    names = sorted({r.name for r in dev.flush_activity() if r.kind == "kernel"})
+    dev.close()
+    single = H.uniform_mesh(*a.dims, periodic=a.periodic, world=1)
+    ref = H.CudaDevice(cfg)
+    ref.set_mesh(single, 0)
+    ref.init_random(2210)
+    ref.set_gravity_tree()
+    ref.gravity_fmm(G=1.0, radius=2)
+    g_ref = ref.download_gravity()[owned]
+    ref.step_gravity(2, G=1.0, radius=2)
+    want = ref.download()[owned]
+    dt_ref = ref.last_dt()
+    ref.close()
+    ok = bool(np.array_equal(g, g_ref)) and bool(np.array_equal(got, want)) and dt == dt_ref
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    print(f"rank {rank}: gravity bitwise={np.array_equal(g, g_ref)} steps bitwise={np.array_equal(got, want)} "
+          f"dt={dt!r} kernels={names}", flush=True)
+    dist.barrier()
+    if rank == 0:
+        print(("MULTIGPU OK" if flag.item() == 1 else "MULTIGPU FAIL") +
+              f" gravity world={world} dims={a.dims} transport={a.transport}", flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 1 else 1
 
