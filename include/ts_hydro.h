@@ -248,8 +248,11 @@ int ts_hydro_launch_count(const ts_hydro_ctx* ctx, uint64_t* launches);
  * output's slabs into the peers' proxies, as the batched step does; a stage-k
  * launch holding a boundary sub-grid is issued once every boundary sub-grid
  * has issued stage k-1; the step's dt is reduced over the ranks when the step
- * closes.  Drop-in steps are collective like ts_hydro_step.  State-changing
- * calls fail with TS_ESTATE while a step is open. */
+ * closes.  Drop-in steps are collective like ts_hydro_step.  On an AMR mesh
+ * (single rank) a stage's proxy fill and the previous stage's reflux run once
+ * every leaf issued that previous stage, and every launch of the stage waits
+ * for them (events): the stages are barriers there, as the reflux needs.
+ * State-changing calls fail with TS_ESTATE while a step is open. */
 int ts_hydro_launch_stage(ts_hydro_ctx* ctx, int32_t stage, const int64_t* owned_index, int64_t count,
                           uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
 /* Close the open per-sub-grid step (every owned sub-grid launched stage 3):

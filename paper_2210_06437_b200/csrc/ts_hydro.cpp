@@ -403,6 +403,12 @@ struct ts_hydro_ctx {
     uint32_t din_halo_target[4] = {0, 0, 0, 0};
     int64_t din_bnd_issued[4] = {0, 0, 0, 0};
     std::vector<int32_t> bnd_host;    // [n_owned] boundary slot (-1: interior)
+    // AMR mesh: a stage's proxy fill needs every leaf's previous stage and the
+    // reflux every leaf's stage, so stage k of any leaf waits (event) for the
+    // reflux of k-1 and the fill of k, enqueued once every leaf issued k-1
+    int64_t din_count[4] = {0, 0, 0, 0};
+    cudaEvent_t ev_amr[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool din_amr_barrier[4] = {false, false, false, false};
 
     // stepping
     uint64_t steps_done = 0;
@@ -1369,6 +1375,20 @@ int dropin_open(ts_hydro_ctx* c) {
         c->bnd_host.assign((size_t)c->n_owned, -1);
         for (size_t b = 0; b < c->boundary.size(); ++b) c->bnd_host[(size_t)c->boundary[b]] = (int32_t)b;
     }
+    if (c->amr) {
+        c->din_chained = false;
+        for (int k = 0; k < 4; ++k) {
+            c->din_count[k] = 0;
+            c->din_amr_barrier[k] = false;
+            if (c->ev_amr[k] == nullptr) TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_amr[k], cudaEventDisableTiming));
+        }
+        if (c->amr_n_proxy > 0) {  // the proxies of U^n, behind everything on the compute stream
+            unsigned long long* stamp = nullptr;
+            if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrFill, 0, 0, &stamp))) return rc;
+            TS_CUDA(c, tsh::launch_amr_fill(c->U[0], c->nf, c->d_amr_proxy, c->amr_slab_fill ? c->d_amr_pmask : nullptr,
+                                            c->amr_n_proxy, stamp, s0));
+        }
+    }
     if (!c->din_chained) {
         TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 1), 0, sizeof(double), s0));
         TS_CUDA(c, cudaMemsetAsync(amax_slot(c, c->steps_done + 2), 0, sizeof(double), s0));
@@ -1386,6 +1406,7 @@ int dropin_open(ts_hydro_ctx* c) {
 
 bool dropin_ready(const ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     if (L.stage == 1) return true;
+    if (c->amr) return c->din_count[L.stage - 1] == c->n_owned;
     const uint8_t need = (uint8_t)(L.stage - 1);
     if (c->world > 1 && c->din_bnd_issued[L.stage - 1] < (int64_t)c->boundary.size()) {
         for (int32_t g : L.list)
@@ -1401,6 +1422,96 @@ bool dropin_ready(const ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     return true;
 }
 
+// The AMR barrier of stage k: the previous stage's reflux and this stage's
+// proxy fill on the compute stream behind every stream the step used.
+int amr_stage_barrier(ts_hydro_ctx* c, int stage) {
+    cudaStream_t s0;
+    int rc = ensure_stream(c, 0, &s0);
+    if (rc) return rc;
+    for (size_t id = 1; id < c->din_streams.size(); ++id) {
+        if (!c->din_streams[id]) continue;
+        TS_CUDA(c, cudaEventRecord(c->ev_in, c->streams[id]));
+        TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
+    }
+    const double* dt_ptr = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+    if (c->amr_n_rec > 0 && stage > 1) {
+        const tsh::StageArgs p = stage_args(c, stage - 1);
+        unsigned long long* stamp = nullptr;
+        if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrReflux, 0, 0, &stamp))) return rc;
+        if (c->d_amr_rf_slot != nullptr)
+            TS_CUDA(c, tsh::launch_amr_reflux_reg(p.Uout, c->nf, c->d_amr_level, c->amr_max_level, c->cfg.dx,
+                                                  c->d_amr_rec, c->amr_n_rec, c->d_amr_rf_slot, c->d_amr_rf_flux,
+                                                  stage - 1, dt_ptr, stamp, s0));
+        else
+            TS_CUDA(c, tsh::launch_amr_reflux(p.Uprev, p.Uout, c->nf, c->cfg.recon, c->cfg.gamma, c->cfg.p_floor,
+                                              c->d_nbr, c->d_amr_level, c->amr_max_level, c->cfg.dx, c->d_amr_rec,
+                                              c->amr_n_rec, stage - 1, dt_ptr, stamp, s0));
+    }
+    if (stage <= 3 && c->amr_n_proxy > 0) {
+        const tsh::StageArgs a = stage_args(c, stage);
+        unsigned long long* stamp = nullptr;
+        if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameAmrFill, 0, 0, &stamp))) return rc;
+        TS_CUDA(c, tsh::launch_amr_fill(const_cast<double*>(a.Uprev), c->nf, c->d_amr_proxy,
+                                        c->amr_slab_fill ? c->d_amr_pmask : nullptr, c->amr_n_proxy, stamp, s0));
+    }
+    if (stage <= 3) TS_CUDA(c, cudaEventRecord(c->ev_amr[stage], s0));
+    return TS_OK;
+}
+
+// A drop-in launch on an AMR mesh: stage-ordered by the barrier events (no
+// dataflow flags), every level in one launch (StageArgs::lvl_*), the flux
+// register as the batched step's.
+int dropin_issue_amr(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L, tsh::StageArgs a, cudaStream_t s) {
+    const int stage = L.stage;
+    int rc;
+    if (stage == 1) {
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_din, 0));
+        a.lead_g1 = 1;
+        a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
+    } else {
+        if (!c->din_amr_barrier[stage]) {
+            if ((rc = amr_stage_barrier(c, stage))) return rc;
+            c->din_amr_barrier[stage] = true;
+        }
+        TS_CUDA(c, cudaStreamWaitEvent(s, c->ev_amr[stage], 0));
+    }
+    if (c->d_amr_rf_slot != nullptr) {
+        a.rf_slot = c->d_amr_rf_slot;
+        a.rf_flux = c->d_amr_rf_flux;
+    }
+    a.lvl_n = c->amr_max_level + 1;
+    for (int lv = 0; lv <= c->amr_max_level; ++lv) {
+        a.lvl_first[lv] = (int)c->amr_level_first[(size_t)lv];
+        a.lvl_dx[lv] = std::ldexp(c->cfg.dx, c->amr_max_level - lv);
+    }
+    a.dx_upd = a.lvl_dx[0];
+    unsigned long long* stamp = nullptr;
+    if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)L.stream_id, L.guid, &stamp))) return rc;
+    a.stamp = stamp;
+    const size_t m = L.list.size();
+    if (m <= (size_t)tsh::StageArgs::kInlineList) {
+        a.list_inline_n = (int)m;
+        for (size_t k = 0; k < m; ++k) a.list_inline[k] = L.list[k];
+        TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)m, s, false));
+    } else {
+        for (size_t k = 0; k < m;) {
+            size_t e = k + 1;
+            while (e < m && L.list[e] == L.list[e - 1] + 1) ++e;
+            a.list_inline_n = 0;
+            a.first = L.list[k];
+            TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)(e - k), s, false));
+            k = e;
+        }
+    }
+    if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
+    for (int32_t g : L.list) c->din_issued[(size_t)g] = (uint8_t)stage;
+    c->din_count[stage] += (int64_t)m;
+    if (stage == 3) c->din_done3 += (int64_t)m;
+    if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
+    c->din_streams[L.stream_id] = 1;
+    return TS_OK;
+}
+
 int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     cudaStream_t s;
     int rc = ensure_stream(c, L.stream_id, &s);
@@ -1411,6 +1522,7 @@ int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     a.amax_in = c->amax_src != nullptr ? c->amax_src : amax_slot(c, c->steps_done);
     a.amax_n = c->amax_src != nullptr ? c->amax_n : 1;
     a.amax_out = amax_slot(c, c->steps_done + 1);
+    if (c->amr) return dropin_issue_amr(c, L, a, s);
     if (c->world > 1) {
         // fused P2P halos, as the batched step (do_step): boundary sub-grids
         // acquire the peers' slabs of U^(k-1) and push their own U^(k)
@@ -2907,7 +3019,8 @@ int ts_hydro_launch_stage(ts_hydro_ctx* c, int32_t stage, const int64_t* owned_i
     if (stream_id >= c->cfg.stream_count) return fail(c, TS_EINVAL, "invalid stream id");
     if (c->world > 1 && !(c->p2p && c->halo_fused && c->d_push_tbl != nullptr))
         return fail(c, TS_ESTATE, "per-sub-grid launches on N ranks need the fused P2P transport (ts_hydro_p2p_import)");
-    if (c->amr) return fail(c, TS_ESTATE, "per-sub-grid launches are not available on an AMR mesh (use ts_hydro_step)");
+    if (c->amr && (c->world > 1 || c->amr_max_level >= tsh::StageArgs::kMaxLevels))
+        return fail(c, TS_ESTATE, "per-sub-grid launches on an AMR mesh: single rank, < 8 levels (use ts_hydro_step)");
     cudaSetDevice(c->dev);
     if (!c->din_open) {
         if (stage != 1) return fail(c, TS_ESTATE, "a per-sub-grid step starts with stage 1");
@@ -3359,8 +3472,19 @@ int ts_hydro_finish_step(ts_hydro_ctx* c) {
         TS_CUDA(c, cudaEventRecord(c->ev_in, c->streams[id]));
         TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
     }
+    if (c->amr) {
+        // the last reflux, then the next dt's signal speed from the corrected
+        // state (as the batched AMR step)
+        if ((rc = amr_stage_barrier(c, 4))) return rc;
+        double* slot = amax_slot(c, c->steps_done + 1);
+        TS_CUDA(c, cudaMemsetAsync(slot, 0, sizeof(double), s0));
+        unsigned long long* stamp = nullptr;
+        if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameSignal, 0, 0, &stamp))) return rc;
+        TS_CUDA(c, tsh::launch_signal(c->U[0], c->nf, c->n_owned, c->cfg.gamma, c->cfg.p_floor, slot, stamp,
+                                      c->sms, s0));
+    }
     c->din_open = false;
-    c->din_chained = c->world == 1;
+    c->din_chained = c->world == 1 && !c->amr;
     c->cnt3_expect += (uint32_t)c->n_owned;  // every stage-3 CTA of the step counted into d_cnt3
     c->amax_src = nullptr;
     if (c->world > 1) {

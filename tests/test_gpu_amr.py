@@ -139,7 +139,7 @@ def test_amr_activity_records_and_refusals(hydro, tmp_path, monkeypatch):
     d = hydro.CudaDevice(hydro.HydroConfig(dx=DX))
     d.set_amr_mesh(m)
     d.upload(U0[:m.n_leaves])
-    with pytest.raises(hydro.TsError, match="AMR"):
+    with pytest.raises(hydro.TsError, match="no dt"):  # the drop-in step needs a dt first, as on uniform meshes
         d.launch_stage(1, [0])
     d.close()
 
@@ -212,3 +212,43 @@ def test_amr_checkpoint_restart_is_a_bitwise_continuation(hydro, tmp_path):
     got = r.download()
     r.close()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("order", ["stage", "grid"])
+def test_amr_dropin_steps_match_batched_bitwise(hydro, golden, order):
+    """The per-sub-grid drop-in on AMR meshes (an L-shaped refinement and the
+    reference's own 4-level build_mesh octree): every leaf's stage launched
+    alone on a rotating stream in a scrambled order — the proxy fill and the
+    reflux between the stages come in behind every leaf's previous stage —
+    bitwise equal to the batched AMR steps, equal dt."""
+    vec, _ = golden
+    ref_mesh = max(vec["build_mesh"], key=lambda e: len(e["level"]))
+    cases = [(amr.amr_mesh(4, 4, 4, L_SHAPE), DX, (0.625, 0.625, 0.5)),
+             (amr.from_reference_mesh(ref_mesh["level"], ref_mesh["pos"]), None, (0.4, 0.55, 0.5))]
+    for m, dx, centre in cases:
+        dx = dx or 1.0 / (8 << m.max_level)
+        U0 = amr.ic_blast(m, 6, dx, width=0.08, centre=centre, drift=(0.3, -0.1, 0.2))
+        r = hydro.CudaDevice(hydro.HydroConfig(dx=dx))
+        r.set_amr_mesh(m)
+        r.upload(U0[:m.n_leaves])
+        r.step(3)
+        want, dt_want = r.download(), r.last_dt()
+        r.close()
+        d = hydro.CudaDevice(hydro.HydroConfig(dx=dx))
+        d.set_amr_mesh(m)
+        d.upload(U0[:m.n_leaves])
+        d.compute_dt()
+        n = m.n_leaves
+        for step in range(3):
+            perm = [(k * 37 + step * 11 + 5) % n for k in range(n)] if n % 37 else list(range(n))[::-1]
+            launches = ([(st, g) for st in (1, 2, 3) for g in perm] if order == "stage"
+                        else [(st, g) for g in perm for st in (1, 2, 3)])
+            for i, (st, g) in enumerate(launches):
+                d.launch_stage(st, [g], stream_id=1 + i % 16, guid=g)
+            d.finish_step()
+        got, dt = d.download(), d.last_dt()
+        names = {r.name for r in d.flush_activity()}
+        d.close()
+        assert dt == dt_want
+        assert np.array_equal(got, want), f"leaves={n}: drop-in differs from the batched AMR steps"
+        assert {"amr_ghost_fill_kernel", "amr_reflux_kernel", "hydro_stage3_kernel"} <= names
