@@ -40,6 +40,8 @@ std::string fmm_build_tree(int64_t n_leaves, const int32_t* level, const int32_t
     for (int64_t k = 0; k < n_leaves; ++k) {
         const int l = level[k];
         if (l < 0 || l > 16) return "leaf levels must be 0..16";
+        for (int a = 0; a < 3; ++a)  // node keys hold 20 bits per coordinate
+            if (((int64_t)dims[a] << l) > (1 << 20)) return "more than 2^20 sub-grids along an axis at some level";
         for (int a = 0; a < 3; ++a)
             if (pos[3 * k + a] < 0 || (int64_t)pos[3 * k + a] >= ((int64_t)dims[a] << l))
                 return "leaf " + std::to_string(k) + " lies outside the domain";
@@ -59,7 +61,7 @@ std::string fmm_build_tree(int64_t n_leaves, const int32_t* level, const int32_t
     }
     // a leaf that is also an ancestor of another leaf: overlapping leaves
     for (const Tmp& n : tmp)
-        if (n.leaf >= 0 && n.d < 40) {
+        if (n.leaf >= 0) {
             for (int c = 0; c < 8; ++c)
                 if (idx.count(key(n.d + 1, 2 * n.x + (c & 1), 2 * n.y + ((c >> 1) & 1), 2 * n.z + (c >> 2))))
                     return "leaf " + std::to_string(n.leaf) + " overlaps finer leaves";
