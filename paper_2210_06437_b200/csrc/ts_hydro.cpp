@@ -1422,6 +1422,38 @@ bool dropin_ready(const ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
     return true;
 }
 
+// The launch(es) of a drop-in list — by value in the parameters (<= 32
+// sub-grids) or as runs of consecutive indices, one launch per run — and the
+// step's bookkeeping.
+int dropin_launch_list(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L, tsh::StageArgs a, cudaStream_t s) {
+    const int stage = L.stage;
+    const size_t m = L.list.size();
+    if (m <= (size_t)tsh::StageArgs::kInlineList) {
+        a.list_inline_n = (int)m;
+        for (size_t k = 0; k < m; ++k) a.list_inline[k] = L.list[k];
+        TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)m, s, false));
+    } else {
+        for (size_t k = 0; k < m;) {
+            size_t e = k + 1;
+            while (e < m && L.list[e] == L.list[e - 1] + 1) ++e;
+            a.list_inline_n = 0;
+            a.first = L.list[k];
+            TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)(e - k), s, false));
+            k = e;
+        }
+    }
+    if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
+    for (int32_t g : L.list) {
+        c->din_issued[(size_t)g] = (uint8_t)stage;
+        if (c->world > 1 && c->bnd_host[(size_t)g] >= 0) ++c->din_bnd_issued[stage];
+    }
+    c->din_count[stage] += (int64_t)m;
+    if (stage == 3) c->din_done3 += (int64_t)m;
+    if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
+    c->din_streams[L.stream_id] = 1;
+    return TS_OK;
+}
+
 // The AMR barrier of stage k: the previous stage's reflux and this stage's
 // proxy fill on the compute stream behind every stream the step used.
 int amr_stage_barrier(ts_hydro_ctx* c, int stage) {
@@ -1488,28 +1520,7 @@ int dropin_issue_amr(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L, tsh::
     unsigned long long* stamp = nullptr;
     if ((rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)L.stream_id, L.guid, &stamp))) return rc;
     a.stamp = stamp;
-    const size_t m = L.list.size();
-    if (m <= (size_t)tsh::StageArgs::kInlineList) {
-        a.list_inline_n = (int)m;
-        for (size_t k = 0; k < m; ++k) a.list_inline[k] = L.list[k];
-        TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)m, s, false));
-    } else {
-        for (size_t k = 0; k < m;) {
-            size_t e = k + 1;
-            while (e < m && L.list[e] == L.list[e - 1] + 1) ++e;
-            a.list_inline_n = 0;
-            a.first = L.list[k];
-            TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)(e - k), s, false));
-            k = e;
-        }
-    }
-    if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
-    for (int32_t g : L.list) c->din_issued[(size_t)g] = (uint8_t)stage;
-    c->din_count[stage] += (int64_t)m;
-    if (stage == 3) c->din_done3 += (int64_t)m;
-    if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
-    c->din_streams[L.stream_id] = 1;
-    return TS_OK;
+    return dropin_launch_list(c, L, a, s);
 }
 
 int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
@@ -1564,38 +1575,12 @@ int dropin_issue(ts_hydro_ctx* c, const ts_hydro_ctx::DropinLaunch& L) {
         }
     }
     if (stage == 3) a.cnt_done = c->d_cnt3;
-    // the sub-grid list: by value in the launch parameters, or as runs of
-    // consecutive indices (first + blockIdx.x), one launch per run
     unsigned long long* stamp = nullptr;
     rc = begin_launch(c, TS_ACTIVITY_KERNEL, kNameStage[stage], (int32_t)L.stream_id, L.guid, &stamp);
     if (rc) return rc;
     a.stamp = stamp;
     a.list = nullptr;
-    const size_t m = L.list.size();
-    if (m <= (size_t)tsh::StageArgs::kInlineList) {
-        a.list_inline_n = (int)m;
-        for (size_t k = 0; k < m; ++k) a.list_inline[k] = L.list[k];
-        TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)m, s, false));
-    } else {
-        size_t k = 0;
-        while (k < m) {
-            size_t e = k + 1;
-            while (e < m && L.list[e] == L.list[e - 1] + 1) ++e;
-            a.list_inline_n = 0;
-            a.first = L.list[k];
-            TS_CUDA(c, tsh::launch_stage(a, c->nf, c->cfg.recon, stage, (int)(e - k), s, false));
-            k = e;
-        }
-    }
-    if (L.done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{L.done, L.user, nullptr}));
-    for (int32_t g : L.list) {
-        c->din_issued[(size_t)g] = (uint8_t)stage;
-        if (c->world > 1 && c->bnd_host[(size_t)g] >= 0) ++c->din_bnd_issued[stage];
-    }
-    if (stage == 3) c->din_done3 += (int64_t)m;
-    if (L.stream_id >= c->din_streams.size()) c->din_streams.resize(L.stream_id + 1, 0);
-    c->din_streams[L.stream_id] = 1;
-    return TS_OK;
+    return dropin_launch_list(c, L, a, s);
 }
 
 // Issue every parked launch whose producers have been issued, until none is
