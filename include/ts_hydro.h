@@ -269,7 +269,9 @@ int ts_hydro_finish_step(ts_hydro_ctx* ctx);
  * mesh) — oracle/hydro_oracle.h orc_gravity_p2p, bitwise.  (The whole
  * solve, near and far field, is ts_hydro_gravity_fmm below.)  owned_index == NULL or
  * count <= 0: every owned sub-grid.  Runs after everything on the compute
- * stream; single rank, uniform mesh, not while a per-sub-grid step is open.
+ * stream; anything that later replaces or steps the state (steps, kicks,
+ * uploads, a drop-in step) waits for it; single rank, uniform mesh, not while
+ * a per-sub-grid step is open.
  * Activity record name "p2p_kernel". */
 int ts_hydro_gravity_p2p(ts_hydro_ctx* ctx, double G, int32_t radius, const int64_t* owned_index, int64_t count,
                          uint32_t stream_id, uint64_t correlation_guid, ts_done_fn done, void* user);
@@ -293,7 +295,7 @@ int ts_hydro_download_gravity(ts_hydro_ctx* ctx, int64_t first, int64_t count, d
 int ts_hydro_set_gravity_tree(ts_hydro_ctx* ctx, int64_t n_leaves, const int32_t* level, const int32_t* pos,
                               const int32_t* dims, double dx0);
 /* One solve of the current state's density on stream `stream_id` (after
- * everything on the compute stream): monopoles about the centre of mass,
+ * everything on the compute stream; later state changes wait for it): monopoles about the centre of mass,
  * first-order local expansions, interaction radius `radius` (1..3 cells: a
  * cell interacts directly with the cells within `radius`, and with its
  * parent's near cells' children beyond it).  Output: ts_hydro_download_gravity.

@@ -257,6 +257,7 @@ struct ts_hydro_ctx {
     double* U[3] = {nullptr, nullptr, nullptr};
     unsigned long long* d_check = nullptr;  // [5] self-check failures (TS_CHECK builds write it)
     double* d_grav = nullptr;               // [n_owned][4][512] gravity P2P output (phi, gx, gy, gz)
+    std::vector<uint8_t> grav_streams;      // streams with gravity work not yet joined into the compute stream
     // gravity FMM (fmm.h): the octree of the owned sub-grids and its device copy
     bool have_fmm = false;
     tsh::FmmTree fmm;
@@ -1344,11 +1345,14 @@ int do_step(ts_hydro_ctx* c) {
 // drop-in step (no flags / stage-3 count on the device for it), dt comes from
 // the stream-ordered signal speed and the max slots this step and the next
 // accumulate into are zeroed here.
+int join_gravity(ts_hydro_ctx* c);
+
 int dropin_open(ts_hydro_ctx* c) {
     if (!c->dt_valid) return fail(c, TS_ESTATE, "no dt (call ts_hydro_compute_dt first)");
     cudaStream_t s0;
     int rc = ensure_stream(c, 0, &s0);
     if (rc) return rc;
+    if ((rc = join_gravity(c))) return rc;  // the step rewrites U^n in stage 3
     if (c->ev_din == nullptr) TS_CUDA(c, cudaEventCreateWithFlags(&c->ev_din, cudaEventDisableTiming));
     if (c->world > 1) {
         // the proxies of U^n: the peers' stage-3 pushes of the previous step,
@@ -1607,9 +1611,31 @@ int dropin_pump(ts_hydro_ctx* c) {
 
 // Entry points that replace or step the state: not while a drop-in step is
 // open; afterwards the next drop-in step starts stream-ordered.
+// Gravity launches on other streams read the state (and write d_grav): join
+// them into the compute stream before anything there replaces or steps it.
+int join_gravity(ts_hydro_ctx* c) {
+#ifdef TS_NO_GRAVITY_JOIN  // diagnostic builds only: shows the ordering test catching the race
+    return c == nullptr ? TS_EINVAL : TS_OK;
+#endif
+    cudaStream_t s0 = nullptr;
+    for (size_t id = 1; id < c->grav_streams.size(); ++id) {
+        if (!c->grav_streams[id]) continue;
+        if (s0 == nullptr) {
+            cudaSetDevice(c->dev);
+            int rc = ensure_stream(c, 0, &s0);
+            if (rc) return rc;
+        }
+        TS_CUDA(c, cudaEventRecord(c->ev_in, c->streams[id]));
+        TS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
+        c->grav_streams[id] = 0;
+    }
+    return TS_OK;
+}
+
 int mutating(ts_hydro_ctx* c) {
     if (c->din_open)
         return fail(c, TS_ESTATE, "a per-sub-grid step is open (launch stage 3 of every sub-grid, then ts_hydro_finish_step)");
+    if (int rc = join_gravity(c)) return rc;
     c->din_chained = false;
     c->halo_pushed = false;  // the proxies no longer hold the peers' last push of this state
     return TS_OK;
@@ -3094,6 +3120,8 @@ int ts_hydro_gravity_p2p(ts_hydro_ctx* c, double G, int32_t radius, const int64_
         }
     }
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    if (stream_id >= c->grav_streams.size()) c->grav_streams.resize(stream_id + 1, 0);
+    c->grav_streams[stream_id] = 1;
     return TS_OK;
 }
 
@@ -3385,6 +3413,8 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
         if ((rc = launch(kNameP2M, nl[2], [&](int k) { return tsh::launch_fmm_leaf(a, k, true, s); }))) return rc;
     }
     if (done != nullptr) TS_CUDA(c, cudaLaunchHostFunc(s, done_host, new DoneThunk{done, user, nullptr}));
+    if (stream_id >= c->grav_streams.size()) c->grav_streams.resize(stream_id + 1, 0);
+    c->grav_streams[stream_id] = 1;
     return TS_OK;
 }
 

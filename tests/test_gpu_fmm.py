@@ -224,3 +224,23 @@ def test_fmm_full_size_sedov_and_amr_match_oracle(hydro, oracle_lib):
     want = oracle_lib.gravity_fmm(6, a.level, a.pos, a.dims, 2 * dx, U0, radius=2, G=1.3)
     assert np.array_equal(got, want)
     assert {"p2p_kernel", "p2m_kernel", "multipole_kernel", "multipole_root_kernel"} <= {r.name for r in recs}
+
+
+def test_gravity_on_another_stream_is_ordered_before_the_next_step(hydro, oracle_lib):
+    """A solve issued on stream 7 reads U^n; the step issued right after it on
+    the compute stream rewrites U^n in stage 3 — it must wait for the solve
+    (the join of the gravity streams), so the field is the pre-step state's."""
+    m = hydro.uniform_mesh(16, 16, 16, order="row")
+    dx = 1.0 / 128
+    d = hydro.CudaDevice(hydro.HydroConfig(dx=dx))
+    d.set_mesh(m)
+    d.upload(hydro.ic_fill(d.config, "sedov", m, np.arange(m.n)))
+    d.step(1)
+    U = d.download()
+    d.set_gravity_tree()
+    d.gravity_fmm(G=1.0, radius=2, stream_id=7)
+    d.step(1)  # no host wait in between
+    got = d.download_gravity()
+    d.close()
+    want = oracle_lib.gravity_fmm(6, np.zeros(m.n, np.int32), m.pos, m.dims, dx, U, radius=2, G=1.0)
+    assert np.array_equal(got, want)
