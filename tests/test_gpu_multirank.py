@@ -32,11 +32,11 @@ def _port():
     return p
 
 
-def _torchrun(script_args, timeout):
-    """torchrun world 2 on 127.0.0.1; a rendezvous port taken between picking
-    and binding it (EADDRINUSE) is retried with a fresh one."""
+def _torchrun(script_args, timeout, nproc=2):
+    """torchrun world `nproc` on 127.0.0.1; a rendezvous port taken between
+    picking and binding it (EADDRINUSE) is retried with a fresh one."""
     for _ in range(3):
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
                os.path.join(ROOT, "tools", "multigpu_check.py"), *script_args]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
@@ -103,6 +103,17 @@ def test_self_gravity_across_ranks_bitwise_equal_to_single_rank(args, transport)
     r = _torchrun([*args, "--transport", transport, "--gravity"], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
+
+
+@pytest.mark.parametrize("extra", [["--transport", "p2p"], ["--transport", "p2p-ce"],
+                                   ["--transport", "p2p", "--dropin", "grid"]])
+def test_eight_ranks_on_one_gpu_bitwise_equal_to_single_rank(extra):
+    """World 8 — the driver's largest scaling run — as eight processes sharing
+    one GPU through CUDA IPC: every peer mask, flag array and push table at
+    eight ranks, batched and drop-in steps, bitwise equal to one rank."""
+    r = _torchrun(["--dims", "4", "4", "8", *extra, "--same-device"], 600, nproc=8)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK world=8" in r.stdout
 
 
 @pytest.mark.parametrize("transport", ["p2p", "p2p-ce"])
