@@ -253,7 +253,7 @@ static void reconstruct(int recon, const double* q, double* uL, double* uR) {
 /* Physical flux of one face state along `axis` plus its normal velocity and
  * local signal speed |v_n| + c.  Ideal gas, pressure floor. */
 static void side_flux(const orc_params* p, int axis, const double* u, double* f, double* vn,
-                      double* a) {
+                      double* c2) {
     const double rho = u[0], sx = u[1], sy = u[2], sz = u[3], E = u[4];
     const double inv = 1.0 / rho;
     const double vx = sx * inv, vy = sy * inv, vz = sz * inv;
@@ -264,9 +264,8 @@ static void side_flux(const orc_params* p, int axis, const double* u, double* f,
     const double ke2 = fma(s3[axis], v3[axis], fma(s3[t1], v3[t1], s3[t2] * v3[t2]));
     double pr = (p->gamma - 1.0) * fma(-0.5, ke2, E);
     pr = fmax(pr, p->p_floor);
-    const double c = sqrt((p->gamma * pr) * inv);
     const double v = v3[axis];
-    *a = fabs(v) + c;
+    *c2 = (p->gamma * pr) * inv; /* squared sound speed (gamma p / rho) */
     *vn = v;
     f[0] = u[1 + axis];
     f[1] = sx * v;
@@ -278,10 +277,13 @@ static void side_flux(const orc_params* p, int axis, const double* u, double* f,
 }
 
 static void kt_flux(const orc_params* p, int axis, const double* uL, const double* uR, double* F) {
-    double fL[16], fR[16], vL, vR, aL, aR;
-    side_flux(p, axis, uL, fL, &vL, &aL);
-    side_flux(p, axis, uR, fR, &vR, &aR);
-    const double a = fmax(aL, aR);
+    double fL[16], fR[16], vL, vR, c2L, c2R;
+    side_flux(p, axis, uL, fL, &vL, &c2L);
+    side_flux(p, axis, uR, fR, &vR, &c2R);
+    /* Davis wave-speed bound max(|v_L|, |v_R|) + max(c_L, c_R); sqrt is
+     * monotone and correctly rounded, so sqrt(max(c2_L, c2_R)) is exactly
+     * max(c_L, c_R) with one square root per face (DESIGN.md §2 item 3) */
+    const double a = fmax(fabs(vL), fabs(vR)) + sqrt(fmax(c2L, c2R));
     for (int k = 0; k < p->nf; ++k) F[k] = 0.5 * fma(-a, uR[k] - uL[k], fL[k] + fR[k]);
 }
 

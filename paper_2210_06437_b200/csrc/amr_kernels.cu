@@ -138,7 +138,7 @@ struct FluxParams {
     double gamma, p_floor;
 };
 
-__device__ void o_side_flux(const FluxParams& p, int axis, const double* u, double* f, double* a) {
+__device__ void o_side_flux(const FluxParams& p, int axis, const double* u, double* f, double* vn, double* c2) {
     const double rho = u[0], sx = u[1], sy = u[2], sz = u[3], E = u[4];
     const double inv = 1.0 / rho;
     const double vx = sx * inv, vy = sy * inv, vz = sz * inv;
@@ -147,9 +147,9 @@ __device__ void o_side_flux(const FluxParams& p, int axis, const double* u, doub
     const double ke2 = fma(s3[axis], v3[axis], fma(s3[t1], v3[t1], s3[t2] * v3[t2]));
     double pr = (p.gamma - 1.0) * fma(-0.5, ke2, E);
     pr = fmax(pr, p.p_floor);
-    const double c = sqrt((p.gamma * pr) * inv);
     const double v = v3[axis];
-    *a = fabs(v) + c;
+    *c2 = (p.gamma * pr) * inv;
+    *vn = v;
     f[0] = u[1 + axis];
     f[1] = sx * v;
     f[2] = sy * v;
@@ -187,14 +187,14 @@ __device__ double o_pencil_value(int nf, const int* nbr, const double* U, int g,
 
 __device__ void o_face_flux(const FluxParams& p, const int* nbr, const double* U, int g, int axis, int a, int b,
                             int j, double* F) {
-    double w[6], sL[kMaxNf], sR[kMaxNf], fL[kMaxNf], fR[kMaxNf], aL, aR;
+    double w[6], sL[kMaxNf], sR[kMaxNf], fL[kMaxNf], fR[kMaxNf], vL, vR, c2L, c2R;
     for (int f = 0; f < p.nf; ++f) {
         for (int k = 0; k < 6; ++k) w[k] = o_pencil_value(p.nf, nbr, U, g, f, axis, a, b, j + k - 3);
         o_face_states(p.recon, w, &sL[f], &sR[f]);
     }
-    o_side_flux(p, axis, sL, fL, &aL);
-    o_side_flux(p, axis, sR, fR, &aR);
-    const double am = fmax(aL, aR);
+    o_side_flux(p, axis, sL, fL, &vL, &c2L);
+    o_side_flux(p, axis, sR, fR, &vR, &c2R);
+    const double am = fmax(fabs(vL), fabs(vR)) + sqrt(fmax(c2L, c2R));
     for (int k = 0; k < p.nf; ++k) F[k] = 0.5 * fma(-am, sR[k] - sL[k], fL[k] + fR[k]);
 }
 

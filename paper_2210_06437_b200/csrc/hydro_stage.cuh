@@ -44,6 +44,10 @@ struct Lanes {
     static constexpr bool pair = TS_PAIR == 2 ? (NF > 6) : (TS_PAIR == 1);
     static constexpr int threads = 64 * (pair ? 2 : 1);
     static constexpr int min_blocks = pair ? 4 : 6;
+    // launch-bounds hint of the single-lane PPM march: 5 lets ptxas schedule
+    // under a 204-register cap; it still allocates 168, so 6 CTAs stay
+    // resident (measured same box: +1.2 %, Sedov 16^3)
+    static constexpr int min_blocks_ppm = pair ? 4 : 5;
 };
 constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 // PPM: reload the retiring cell's U^(k-1) from L1 (it was loaded two faces
@@ -55,6 +59,23 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 
 #ifndef TS_PREFETCH
 #define TS_PREFETCH 1
+#endif
+#ifndef TS_SMEM_FP
+#define TS_SMEM_FP 0
+#endif
+// sweeps (bit = mode) whose face march is unrolled by 2 regardless of FaceUnroll
+#ifndef TS_PF_AHEAD
+#define TS_PF_AHEAD 0
+#endif
+#ifndef TS_PF_SPAN
+#define TS_PF_SPAN 1
+#endif
+#ifndef TS_UNROLL_MODES
+#define TS_UNROLL_MODES 0
+#endif
+// Preferred shared-memory carveout (percent) of the stage kernels; -1: driver default.
+#ifndef TS_CARVEOUT
+#define TS_CARVEOUT -1
 #endif
 // U^n of the retiring cell (stages 2, 3, z sweep): loaded at the top of the
 // face that retires it (not carried across faces: 12 fewer loop-carried
@@ -91,9 +112,9 @@ constexpr int kFaces = N + 1;
 
 // Resident CTAs per SM the register allocation is sized for (tuning knob).
 #ifdef TS_MINB
-#define TS_MINB_FOR(NF) TS_MINB
+#define TS_MINB_FOR(NF, RECON) TS_MINB
 #else
-#define TS_MINB_FOR(NF) (Lanes<NF>::min_blocks)
+#define TS_MINB_FOR(NF, RECON) (RECON == 0 ? Lanes<NF>::min_blocks_ppm : Lanes<NF>::min_blocks)
 #endif
 #ifndef TS_LAZY_DT
 #define TS_LAZY_DT 1
@@ -123,7 +144,10 @@ struct StageSmem {
     // so the CTA's shared memory stays small enough for 4 resident CTAs.
     static constexpr int dU = (NF > kFA ? kFA : NF) * NC;
     static constexpr int cache = NF > kFA ? kFaces * 3 * kPencils : 0;  // (vL, vR, a) per face
-    static constexpr int doubles = dU + cache;
+    // TS_SMEM_FP: the previous face's fluxes of the single-lane march, one
+    // private slot per (field, pencil) instead of 12 loop-carried registers
+    static constexpr int fp = (TS_SMEM_FP && !Lanes<NF>::pair) ? kFA * kPencils : 0;
+    static constexpr int doubles = dU + cache + fp;
 };
 
 // TS_TMA: the own sub-grid's U^(k-1) (the 6 marched fields) is staged into
@@ -372,6 +396,7 @@ struct StageCtx {
     double* __restrict__ dU;     // shared accumulator
 #endif
     double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
+    double* __restrict__ fps;    // TS_SMEM_FP: previous-face flux slots [field][pencil]
     size_t own;                  // element offset of the sub-grid's field 0
     double dtdx;                 // 0.5 dt/dx: fluxes are carried doubled (kt2)
     EosParams e;
@@ -462,9 +487,8 @@ __device__ __forceinline__ void kt_face(const EosParams& e, const double (&uL)[k
     const double keR = fma(uR[1], vR, fma(uR[2], uR[2] * invR, uR[3] * (uR[3] * invR)));
     const double pL = dmax(e.gm1 * fma(-0.5, keL, uL[4]), e.p_floor);
     const double pR = dmax(e.gm1 * fma(-0.5, keR, uR[4]), e.p_floor);
-    const double aL = fabs(vL) + eos_sqrt((e.gamma * pL) * invL);
-    const double aR = fabs(vR) + eos_sqrt((e.gamma * pR) * invR);
-    a = dmax(aL, aR);
+    // Davis bound max(|v_L|, |v_R|) + max(c_L, c_R), one square root per face
+    a = dmax(fabs(vL), fabs(vR)) + eos_sqrt(dmax((e.gamma * pL) * invL, (e.gamma * pR) * invR));
     F[0] = kt2(a, uL[0], uR[0], uL[1], uR[1]);
     F[1] = kt2(a, uL[1], uR[1], fma(uL[1], vL, pL), fma(uR[1], vR, pR));
     F[2] = kt2(a, uL[2], uR[2], uL[2] * vL, uR[2] * vR);
@@ -501,6 +525,10 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         for (int k = 0; k < kFA; ++k) recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         double vL, vR, a;
         kt_face(c.e, uL, uR, Fp, vL, vR, a);
+        if (TS_SMEM_FP) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) c.fps[k * kPencils + t] = Fp[k];
+        }
         if (NF > kFA) {
             c.cache[(0 * 3 + 0) * kPencils + t] = vL;
             c.cache[(0 * 3 + 1) * kPencils + t] = vR;
@@ -511,7 +539,8 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
             for (int k = 0; k < kFA; ++k) rf_store(c.rf_lo, fm[k], c.rf_cell, Fp[k]);
         }
     }
-#pragma unroll FaceUnroll<RECON>::value
+    constexpr int kUnroll = ((TS_UNROLL_MODES >> MODE) & 1) ? 2 : FaceUnroll<RECON>::value;
+#pragma unroll kUnroll
     for (int j = 1; j < kFaces; ++j) {
         const double* next = next_addr<RECON, SM>(p, j);
         if (TS_PF_L1 != 0 && ((TS_PF_L1_MODES >> MODE) & 1) && !SM) {
@@ -545,8 +574,17 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         }
         const int o = p.base + (j - 1) * p.ss;
         double out[kFA];
+        if (TS_SMEM_FP) {
 #pragma unroll
-        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+            for (int k = 0; k < kFA; ++k) {
+                const double fq = c.fps[k * kPencils + t];
+                c.fps[k * kPencils + t] = F[k];
+                out[k] = retire_m<MODE, STAGE>(c, fm[k], o, fq - F[k], up[k], un[k]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+        }
         if (STAGE == 3 && MODE == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
             amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
         if (kUn && !TS_UN_LATE) {
@@ -554,8 +592,10 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
             for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + jn * p.ss + fo[k]);
         }
+        if (!TS_SMEM_FP) {
 #pragma unroll
-        for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
+            for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
+        }
     }
     if (NF > kFA) {
         // passive species: same march, transported with the hydro face data
@@ -649,11 +689,12 @@ __device__ __forceinline__ void sweep_pair(const StageCtx& c, const Pencil& p, c
         const double v = S1 * inv;
         const double ke = fma(S1, v, fma(S2, S2 * inv, S3 * (S3 * inv)));
         const double pr = dmax(c.e.gm1 * fma(-0.5, ke, S4), c.e.p_floor);
-        const double as = fabs(v) + eos_sqrt((c.e.gamma * pr) * inv);
-        const double vo = xlane(v), po = xlane(pr), ao = xlane(as);
+        const double c2 = (c.e.gamma * pr) * inv;
+        const double vo = xlane(v), po = xlane(pr), c2o = xlane(c2);
         const double vL = role ? vo : v, vR = role ? v : vo;
         const double pL = role ? po : pr, pR = role ? pr : po;
-        const double a = dmax(role ? ao : as, role ? as : ao);
+        // Davis bound, as kt_face: both lanes take the one square root
+        const double a = dmax(fabs(vL), fabs(vR)) + eos_sqrt(dmax(role ? c2o : c2, role ? c2 : c2o));
         // physical fluxes of the own fields
         //   role 0: (s_n, fma(s_n, v, p), s_t1 v)      role 1: (s_t2 v, (E + p) v, tau v)
         const double fL0 = role ? uL[0] * vL : uL[1];
@@ -923,7 +964,7 @@ constexpr size_t stage_smem_bytes() {
 // instantiation so the uniform kernels carry none of its state (measured: the
 // register-pressed nf 11 kernel lost 4.5 % with it).
 template <int NF, int RECON, int STAGE, bool RF>
-__global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_kernel(const __grid_constant__ StageArgs A) {
+__global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) stage_kernel(const __grid_constant__ StageArgs A) {
     extern __shared__ __align__(16) double smem_raw[];
 #if TS_TMA
     double* smem = reinterpret_cast<double*>(
@@ -942,6 +983,18 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
         const int gp = A.list_inline_n > 0 ? A.list_inline[blockIdx.x]
                        : (A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x);
         prefetch_l2(A.Un + (size_t)gp * NF * NC, (unsigned)(NF * NC * sizeof(double)));
+    }
+#endif
+#if TS_PF_AHEAD > 0
+    // L2 prefetch of U^(k-1) of the sub-grid a CTA of the next wave will
+    // take (and its x neighbours, adjacent in memory: TS_PF_SPAN = 3)
+    if (threadIdx.x == 32 && A.list_inline_n == 0 && A.list == nullptr && A.n_local > 0) {
+        const long long ga = (long long)A.first + blockIdx.x + TS_PF_AHEAD - (TS_PF_SPAN > 1 ? 1 : 0);
+        const long long lo = ga < 0 ? 0 : ga;
+        long long hi = ga + TS_PF_SPAN;
+        if (hi > A.n_local) hi = A.n_local;
+        if (hi > lo)
+            prefetch_l2(A.Uprev + lo * NF * NC, (unsigned)((hi - lo) * NF * NC * sizeof(double)));
     }
 #endif
     if (A.cta_log != nullptr && threadIdx.x == 0) {
@@ -1052,6 +1105,7 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF)) stage_ker
     c.Uout = A.Uout;
     c.dU = smem;
     c.cache = smem + StageSmem<NF>::dU;
+    c.fps = smem + StageSmem<NF>::dU + StageSmem<NF>::cache;
     c.own = (size_t)g * NF * NC;
     c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
     __shared__ int scr_slot;
@@ -1261,6 +1315,11 @@ inline cudaError_t launch_stage_rf(const StageArgs& a, int n_ctas, cudaStream_t 
         e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
         if (e != cudaSuccess) return e;
+#if TS_CARVEOUT >= 0
+        e = cudaFuncSetAttribute(stage_kernel<NF, RECON, STAGE, RF>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 TS_CARVEOUT);
+        if (e != cudaSuccess) return e;
+#endif
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     if (!pdl) {
