@@ -64,6 +64,9 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 #define TS_SMEM_FP 0
 #endif
 // sweeps (bit = mode) whose face march is unrolled by 2 regardless of FaceUnroll
+#ifndef TS_SWP
+#define TS_SWP 0
+#endif
 #ifndef TS_PF_AHEAD
 #define TS_PF_AHEAD 0
 #endif
@@ -637,6 +640,100 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
     }
 }
 
+// Software-pipelined single-lane march (TS_SWP, nf = 6, PPM): iteration j
+// reconstructs face j's states while the EOS -> KT flux of face j-1 (whose
+// states the previous iteration produced) runs in the same basic block, so
+// ptxas can interleave the two-chain EOS (reciprocal -> pressure -> square
+// root, ~30 dependent FP64 operations) with the six independent limiter
+// chains of the next face.  Costs the 12 pending face states in registers.
+// Same arithmetic, operation by operation, as sweep() (bitwise).
+template <int NF, int RECON, int STAGE, int MODE, bool RF>
+__device__ __forceinline__ void sweep_swp(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
+    static_assert(NF == kFA && RECON == 0, "pipelined march: nf 6 PPM");
+    constexpr bool kUn = STAGE > 1 && MODE == 2;
+    int fo[kFA];
+#pragma unroll
+    for (int k = 0; k < kFA; ++k) fo[k] = fm[k] * NC;
+    Recon r[kFA];
+#pragma unroll
+    for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
+    const double* un_row = c.Un + c.own + p.base;
+    double un[kFA];
+    if (kUn) {
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + fo[k]);
+    }
+    double uL[kFA], uR[kFA], Fp[kFA];
+    {  // face 0's states
+        const double* next = next_addr<RECON>(p, 0);
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
+    }
+    {  // face 1's states || face 0's flux
+        const double* next = next_addr<RECON>(p, 1);
+        double nL[kFA], nR[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], nL[k], nR[k]);
+        double vL, vR, a;
+        kt_face(c.e, uL, uR, Fp, vL, vR, a);
+        if (RF && c.rf_lo != nullptr) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) rf_store(c.rf_lo, fm[k], c.rf_cell, Fp[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) {
+            uL[k] = nL[k];
+            uR[k] = nR[k];
+        }
+    }
+#pragma unroll 1
+    for (int j = 2; j < kFaces; ++j) {
+        // face j's states || face j-1's flux, retiring cell j-2
+        const double* next = next_addr<RECON>(p, j);
+        double up[kFA], nL[kFA], nR[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) {
+            up[k] = ld_pen<false>(paddr<false>(p, j - 2) + fo[k]);
+            recon_step<RECON>(next, fo[k], r[k], nL[k], nR[k]);
+        }
+        double F[kFA], vL, vR, a;
+        kt_face(c.e, uL, uR, F, vL, vR, a);
+        const int o = p.base + (j - 2) * p.ss;
+        double out[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+        if (STAGE == 3 && MODE == 2)
+            amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
+        if (kUn) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + (j - 1) * p.ss + fo[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) {
+            Fp[k] = F[k];
+            uL[k] = nL[k];
+            uR[k] = nR[k];
+        }
+    }
+    {  // face N's flux, retiring cell N-1
+        double up[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) up[k] = ld_pen<false>(paddr<false>(p, N - 1) + fo[k]);
+        double F[kFA], vL, vR, a;
+        kt_face(c.e, uL, uR, F, vL, vR, a);
+        if (RF && c.rf_hi != nullptr) {
+#pragma unroll
+            for (int k = 0; k < kFA; ++k) rf_store(c.rf_hi, fm[k], c.rf_cell, F[k]);
+        }
+        const int o = p.base + (N - 1) * p.ss;
+        double out[kFA];
+#pragma unroll
+        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
+        if (STAGE == 3 && MODE == 2)
+            amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
+    }
+}
+
 // Lane-pair march.  Lane role 0 owns (rho, s_n, s_t1), role 1 owns (s_t2, E,
 // tau) of the same pencil.  Per face: each lane advances its 3 fields, the
 // pair swaps the face states the other side needs (one shuffle round), role 0
@@ -1192,6 +1289,15 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
                 sweep_pair<NF, RECON, STAGE, 1, RF>(c, p, fm, amax);
             else
                 sweep_pair<NF, RECON, STAGE, 2, RF>(c, p, fm, amax);
+        } else if (TS_SWP && NF == kFA && RECON == 0) {
+            constexpr int R0 = NF == kFA ? RECON : 0;  // keeps the nf > 6 / PLM instantiations out of sweep_swp
+            constexpr int NF0 = NF == kFA ? NF : kFA;
+            if (axis == 0)
+                sweep_swp<NF0, R0 == 0 ? 0 : 0, STAGE, 0, RF>(c, p, fm, amax);
+            else if (axis == 1)
+                sweep_swp<NF0, 0, STAGE, 1, RF>(c, p, fm, amax);
+            else
+                sweep_swp<NF0, 0, STAGE, 2, RF>(c, p, fm, amax);
         } else if (axis == 0)
             sweep<NF, RECON, STAGE, 0, RF>(c, p, fm, amax);
         else if (axis == 1)
