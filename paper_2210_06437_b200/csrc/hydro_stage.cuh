@@ -67,6 +67,9 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 #ifndef TS_SWP
 #define TS_SWP 0
 #endif
+#ifndef TS_REV_STAGES
+#define TS_REV_STAGES 0
+#endif
 #ifndef TS_PF_AHEAD
 #define TS_PF_AHEAD 0
 #endif
@@ -1050,6 +1053,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Launch slot -> position in the sub-grid list.  TS_REV_STAGES (bit s-1 =
+// stage s) walks a stage's list backwards, so it first reads what the
+// previous stage wrote last (still in L2) instead of the oldest lines.
+template <int STAGE>
+__device__ __forceinline__ int cta_slot() {
+    return ((TS_REV_STAGES >> (STAGE - 1)) & 1) ? (int)(gridDim.x - 1u - blockIdx.x) : (int)blockIdx.x;
+}
+
 // Dynamic shared memory of a stage CTA: the dU accumulator (TS_TMA: 1024-byte
 // aligned for the 128-byte swizzle, plus the mbarrier) and the nf > 6 cache.
 template <int NF>
@@ -1077,8 +1088,8 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
     // its use: measured (ncu source view) as the z sweep's long-scoreboard
     // stall in stages 2 and 3.  Ask L2 for all of it now.
     if (STAGE > 1 && threadIdx.x == 32) {
-        const int gp = A.list_inline_n > 0 ? A.list_inline[blockIdx.x]
-                       : (A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x);
+        const int gp = A.list_inline_n > 0 ? A.list_inline[cta_slot<STAGE>()]
+                       : (A.list != nullptr ? A.list[cta_slot<STAGE>()] : A.first + cta_slot<STAGE>());
         prefetch_l2(A.Un + (size_t)gp * NF * NC, (unsigned)(NF * NC * sizeof(double)));
     }
 #endif
@@ -1100,8 +1111,8 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
         A.cta_log[4 * blockIdx.x] = sm;
         A.cta_log[4 * blockIdx.x + 1] = globaltimer();
     }
-    const int g = A.list_inline_n > 0 ? A.list_inline[blockIdx.x]
-                  : (A.list != nullptr ? A.list[blockIdx.x] : A.first + (int)blockIdx.x);
+    const int g = A.list_inline_n > 0 ? A.list_inline[cta_slot<STAGE>()]
+                  : (A.list != nullptr ? A.list[cta_slot<STAGE>()] : A.first + cta_slot<STAGE>());
     const int t = threadIdx.x;
     // stage 1's once-per-step duties (see StageArgs::lead_g1)
     const bool lead = A.lead_g1 == 0 ? blockIdx.x == 0 : g == A.lead_g1 - 1;
