@@ -124,9 +124,13 @@ struct StageArgs {
     // cnt_done after its max atomics) and only then reads amax_in.  The max
     // slots form a ring of three: block 0 of stage 1 zeroes the slot two steps
     // ahead (amax_reset2) once the count is complete.
+    // With N ranks (fused P2P, dt gathered in stage 3's tail) the same chain
+    // holds, but dt is global: cnt_gather = 1 makes only the gathering last
+    // CTA count, by flow_n, once amax_global is written.
     const unsigned int* cnt_wait;
     unsigned int cnt_expect;
     unsigned int* cnt_done;
+    int cnt_gather;
     double* amax_reset2;
     int flow_n;                          // owned sub-grids (flag count); proxies are gated by the halo flags
     int pdl_trigger;

@@ -1365,12 +1365,12 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
             // barrier ordered before them) instead of a full fence + atomic
             if (A.flow_done != nullptr)
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.flow_done + g), "r"(A.flow_seq) : "memory");
-            if (STAGE == 3 && A.cnt_done != nullptr)
+            if (STAGE == 3 && A.cnt_done != nullptr && !A.cnt_gather)
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.cnt_done) : "memory");
 #else
             __threadfence();
             if (A.flow_done != nullptr) atomicExch(A.flow_done + g, A.flow_seq);
-            if (STAGE == 3 && A.cnt_done != nullptr) atomicAdd(A.cnt_done, 1u);
+            if (STAGE == 3 && A.cnt_done != nullptr && !A.cnt_gather) atomicAdd(A.cnt_done, 1u);
 #endif
         }
     }
@@ -1397,6 +1397,11 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
                     double g = A.gather_own[0];
                     for (int q = 1; q < A.push_n; ++q) g = fmax(g, A.gather_own[q]);
                     *A.amax_global = g;
+                    if (A.cnt_gather && A.cnt_done != nullptr) {
+                        // the next step's chained stage 1 reads amax_global after this count
+                        __threadfence();
+                        atomicAdd(A.cnt_done, (unsigned)A.flow_n);
+                    }
                 }
             }
         }

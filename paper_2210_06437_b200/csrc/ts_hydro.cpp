@@ -337,13 +337,16 @@ struct ts_hydro_ctx {
     bool flow = true;                 // single rank: stages 2, 3 as PDL dependents gated by per-sub-grid flags
     bool flow_chain = false;          // the last stream op was this call's stage 3: the next stage 1 may be a PDL dependent
     bool flow_steps = true;           // TS_HYDRO_FLOW_STEPS=0: stage 1 stays stream-ordered
+    bool mchain = true;               // TS_HYDRO_MCHAIN=0: N ranks keep stage 1 stream-ordered
     uint32_t* d_cnt3 = nullptr;       // finished stage-3 CTAs (monotonic)
     uint32_t cnt3_expect = 0;
-    // P2P dt all-reduce: a one-thread kernel between stage 3 and the next
-    // stage 1 (default) or the stage-3 tail (TS_HYDRO_DT=tail: every CTA
-    // counts out after a fence, the last one pushes).  Same-box A/B, Sedov
-    // 4096/GPU: kernel +0.7 % at 2 B200s, +0.2 % at 4.
-    bool dt_kernel = true;
+    // P2P dt all-reduce: in the stage-3 tail (default: every CTA counts out
+    // after a fence, the last one pushes and gathers, and the next step's
+    // stage 1 is chained behind it as a PDL dependent — StageArgs::cnt_gather)
+    // or a one-thread kernel between stage 3 and the next stage 1
+    // (TS_HYDRO_DT=kernel).  Same-box A/B, Sedov 4096/GPU at 2 B200s: tail +
+    // chain 7.51-7.52 G, kernel 7.38-7.39, tail without the chain 7.34-7.37.
+    bool dt_kernel = false;
     uint32_t flow_seq = 0;
     bool halo_pushed = false;         // proxies of U^n were pushed by the last stage 3 (flags of xseq)
     uint64_t halo_recv_mask = 0;      // ranks that push slabs to this one
@@ -841,11 +844,10 @@ int build_plans(ts_hydro_ctx* c, const int64_t* nbr, const int32_t* owner) {
     return TS_OK;
 }
 
-// Max-signal-speed slot of step s: with one rank a ring of three (stage 1 of
-// one step may run while the previous step's stage 3 still accumulates; see
-// StageArgs::cnt_wait), with N ranks the two-slot parity the exchanges use.
+// Max-signal-speed slot of step s: a ring of three (stage 1 of one step may
+// run while the previous step's stage 3 still accumulates; see
+// StageArgs::cnt_wait) — on one rank and, for the chained fused-P2P steps, on N.
 double* amax_slot(const ts_hydro_ctx* c, uint64_t s) {
-    if (c->world > 1) return c->d_scal + (s & 1);
     static constexpr int kRing[3] = {0, 1, 5};
     return c->d_scal + kRing[s % 3];
 }
@@ -1023,6 +1025,35 @@ int reduce_amax(ts_hydro_ctx* c, double* slot, cudaStream_t s) {
     return TS_OK;
 }
 
+// Device-side barrier of the ranks on stream `s` (P2P: one flag word per peer
+// on the dt-gather channel, no data; NCCL: an all-reduce of a scratch word).
+// ts_hydro_time_steps starts its clock behind it, so the host-side skew of the
+// ranks entering the call (a gloo barrier releases them tens of microseconds
+// apart) is not charged to the steps.
+int device_barrier(ts_hydro_ctx* c, cudaStream_t s) {
+    if (c->world <= 1) return TS_OK;
+    if (c->p2p) {
+        StreamMemOps& m = memops();
+        const uint32_t seq = ++c->aseq;
+        uint64_t others = 0;
+        for (int r = 0; r < c->world; ++r) {
+            if (r == c->rank) continue;
+            others |= 1ull << r;
+            if (m.write32(s, (CUdeviceptr)(c->pm[(size_t)r].flags + c->world + c->rank), seq,
+                          CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                return fail(c, TS_ECUDA, "cuStreamWriteValue32 to a peer flag failed");
+        }
+        TS_CUDA(c, tsh::launch_wait_flags(reinterpret_cast<const unsigned int*>(c->d_flags + c->world), others, seq,
+                                          c->h_clock + 1, c->wait_ns, s));
+        return TS_OK;
+    }
+    if (c->comm != nullptr && c->comm_size > 1) {
+        Nccl& n = nccl();
+        TS_NCCL(c, n.AllReduce(c->d_scal + 6, c->d_scal + 6, 1, ncclFloat64, ncclMax, c->comm, s));
+    }
+    return TS_OK;
+}
+
 int do_compute_dt(ts_hydro_ctx* c) {
     cudaStream_t s;
     int rc = ensure_stream(c, 0, &s);
@@ -1172,14 +1203,18 @@ int do_step(ts_hydro_ctx* c) {
     // neighbours stay gated by the halo flags, local ones by the stage flags.
     const bool flow = (!multi || fused_halo) && c->flow && c->d_flow != nullptr &&
                       c->n_owned <= 10 * 6 * (int64_t)c->sms;
+    // across the step boundary too (stage 1 a PDL dependent of stage 3): one
+    // rank, or N ranks whose dt is gathered in stage 3's tail (StageArgs::cnt_gather)
+    const bool mchain = fused_halo && !c->dt_kernel && c->mchain;
+    const bool steps = flow && c->flow_steps && (!multi || mchain);
     if (flow) ++c->flow_seq;
     for (int stage = 1; stage <= 3; ++stage) {
         tsh::StageArgs a = stage_args(c, stage);
         if (c->d_cta_log != nullptr) a.cta_log = c->d_cta_log + 4 * (size_t)(stage - 1) * (size_t)c->n_owned;
-        const bool chain = flow && !multi && c->flow_steps && c->flow_chain;
+        const bool chain = steps && c->flow_chain;
         if (stage == 1) {
             a.amax_reset = chain ? nullptr : amax_slot(c, c->steps_done + 1);
-            if (!multi) a.amax_reset2 = amax_slot(c, c->steps_done + 2);
+            if (!multi || mchain) a.amax_reset2 = amax_slot(c, c->steps_done + 2);
             a.dt_out = c->d_dt_hist + (c->steps_done % ts_hydro_ctx::kDtHist);
         }
         if (stage == 1 && c->h2d_arm) {
@@ -1212,8 +1247,7 @@ int do_step(ts_hydro_ctx* c) {
         }
         if (flow) {
             const size_t n = (size_t)c->n_owned;
-            const bool steps = !multi && c->flow_steps;  // stage 3 feeds the next stage 1 too
-            a.flow_seq = c->flow_seq;
+            a.flow_seq = c->flow_seq;  // `steps`: stage 3 feeds the next stage 1 too
             a.flow_wait_seq = c->flow_seq;
 #if defined(TS_CHECK) && TS_CHECK
             // detector self-test (check builds only): wait for the PREVIOUS
@@ -1232,6 +1266,7 @@ int do_step(ts_hydro_ctx* c) {
             }
             if (stage == 3 && steps) {
                 a.cnt_done = c->d_cnt3;
+                a.cnt_gather = multi ? 1 : 0;  // N ranks: the gathering CTA counts, once dt is global
                 c->cnt3_expect += (uint32_t)c->n_owned;
             }
         }
@@ -1277,7 +1312,7 @@ int do_step(ts_hydro_ctx* c) {
             // a stage that began with the copy-engine refresh waits on its
             // event in stream order; the others start in the previous tail
             rc = launch_stage_list(c, a, stage, c->d_order, c->n_owned, 0, 0, 0,
-                                   flow && stage > 1 && a.halo_wait != nullptr);
+                                   flow && (stage > 1 || chain) && a.halo_wait != nullptr);
             if (rc) return rc;
             c->halo_pushed = true;
             continue;
@@ -1311,7 +1346,7 @@ int do_step(ts_hydro_ctx* c) {
     }
     if (p2p) {
         if (c->dt_kernel) {
-            TS_CUDA(c, tsh::launch_dt_exchange(c->d_scal + ((c->steps_done & 1) ^ 1),
+            TS_CUDA(c, tsh::launch_dt_exchange(amax_slot(c, c->steps_done + 1),
                                                c->d_push_gather + (size_t)(push_seq & 1) * c->world, c->d_push_flag,
                                                c->world, c->rank, push_seq,
                                                reinterpret_cast<const unsigned int*>(c->d_flags + c->world),
@@ -1324,7 +1359,7 @@ int do_step(ts_hydro_ctx* c) {
         c->amax_src = c->d_scal + 4;
         c->amax_n = 1;
     } else if (multi) {
-        double* slot = c->d_scal + ((c->steps_done & 1) ^ 1);
+        double* slot = amax_slot(c, c->steps_done + 1);
         TS_CUDA(c, cudaEventRecord(c->ev_in, s));
         TS_CUDA(c, cudaStreamWaitEvent(cs, c->ev_in, 0));
         rc = reduce_amax(c, slot, cs);
@@ -1334,7 +1369,7 @@ int do_step(ts_hydro_ctx* c) {
     } else {
         c->amax_src = nullptr;
     }
-    c->flow_chain = flow && !multi;
+    c->flow_chain = steps;
     c->steps_done++;
     return TS_OK;
 }
@@ -1733,7 +1768,8 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_HALO")) c->halo_fused = std::strcmp(w, "ce") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW_STEPS")) c->flow_steps = std::strcmp(w, "0") != 0;
-    if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "tail") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_MCHAIN")) c->mchain = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "kernel") == 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_E2E_WAVE")) c->e2e_wave = std::strcmp(w, "0") != 0;
@@ -2968,6 +3004,8 @@ int ts_hydro_time_steps(ts_hydro_ctx* c, uint64_t nsteps, double* ms) {
         rc = do_compute_dt(c);
         if (rc) return rc;
     }
+    rc = device_barrier(c, s);
+    if (rc) return rc;
     cudaEvent_t e0, e1;
     TS_CUDA(c, cudaEventCreate(&e0));
     TS_CUDA(c, cudaEventCreate(&e1));

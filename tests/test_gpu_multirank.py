@@ -32,14 +32,15 @@ def _port():
     return p
 
 
-def _torchrun(script_args, timeout, nproc=2):
+def _torchrun(script_args, timeout, nproc=2, env=None):
     """torchrun world `nproc` on 127.0.0.1; a rendezvous port taken between
     picking and binding it (EADDRINUSE) is retried with a fresh one."""
+    env = dict(os.environ, **(env or {}))
     for _ in range(3):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
                os.path.join(ROOT, "tools", "multigpu_check.py"), *script_args]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
         if "EADDRINUSE" not in r.stderr:
             return r
     return r
@@ -75,6 +76,19 @@ def test_two_ranks_on_one_gpu_bitwise_equal_to_single_rank(args, transport):
     if _gpus() < 1:
         pytest.skip("needs a GPU")
     r = _torchrun([*args, "--transport", transport, "--same-device"], 600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MULTIGPU OK" in r.stdout
+
+
+@pytest.mark.parametrize("env", [{"TS_HYDRO_DT": "kernel"}, {"TS_HYDRO_MCHAIN": "0"}])
+@pytest.mark.parametrize("args", SAME_DEVICE_MESHES[:2])
+def test_two_ranks_on_one_gpu_dt_variants(args, env):
+    """The default fused-P2P step gathers dt in stage 3's tail and chains the
+    next stage 1 behind it (StageArgs::cnt_gather); the one-thread dt kernel
+    and the unchained tail stay bitwise equal to one rank too."""
+    if _gpus() < 1:
+        pytest.skip("needs a GPU")
+    r = _torchrun([*args, "--transport", "p2p", "--same-device", "--steps", "5"], 600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTIGPU OK" in r.stdout
 
