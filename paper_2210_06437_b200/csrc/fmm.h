@@ -18,7 +18,7 @@ namespace tsh {
 constexpr int kFmmRMax = 3;         // interaction radius R (cells) 1..3: reach 2R+1 <= 7 < 8
 constexpr int kFmmRootK = 7;        // the root's table spans [-7, 7]^3
 constexpr int kFmmChunk = 64;       // a refined node's far sum: chunk sums of 64 entries (ORC_FMM_CHUNK)
-constexpr int kFmmSplitMax = 2048;  // (node, chunk) partial sums of one split M2L launch (scratch rows)
+constexpr int kFmmSplitMax = 4096;  // (node, chunk) partial sums of one split M2L launch (scratch rows, 168 MB)
 constexpr int kFmmNone = -1;        // nb27 code: no source (outside the domain)
 // nb27 code <= -2: the slot lies inside a coarser leaf, node id = -2 - code
 
@@ -93,6 +93,14 @@ cudaError_t launch_fmm_restrict(const FmmArgs& a, int n_ctas, cudaStream_t s);  
 // L2L + M2L of refined nodes a.first .. + n_nodes - 1 (one depth): (chunk,
 // node) CTAs + an in-order combine; n_nodes * chunks <= kFmmSplitMax
 cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s);
+// The halves of launch_fmm_m2l_split for a merged solve: one part launch over
+// the refined nodes of every depth (rows of a.part in launch order), then the
+// per-depth combines in root-first order (a.part offset to the depth's rows).
+cudaError_t launch_fmm_m2l_combine(const FmmArgs& a, int n_nodes, cudaStream_t s);
+// One part launch for the root (root_node >= 0, its table; rows after the
+// deeper ones) and n_nodes listed deeper nodes (a.table, a.list + a.first).
+cudaError_t launch_fmm_m2l_part_flat(const FmmArgs& a, int n_nodes, int root_node, const FmmEntry* root_tab,
+                                     int n_root_tab, cudaStream_t s);
 cudaError_t launch_fmm_leaf(const FmmArgs& a, int n_ctas, bool restricted, cudaStream_t s);  // leaves: L2L + near + far
 
 // Gravity source over dt on the first n sub-grids (dt_dev: the device's

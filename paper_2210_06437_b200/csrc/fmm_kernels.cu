@@ -201,10 +201,9 @@ __global__ void __launch_bounds__(NC) fmm_restrict_kernel(const __grid_constant_
 // in order (the oracle's contract), spread over CTAs: CTA (c, n) sums chunk c
 // of node first + n for all 512 cells into part[n][c]; the combine kernel
 // adds the parent's shifted expansion and the chunk sums in order.
-__global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant__ FmmArgs A) {
-    __shared__ int nb[27];
-    stamp_begin(A);
-    const int node = A.list != nullptr ? A.list[A.first + (int)blockIdx.y] : A.first + (int)blockIdx.y;
+// Chunk `chunk` of node `node`'s far sum over table `tab` for all 512 cells into row `o` of A.part.
+__device__ __forceinline__ void m2l_part_body(const FmmArgs& A, int node, int chunk, const FmmEntry* tab, int n_tab,
+                                              double* o, int* nb) {
     const int t = threadIdx.x;
     if (t < 27) nb[t] = A.nb27[27 * node + t];
     __syncthreads();
@@ -215,21 +214,48 @@ __global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant_
     const double xc[3] = {centre(I[0], h), centre(I[1], h), centre(I[2], h)};
     double phi = 0.0, g[3] = {0.0, 0.0, 0.0}, T[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const int sx = (I[0] & 1) ? -1 : 1, sy = (I[1] & 1) ? -1 : 1, sz = (I[2] & 1) ? -1 : 1;
-    const int k0 = (int)blockIdx.x * kFmmChunk, k1 = min(k0 + kFmmChunk, A.n_table);
+    const int k0 = chunk * kFmmChunk, k1 = min(k0 + kFmmChunk, n_tab);
     for (int k = k0; k < k1; ++k) {
-        const int4 u = __ldg(reinterpret_cast<const int4*>(A.table + k));
+        const int4 u = __ldg(reinterpret_cast<const int4*>(tab + k));
         const int J[3] = {I[0] + sx * u.x, I[1] + sy * u.y, I[2] + sz * u.z};
         double m, rho, c[3];
         if (source(A, nb, q, d, h, J, m, rho, c) == 0) continue;
         m2l<true>(A.G, m, c[0], c[1], c[2], xc[0], xc[1], xc[2], phi, g, T);
     }
-    double* o = A.part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 10 * NC + t;
+    o += t;
     o[0] = phi;
     o[NC] = g[0];
     o[2 * NC] = g[1];
     o[3 * NC] = g[2];
 #pragma unroll
     for (int k = 0; k < 6; ++k) o[(4 + k) * NC] = T[k];
+}
+
+__global__ void __launch_bounds__(NC) fmm_m2l_part_kernel(const __grid_constant__ FmmArgs A) {
+    __shared__ int nb[27];
+    stamp_begin(A);
+    const int node = A.list != nullptr ? A.list[A.first + (int)blockIdx.y] : A.first + (int)blockIdx.y;
+    m2l_part_body(A, node, (int)blockIdx.x, A.table, A.n_table,
+                  A.part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 10 * NC, nb);
+    stamp_end(A);
+}
+
+// One launch for the root's chunks (its own table; rows n_far_rows onward)
+// and every chunk of the listed deeper nodes (A.table; rows from 0): CTA i
+// < n_root_chunks takes root chunk i, the others (node, chunk) in row order.
+__global__ void __launch_bounds__(NC) fmm_m2l_part_flat_kernel(const __grid_constant__ FmmArgs A, int root_node,
+                                                               int n_root_chunks, const FmmEntry* root_tab,
+                                                               int n_root_tab, int n_far_chunks, int n_far_rows) {
+    __shared__ int nb[27];
+    stamp_begin(A);
+    const int i = (int)blockIdx.x;
+    if (i < n_root_chunks) {
+        m2l_part_body(A, root_node, i, root_tab, n_root_tab, A.part + (size_t)(n_far_rows + i) * 10 * NC, nb);
+    } else {
+        const int j = i - n_root_chunks;
+        const int node = A.list[A.first + j / n_far_chunks];
+        m2l_part_body(A, node, j % n_far_chunks, A.table, A.n_table, A.part + (size_t)j * 10 * NC, nb);
+    }
     stamp_end(A);
 }
 
@@ -500,6 +526,23 @@ cudaError_t launch_fmm_m2l_split(const FmmArgs& a, int n_nodes, cudaStream_t s) 
     const int n_chunks = (a.n_table + kFmmChunk - 1) / kFmmChunk;
     if (n_nodes <= 0 || n_chunks <= 0) return cudaSuccess;
     fmm_m2l_part_kernel<<<dim3(n_chunks, n_nodes), NC, 0, s>>>(a);
+    fmm_m2l_combine_kernel<<<dim3(n_nodes, 10), NC, 0, s>>>(a, n_chunks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fmm_m2l_part_flat(const FmmArgs& a, int n_nodes, int root_node, const FmmEntry* root_tab,
+                                     int n_root_tab, cudaStream_t s) {
+    const int n_far = (a.n_table + kFmmChunk - 1) / kFmmChunk;
+    const int n_root = root_node >= 0 ? (n_root_tab + kFmmChunk - 1) / kFmmChunk : 0;
+    const int n_ctas = n_root + n_nodes * n_far;
+    if (n_ctas <= 0) return cudaSuccess;
+    fmm_m2l_part_flat_kernel<<<n_ctas, NC, 0, s>>>(a, root_node, n_root, root_tab, n_root_tab, n_far, n_nodes * n_far);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fmm_m2l_combine(const FmmArgs& a, int n_nodes, cudaStream_t s) {
+    const int n_chunks = (a.n_table + kFmmChunk - 1) / kFmmChunk;
+    if (n_nodes <= 0 || n_chunks <= 0) return cudaSuccess;
     fmm_m2l_combine_kernel<<<dim3(n_nodes, 10), NC, 0, s>>>(a, n_chunks);
     return cudaGetLastError();
 }

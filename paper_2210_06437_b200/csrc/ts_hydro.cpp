@@ -338,6 +338,7 @@ struct ts_hydro_ctx {
     bool flow_chain = false;          // the last stream op was this call's stage 3: the next stage 1 may be a PDL dependent
     bool flow_steps = true;           // TS_HYDRO_FLOW_STEPS=0: stage 1 stays stream-ordered
     bool mchain = true;               // TS_HYDRO_MCHAIN=0: N ranks keep stage 1 stream-ordered
+    bool fmm_merge = true;            // TS_HYDRO_FMM_MERGE=0: one M2L part launch per depth
     uint32_t* d_cnt3 = nullptr;       // finished stage-3 CTAs (monotonic)
     uint32_t cnt3_expect = 0;
     // P2P dt all-reduce: in the stage-3 tail (default: every CTA counts out
@@ -1769,6 +1770,7 @@ int ts_hydro_create(const ts_hydro_config* cfg, ts_hydro_ctx** out) {
     if (const char* w = std::getenv("TS_HYDRO_FLOW")) c->flow = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_FLOW_STEPS")) c->flow_steps = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_MCHAIN")) c->mchain = std::strcmp(w, "0") != 0;
+    if (const char* w = std::getenv("TS_HYDRO_FMM_MERGE")) c->fmm_merge = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_DT")) c->dt_kernel = std::strcmp(w, "kernel") == 0;
     if (const char* w = std::getenv("TS_HYDRO_CHUNK_OVERLAP")) c->chunk_overlap = std::strcmp(w, "0") != 0;
     if (const char* w = std::getenv("TS_HYDRO_H2D_GATE")) c->h2d_gate = std::strcmp(w, "0") != 0;
@@ -3405,8 +3407,71 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
                          [&](int k) { return tsh::launch_fmm_restrict(a, k, s); })))
             return rc;
     }
-    // L2L + M2L, root first
+    // L2L + M2L, root first.  The depths below the root share one table, so
+    // when all their (node, chunk) rows fit the scratch their part sums are
+    // ONE launch (the shallow depths' few CTAs no longer run as launches of
+    // their own) and only the in-order combines stay per depth.
+    int merged_rows = 0, merged_nodes = 0;
+    if (t.max_depth > 2) {
+        if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
+        const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
+        for (int d = 1; d < t.max_depth; ++d) merged_nodes += c->fmm_m2l_count[(size_t)d];
+        merged_rows = merged_nodes * n_chunks;
+        // room left for the root's rows (one node, the root table's chunks)
+        int root_rows = 0;
+        if (c->fmm_m2l_count[0] > 0) {
+            const tsh::FmmEntry* rt = nullptr;
+            int n_rt = 0;
+            if ((rc = fmm_table_dev(c, radius, true, true, &rt, &n_rt))) return rc;
+            root_rows = c->fmm_m2l_count[0] * ((n_rt + tsh::kFmmChunk - 1) / tsh::kFmmChunk);
+        }
+        if (c->fmm_merge && merged_rows + root_rows <= tsh::kFmmSplitMax && merged_nodes > 0) {
+            // the root's chunks ride in the same launch (its own table, rows after the deeper ones)
+            const tsh::FmmEntry* rt = nullptr;
+            int n_rt = 0;
+            if ((rc = fmm_table_dev(c, radius, true, true, &rt, &n_rt))) return rc;
+            if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
+            const int root_node = c->fmm_m2l_count[0] > 0 ? t.int_first[0] : -1;
+            a.list = c->d_fmm_lists;
+            a.first = c->fmm_m2l_first[1];
+            a.part = c->d_fmm_part;
+            if ((rc = launch(kNameMultipole, merged_nodes, [&](int k) {
+                     return tsh::launch_fmm_m2l_part_flat(a, k, root_node, rt, n_rt, s);
+                 })))
+                return rc;
+            a.list = nullptr;
+        } else {
+            merged_nodes = 0;
+        }
+    }
     for (int d = 0; d < t.max_depth; ++d) {
+        if (d == 0 && merged_nodes > 0) {
+            // the root's chunk sums (from the merged launch): combine only
+            if ((rc = fmm_table_dev(c, radius, true, true, &a.table, &a.n_table))) return rc;
+            a.list = c->d_fmm_lists;
+            a.first = c->fmm_m2l_first[0];
+            a.part = c->d_fmm_part + (size_t)merged_rows * 10 * kNC;
+            if ((rc = launch(kNameMultipoleRoot, c->fmm_m2l_count[0],
+                             [&](int k) { return tsh::launch_fmm_m2l_combine(a, k, s); })))
+                return rc;
+            a.part = c->d_fmm_part;
+            a.list = nullptr;
+            continue;
+        }
+        if (d > 0 && merged_nodes > 0) {
+            // this depth's chunk sums are rows (node index in the merged launch) * n_chunks onward
+            if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
+            const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
+            const int nn = c->fmm_m2l_count[(size_t)d];
+            a.list = c->d_fmm_lists;
+            a.first = c->fmm_m2l_first[(size_t)d];
+            a.part = c->d_fmm_part + (size_t)(a.first - c->fmm_m2l_first[1]) * n_chunks * 10 * kNC;
+            if ((rc = launch(kNameMultipole, nn, [&](int k) { return tsh::launch_fmm_m2l_combine(a, k, s); })))
+                return rc;
+            a.part = c->d_fmm_part;
+            a.list = nullptr;
+            continue;
+        }
         if ((rc = fmm_table_dev(c, radius, d == 0, true, &a.table, &a.n_table))) return rc;
         // each node's chunks spread over CTAs + an in-order combine, in
         // batches of nodes whose chunk sums fit the scratch (84 MB).  Measured
@@ -3417,9 +3482,12 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
         // them on one rank)
         const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
         const int nn = c->fmm_m2l_count[(size_t)d];
-        const int batch = std::max(1, tsh::kFmmSplitMax / n_chunks);
+        // (the root, with merged deeper parts: the rows after theirs)
+        const int free_rows = tsh::kFmmSplitMax - (merged_nodes > 0 ? merged_rows : 0);
+        const int batch = std::max(1, free_rows / n_chunks);
         const int first = c->fmm_m2l_first[(size_t)d];
         a.list = c->d_fmm_lists;
+        a.part = c->d_fmm_part + (size_t)(merged_nodes > 0 ? merged_rows : 0) * 10 * kNC;
         if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, nn, [&](int k) {
                  cudaError_t e = cudaSuccess;
                  for (int b = 0; b < k && e == cudaSuccess; b += batch) {
@@ -3430,6 +3498,7 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
              })))
             return rc;
         a.list = nullptr;
+        a.part = c->d_fmm_part;
     }
     // leaves: the root alone, or the p2p / p2m lists
     if (t.root_leaf >= 0) {
