@@ -60,21 +60,9 @@ constexpr int kPencils = 64;  // pencils per sweep of one sub-grid
 #ifndef TS_PREFETCH
 #define TS_PREFETCH 1
 #endif
-#ifndef TS_SMEM_FP
-#define TS_SMEM_FP 0
-#endif
 // sweeps (bit = mode) whose face march is unrolled by 2 regardless of FaceUnroll
-#ifndef TS_SWP
-#define TS_SWP 0
-#endif
 #ifndef TS_REV_STAGES
 #define TS_REV_STAGES 0
-#endif
-#ifndef TS_PF_AHEAD
-#define TS_PF_AHEAD 0
-#endif
-#ifndef TS_PF_SPAN
-#define TS_PF_SPAN 1
 #endif
 #ifndef TS_UNROLL_MODES
 #define TS_UNROLL_MODES 0
@@ -150,10 +138,7 @@ struct StageSmem {
     // so the CTA's shared memory stays small enough for 4 resident CTAs.
     static constexpr int dU = (NF > kFA ? kFA : NF) * NC;
     static constexpr int cache = NF > kFA ? kFaces * 3 * kPencils : 0;  // (vL, vR, a) per face
-    // TS_SMEM_FP: the previous face's fluxes of the single-lane march, one
-    // private slot per (field, pencil) instead of 12 loop-carried registers
-    static constexpr int fp = (TS_SMEM_FP && !Lanes<NF>::pair) ? kFA * kPencils : 0;
-    static constexpr int doubles = dU + cache + fp;
+    static constexpr int doubles = dU + cache;
 };
 
 // TS_TMA: the own sub-grid's U^(k-1) (the 6 marched fields) is staged into
@@ -402,7 +387,6 @@ struct StageCtx {
     double* __restrict__ dU;     // shared accumulator
 #endif
     double* __restrict__ cache;  // shared (vL, vR, a) per face, NF > 6
-    double* __restrict__ fps;    // TS_SMEM_FP: previous-face flux slots [field][pencil]
     size_t own;                  // element offset of the sub-grid's field 0
     double dtdx;                 // 0.5 dt/dx: fluxes are carried doubled (kt2)
     EosParams e;
@@ -531,10 +515,6 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         for (int k = 0; k < kFA; ++k) recon_step<RECON, SM>(next, fo[k], r[k], uL[k], uR[k]);
         double vL, vR, a;
         kt_face(c.e, uL, uR, Fp, vL, vR, a);
-        if (TS_SMEM_FP) {
-#pragma unroll
-            for (int k = 0; k < kFA; ++k) c.fps[k * kPencils + t] = Fp[k];
-        }
         if (NF > kFA) {
             c.cache[(0 * 3 + 0) * kPencils + t] = vL;
             c.cache[(0 * 3 + 1) * kPencils + t] = vR;
@@ -580,17 +560,8 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
         }
         const int o = p.base + (j - 1) * p.ss;
         double out[kFA];
-        if (TS_SMEM_FP) {
 #pragma unroll
-            for (int k = 0; k < kFA; ++k) {
-                const double fq = c.fps[k * kPencils + t];
-                c.fps[k * kPencils + t] = F[k];
-                out[k] = retire_m<MODE, STAGE>(c, fm[k], o, fq - F[k], up[k], un[k]);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
-        }
+        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
         if (STAGE == 3 && MODE == 2)  // z sweep: fm = {rho, sz, sx, sy, E, tau}
             amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
         if (kUn && !TS_UN_LATE) {
@@ -598,10 +569,8 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
 #pragma unroll
             for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + jn * p.ss + fo[k]);
         }
-        if (!TS_SMEM_FP) {
 #pragma unroll
-            for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
-        }
+        for (int k = 0; k < kFA; ++k) Fp[k] = F[k];
     }
     if (NF > kFA) {
         // passive species: same march, transported with the hydro face data
@@ -640,100 +609,6 @@ __device__ __forceinline__ void sweep(const StageCtx& c, const Pencil& p, const 
                 Fq = F;
             }
         }
-    }
-}
-
-// Software-pipelined single-lane march (TS_SWP, nf = 6, PPM): iteration j
-// reconstructs face j's states while the EOS -> KT flux of face j-1 (whose
-// states the previous iteration produced) runs in the same basic block, so
-// ptxas can interleave the two-chain EOS (reciprocal -> pressure -> square
-// root, ~30 dependent FP64 operations) with the six independent limiter
-// chains of the next face.  Costs the 12 pending face states in registers.
-// Same arithmetic, operation by operation, as sweep() (bitwise).
-template <int NF, int RECON, int STAGE, int MODE, bool RF>
-__device__ __forceinline__ void sweep_swp(const StageCtx& c, const Pencil& p, const int (&fm)[kFA], double& amax) {
-    static_assert(NF == kFA && RECON == 0, "pipelined march: nf 6 PPM");
-    constexpr bool kUn = STAGE > 1 && MODE == 2;
-    int fo[kFA];
-#pragma unroll
-    for (int k = 0; k < kFA; ++k) fo[k] = fm[k] * NC;
-    Recon r[kFA];
-#pragma unroll
-    for (int k = 0; k < kFA; ++k) recon_begin<RECON>(p, fo[k], r[k]);
-    const double* un_row = c.Un + c.own + p.base;
-    double un[kFA];
-    if (kUn) {
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + fo[k]);
-    }
-    double uL[kFA], uR[kFA], Fp[kFA];
-    {  // face 0's states
-        const double* next = next_addr<RECON>(p, 0);
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], uL[k], uR[k]);
-    }
-    {  // face 1's states || face 0's flux
-        const double* next = next_addr<RECON>(p, 1);
-        double nL[kFA], nR[kFA];
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) recon_step<RECON>(next, fo[k], r[k], nL[k], nR[k]);
-        double vL, vR, a;
-        kt_face(c.e, uL, uR, Fp, vL, vR, a);
-        if (RF && c.rf_lo != nullptr) {
-#pragma unroll
-            for (int k = 0; k < kFA; ++k) rf_store(c.rf_lo, fm[k], c.rf_cell, Fp[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) {
-            uL[k] = nL[k];
-            uR[k] = nR[k];
-        }
-    }
-#pragma unroll 1
-    for (int j = 2; j < kFaces; ++j) {
-        // face j's states || face j-1's flux, retiring cell j-2
-        const double* next = next_addr<RECON>(p, j);
-        double up[kFA], nL[kFA], nR[kFA];
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) {
-            up[k] = ld_pen<false>(paddr<false>(p, j - 2) + fo[k]);
-            recon_step<RECON>(next, fo[k], r[k], nL[k], nR[k]);
-        }
-        double F[kFA], vL, vR, a;
-        kt_face(c.e, uL, uR, F, vL, vR, a);
-        const int o = p.base + (j - 2) * p.ss;
-        double out[kFA];
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
-        if (STAGE == 3 && MODE == 2)
-            amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
-        if (kUn) {
-#pragma unroll
-            for (int k = 0; k < kFA; ++k) un[k] = ld_un(un_row + (j - 1) * p.ss + fo[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) {
-            Fp[k] = F[k];
-            uL[k] = nL[k];
-            uR[k] = nR[k];
-        }
-    }
-    {  // face N's flux, retiring cell N-1
-        double up[kFA];
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) up[k] = ld_pen<false>(paddr<false>(p, N - 1) + fo[k]);
-        double F[kFA], vL, vR, a;
-        kt_face(c.e, uL, uR, F, vL, vR, a);
-        if (RF && c.rf_hi != nullptr) {
-#pragma unroll
-            for (int k = 0; k < kFA; ++k) rf_store(c.rf_hi, fm[k], c.rf_cell, F[k]);
-        }
-        const int o = p.base + (N - 1) * p.ss;
-        double out[kFA];
-#pragma unroll
-        for (int k = 0; k < kFA; ++k) out[k] = retire_m<MODE, STAGE>(c, fm[k], o, Fp[k] - F[k], up[k], un[k]);
-        if (STAGE == 3 && MODE == 2)
-            amax = fmax(amax, cell_signal_speed(out[0], out[2], out[3], out[1], out[4], c.e));
     }
 }
 
@@ -1093,18 +968,6 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
         prefetch_l2(A.Un + (size_t)gp * NF * NC, (unsigned)(NF * NC * sizeof(double)));
     }
 #endif
-#if TS_PF_AHEAD > 0
-    // L2 prefetch of U^(k-1) of the sub-grid a CTA of the next wave will
-    // take (and its x neighbours, adjacent in memory: TS_PF_SPAN = 3)
-    if (threadIdx.x == 32 && A.list_inline_n == 0 && A.list == nullptr && A.n_local > 0) {
-        const long long ga = (long long)A.first + blockIdx.x + TS_PF_AHEAD - (TS_PF_SPAN > 1 ? 1 : 0);
-        const long long lo = ga < 0 ? 0 : ga;
-        long long hi = ga + TS_PF_SPAN;
-        if (hi > A.n_local) hi = A.n_local;
-        if (hi > lo)
-            prefetch_l2(A.Uprev + lo * NF * NC, (unsigned)((hi - lo) * NF * NC * sizeof(double)));
-    }
-#endif
     if (A.cta_log != nullptr && threadIdx.x == 0) {
         unsigned int sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -1213,7 +1076,6 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
     c.Uout = A.Uout;
     c.dU = smem;
     c.cache = smem + StageSmem<NF>::dU;
-    c.fps = smem + StageSmem<NF>::dU + StageSmem<NF>::cache;
     c.own = (size_t)g * NF * NC;
     c.scr = A.scratch != nullptr ? A.scratch + c.own : nullptr;
     __shared__ int scr_slot;
@@ -1300,15 +1162,6 @@ __global__ void __launch_bounds__(Lanes<NF>::threads, TS_MINB_FOR(NF, RECON)) st
                 sweep_pair<NF, RECON, STAGE, 1, RF>(c, p, fm, amax);
             else
                 sweep_pair<NF, RECON, STAGE, 2, RF>(c, p, fm, amax);
-        } else if (TS_SWP && NF == kFA && RECON == 0) {
-            constexpr int R0 = NF == kFA ? RECON : 0;  // keeps the nf > 6 / PLM instantiations out of sweep_swp
-            constexpr int NF0 = NF == kFA ? NF : kFA;
-            if (axis == 0)
-                sweep_swp<NF0, R0 == 0 ? 0 : 0, STAGE, 0, RF>(c, p, fm, amax);
-            else if (axis == 1)
-                sweep_swp<NF0, 0, STAGE, 1, RF>(c, p, fm, amax);
-            else
-                sweep_swp<NF0, 0, STAGE, 2, RF>(c, p, fm, amax);
         } else if (axis == 0)
             sweep<NF, RECON, STAGE, 0, RF>(c, p, fm, amax);
         else if (axis == 1)
