@@ -3408,29 +3408,30 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
             return rc;
     }
     // L2L + M2L, root first.  The depths below the root share one table, so
-    // when all their (node, chunk) rows fit the scratch their part sums are
+    // the part sums of the root and of depths 1 .. merged_depth — the deepest
+    // run of depths whose (node, chunk) rows fit the scratch together — are
     // ONE launch (the shallow depths' few CTAs no longer run as launches of
-    // their own) and only the in-order combines stay per depth.
-    int merged_rows = 0, merged_nodes = 0;
-    if (t.max_depth > 2) {
+    // their own); their combines stay per depth, in order; deeper depths (a
+    // tree too big for the scratch) keep the per-depth batches.
+    int merged_rows = 0, merged_depth = 0;
+    if (c->fmm_merge && t.max_depth > 2) {
+        const tsh::FmmEntry* rt = nullptr;
+        int n_rt = 0;
+        if ((rc = fmm_table_dev(c, radius, true, true, &rt, &n_rt))) return rc;
         if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
         const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
-        for (int d = 1; d < t.max_depth; ++d) merged_nodes += c->fmm_m2l_count[(size_t)d];
-        merged_rows = merged_nodes * n_chunks;
-        // room left for the root's rows (one node, the root table's chunks)
-        int root_rows = 0;
-        if (c->fmm_m2l_count[0] > 0) {
-            const tsh::FmmEntry* rt = nullptr;
-            int n_rt = 0;
-            if ((rc = fmm_table_dev(c, radius, true, true, &rt, &n_rt))) return rc;
-            root_rows = c->fmm_m2l_count[0] * ((n_rt + tsh::kFmmChunk - 1) / tsh::kFmmChunk);
+        const int root_rows = c->fmm_m2l_count[0] * ((n_rt + tsh::kFmmChunk - 1) / tsh::kFmmChunk);
+        int rows = 0;
+        for (int d = 1; d < t.max_depth; ++d) {
+            const int r = rows + c->fmm_m2l_count[(size_t)d] * n_chunks;
+            if (r + root_rows > tsh::kFmmSplitMax) break;
+            rows = r;
+            merged_depth = d;
         }
-        if (c->fmm_merge && merged_rows + root_rows <= tsh::kFmmSplitMax && merged_nodes > 0) {
+        if (merged_depth >= 2 && rows > 0) {
             // the root's chunks ride in the same launch (its own table, rows after the deeper ones)
-            const tsh::FmmEntry* rt = nullptr;
-            int n_rt = 0;
-            if ((rc = fmm_table_dev(c, radius, true, true, &rt, &n_rt))) return rc;
-            if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
+            merged_rows = rows;
+            const int merged_nodes = rows / n_chunks;
             const int root_node = c->fmm_m2l_count[0] > 0 ? t.int_first[0] : -1;
             a.list = c->d_fmm_lists;
             a.first = c->fmm_m2l_first[1];
@@ -3441,11 +3442,11 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
                 return rc;
             a.list = nullptr;
         } else {
-            merged_nodes = 0;
+            merged_depth = 0;
         }
     }
     for (int d = 0; d < t.max_depth; ++d) {
-        if (d == 0 && merged_nodes > 0) {
+        if (d == 0 && merged_depth > 0) {
             // the root's chunk sums (from the merged launch): combine only
             if ((rc = fmm_table_dev(c, radius, true, true, &a.table, &a.n_table))) return rc;
             a.list = c->d_fmm_lists;
@@ -3458,7 +3459,7 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
             a.list = nullptr;
             continue;
         }
-        if (d > 0 && merged_nodes > 0) {
+        if (d > 0 && d <= merged_depth) {
             // this depth's chunk sums are rows (node index in the merged launch) * n_chunks onward
             if ((rc = fmm_table_dev(c, radius, false, true, &a.table, &a.n_table))) return rc;
             const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
@@ -3482,12 +3483,12 @@ int ts_hydro_gravity_fmm(ts_hydro_ctx* c, double G, int32_t radius, uint32_t str
         // them on one rank)
         const int n_chunks = (a.n_table + tsh::kFmmChunk - 1) / tsh::kFmmChunk;
         const int nn = c->fmm_m2l_count[(size_t)d];
-        // (the root, with merged deeper parts: the rows after theirs)
-        const int free_rows = tsh::kFmmSplitMax - (merged_nodes > 0 ? merged_rows : 0);
-        const int batch = std::max(1, free_rows / n_chunks);
+        // (depths below the merged ones: the merged rows were consumed by
+        // their combines, earlier on the stream, so the scratch is free again)
+        const int batch = std::max(1, tsh::kFmmSplitMax / n_chunks);
         const int first = c->fmm_m2l_first[(size_t)d];
         a.list = c->d_fmm_lists;
-        a.part = c->d_fmm_part + (size_t)(merged_nodes > 0 ? merged_rows : 0) * 10 * kNC;
+        a.part = c->d_fmm_part;
         if ((rc = launch(d == 0 ? kNameMultipoleRoot : kNameMultipole, nn, [&](int k) {
                  cudaError_t e = cudaSuccess;
                  for (int b = 0; b < k && e == cudaSuccess; b += batch) {
