@@ -244,3 +244,20 @@ def test_gravity_on_another_stream_is_ordered_before_the_next_step(hydro, oracle
     d.close()
     want = oracle_lib.gravity_fmm(6, np.zeros(m.n, np.int32), m.pos, m.dims, dx, U, radius=2, G=1.0)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("merge", ["0", "1"])
+@pytest.mark.parametrize("radius", [1, 3])
+def test_fmm_merged_and_per_depth_m2l_match_oracle(hydro, oracle_lib, monkeypatch, merge, radius):
+    """The M2L part sums of the root and the depths below it as ONE launch
+    (default; R = 3 merges only the depths that fit the scratch) or one launch
+    per depth (TS_HYDRO_FMM_MERGE=0): both bitwise to the oracle, on an 8^3
+    mesh (refined depths 0-2, so the merge spans two depths below the root)."""
+    monkeypatch.setenv("TS_HYDRO_FMM_MERGE", merge)
+    m = hydro.uniform_mesh(8, 8, 8)
+    dx = 1.0 / 64
+    lev = np.zeros(m.n, np.int32)
+    U = blob(lev, m.pos, dx, 6)
+    got, _ = fmm_gpu(hydro, lambda d: d.set_mesh(m), U, radius, dx=dx)
+    want = oracle_lib.gravity_fmm(6, lev, m.pos, m.dims, dx, U, radius=radius, G=1.3)
+    assert np.array_equal(got, want), f"max abs diff {np.abs(got - want).max():.3e}"
