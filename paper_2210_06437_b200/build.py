@@ -27,6 +27,7 @@ VARIANT = os.environ.get("TS_VARIANT", "")
 BUILD = os.path.join(PKG, "build" + (f"_{VARIANT}" if VARIANT else ""))
 LIB = os.path.join(PKG, "libts_hydro" + (f"_{VARIANT}" if VARIANT else "") + ".so")
 EXTRA = os.environ.get("TS_DEFINES", "").split()
+NVCC_EXTRA = os.environ.get("TS_NVCC_FLAGS", "").split()  # nvcc only (e.g. -Xptxas options)
 
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = shutil.which("nvcc") or os.path.join(CUDA_HOME, "bin", "nvcc")
@@ -54,7 +55,7 @@ def _compile(src: str, force: bool):
     if not force and not _stale(obj, src, _headers()):
         return obj, None
     if src.endswith(".cu"):
-        cmd = [NVCC, *NVCC_FLAGS, *EXTRA, "-c", src, "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, *EXTRA, *NVCC_EXTRA, "-c", src, "-o", obj]
     else:
         cmd = ["g++", *CXX_FLAGS, *EXTRA, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
